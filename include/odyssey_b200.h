@@ -1,0 +1,169 @@
+/*
+ * odyssey_b200.h -- C ABI of libodyssey_b200.so, the B200 (sm_100a) drop-in for the
+ * reference's W4A8 FastGEMM hot path.
+ *
+ * Part 1 re-declares, with IDENTICAL names, signatures, status codes and ownership
+ * rules, the hot-path subset of the reference ABI (/root/reference/proj/include/
+ * odyssey/odyssey.h).  A program linked against libodyssey.so for these calls links
+ * against libodyssey_b200.so unchanged; the work runs on the GPU, never on a CPU
+ * fallback.  Each declaration cites the reference declaration it replaces.
+ *
+ * Part 2 is the device-pointer, stream-ordered API underneath (the "thin C-ABI
+ * layer" of the north star): plain pointers, sizes and a cudaStream_t passed as
+ * void*, no torch types.  Part 3 holds the parity/inspection accessors the
+ * reference ABI lacks (ref odyssey.h:79-94 has no code/scale accessors).
+ *
+ * Conventions (ref odyssey.h:1-10): every call returns ody_status, ODY_OK == 0;
+ * on failure ody_last_error() returns a thread-local message; handles are opaque
+ * and released with their *_free function.
+ */
+#ifndef ODYSSEY_B200_H
+#define ODYSSEY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ================================================================ part 1 */
+
+/* ref odyssey.h:21-27 (+ ODY_EDEVICE: CUDA runtime / launch failure) */
+typedef enum ody_status {
+    ODY_OK = 0,
+    ODY_EINVAL = 1,
+    ODY_EIO = 2,
+    ODY_EPARSE = 3,
+    ODY_ENUMERIC = 4,
+    ODY_EDEVICE = 5,
+} ody_status;
+
+/* ref odyssey.h:29-34 */
+typedef enum ody_granularity {
+    ODY_PER_TENSOR = 0,
+    ODY_PER_CHANNEL = 1,
+    ODY_PER_TOKEN = 2,
+    ODY_PER_GROUP = 3,
+} ody_granularity;
+
+/* ref odyssey.h:36-42.  Only ODY_ENGINE_FAST runs here; the comparison engines
+ * return ODY_EINVAL ("not implemented on the B200 path"), never a CPU fallback. */
+typedef enum ody_engine {
+    ODY_ENGINE_W4A16 = 0,
+    ODY_ENGINE_FINEGRAINED = 1,
+    ODY_ENGINE_ASYMMETRIC = 2,
+    ODY_ENGINE_FAST = 3,
+    ODY_ENGINE_W8A8 = 4,
+} ody_engine;
+
+typedef struct ody_tensor ody_tensor;   /* ref odyssey.h:44 -- host row-major f32 */
+typedef struct ody_qtensor ody_qtensor; /* ref odyssey.h:45 -- device-resident codes+scales */
+
+/* ref odyssey.h:47-52 */
+typedef struct ody_gemm_counters {
+    uint64_t int8_mac_ops;
+    uint64_t dequant_events;
+    uint64_t zero_point_sub_ops;
+    uint64_t final_scale_ops;
+} ody_gemm_counters;
+
+const char* ody_last_error(void);                 /* ref odyssey.h:55 */
+void ody_string_free(char* s);                    /* ref odyssey.h:57 */
+void ody_set_threads(int n);                      /* ref odyssey.h:61 (host threads: no-op) */
+
+ody_status ody_tensor_create(size_t rows, size_t cols, const float* data,
+                             ody_tensor** out);   /* ref odyssey.h:65 */
+void ody_tensor_free(ody_tensor* t);              /* ref odyssey.h:66 */
+ody_status ody_tensor_dims(const ody_tensor* t, size_t* rows, size_t* cols); /* :67 */
+ody_status ody_tensor_data(const ody_tensor* t, const float** data);        /* :69 */
+
+void ody_qtensor_free(ody_qtensor* q);                                        /* :79 */
+ody_status ody_qtensor_dims(const ody_qtensor* q, size_t* rows, size_t* cols); /* :82 */
+
+/* ref odyssey.h:87-89.  Hot path: bits == 4, ODY_PER_CHANNEL (group_size ignored),
+ * optional per-row clip_gamma / clip_beta in (0,1].  Quantizes on the GPU straight
+ * into the kernel's prepacked tile layout. */
+ody_status ody_quantize_weights(const ody_tensor* w, int bits, ody_granularity granularity,
+                                size_t group_size, const float* clip_gamma,
+                                const float* clip_beta, ody_qtensor** out);
+
+/* ref odyssey.h:92 -- dynamic symmetric per-token INT8, on the GPU. */
+ody_status ody_quantize_activations(const ody_tensor* a, ody_qtensor** out);
+
+/* ref odyssey.h:94 */
+ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out);
+
+/* ref odyssey.h:120-121 -- ODY_ENGINE_FAST only; returns a new host f32 tensor. */
+ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q,
+                    const ody_qtensor* w_q, ody_gemm_counters* counters, ody_tensor** out);
+
+/* ================================================================ part 2 */
+
+typedef enum ody_dtype { ODY_DTYPE_F32 = 0, ODY_DTYPE_F16 = 1, ODY_DTYPE_BF16 = 2 } ody_dtype;
+
+/* Byte sizes of the device layouts (see paper_2311_09550_b200/csrc/layout.h). */
+size_t ody_dev_a8_bytes(size_t m, size_t k);          /* per-token INT8 codes, k-block layout */
+size_t ody_dev_w4_bytes(size_t n, size_t k);          /* prepacked INT4 tile layout */
+size_t ody_dev_workspace_bytes(size_t m, size_t n, size_t k); /* stream-K partial sums */
+
+/* K1 (replaces ref quantize.cpp:113-132): x is m x k row-major with row stride ldx
+ * elements; q receives ody_dev_a8_bytes(m,k) bytes, s receives m f32 scales.
+ * absmax_in (optional, m floats) overrides the row max -- row-parallel TP passes
+ * the all-reduced global max of a K-sharded row.  absmax_out (optional) exports it. */
+ody_status ody_dev_act_quant(const void* x, ody_dtype dtype, size_t ldx, size_t m, size_t k,
+                             void* q, float* s, const float* absmax_in, float* absmax_out,
+                             int pdl, void* stream);
+/* Row max|x| only (the local half of the row-parallel scale all-reduce). */
+ody_status ody_dev_row_absmax(const void* x, ody_dtype dtype, size_t ldx, size_t m, size_t k,
+                              float* absmax, void* stream);
+
+/* K2 (replaces ref quantize.cpp:75-111 per-channel, tensor.cpp:30-60 packing):
+ * w is n x k f32 on the device; writes ody_dev_w4_bytes(n,k) bytes and n scales.
+ * gamma/beta optional per-row device arrays. bits must be 4. */
+ody_status ody_dev_w4_quantize(const float* w, size_t n, size_t k, const float* gamma,
+                               const float* beta, void* w_packed, float* s_w, void* stream);
+/* K2 prepack only: reference flat PackedInt4Buffer bytes ((n*k+1)/2, element 2i low
+ * nibble) -> tile layout; and the inverse for export / parity. */
+ody_status ody_dev_w4_prepack(const void* flat_nibbles, size_t n, size_t k, void* w_packed,
+                              void* stream);
+ody_status ody_dev_w4_unpack(const void* w_packed, size_t n, size_t k, void* flat_nibbles,
+                             void* stream);
+
+/* K3+K4 (replaces ref gemm.cpp:229-279): out[i][j] = float((sum a*16w) >> 4) * (sa*sw).
+ * out (m x n row-major, out_dtype) and/or acc_out (m x n int32 pre-shift accumulators,
+ * ref gemm_w4a8_fast_accumulators) may be NULL but not both.  workspace must hold
+ * ody_dev_workspace_bytes(m,n,k) bytes, zeroed once (ody_dev_workspace_init); the
+ * kernel leaves it zeroed.  max_ctas 0 = all SMs.  Requires k <= 2^17. */
+ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_packed,
+                             const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                             void* out, int32_t* acc_out, void* workspace,
+                             size_t workspace_bytes, int max_ctas, int pdl, void* stream);
+ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream);
+
+/* Inspection: activation codes back to row-major int8 (and/or dequantized f32). */
+ody_status ody_dev_a8_unpack(const void* q, const float* s, size_t m, size_t k, int8_t* codes,
+                             float* dequant, void* stream);
+
+/* ================================================================ part 3 */
+
+/* Host copies of a qtensor's content in the REFERENCE layouts: activations ->
+ * m*k int8 codes; weights -> (n*k+1)/2 flat PackedInt4Buffer bytes; plus scales. */
+ody_status ody_qtensor_export(const ody_qtensor* q, void* codes_or_nibbles, float* scales);
+/* Build a weight qtensor from reference-layout packed nibbles + scales (e.g. an OTF
+ * payload.otf / scales.otf pair, ref otf.cpp:121-153). */
+ody_status ody_qtensor_import_w4(size_t n, size_t k, const void* flat_nibbles,
+                                 const float* scales, ody_qtensor** out);
+/* Build an activation qtensor from reference-layout int8 codes + scales. */
+ody_status ody_qtensor_import_a8(size_t m, size_t k, const int8_t* codes, const float* scales,
+                                 ody_qtensor** out);
+/* ref gemm.cpp:229-249: int32 accumulators before the >>4, m*n row-major. */
+ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q, int32_t* acc);
+/* Library/device identification, e.g. "libodyssey_b200 sm_100a NVIDIA B200 (148 SMs)". */
+const char* ody_b200_version(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* ODYSSEY_B200_H */

@@ -1,0 +1,194 @@
+"""Host-side mirror of the reference's hot-path interface, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(ref proj/src/core/quantize.hpp:31-34, gemm.hpp:70-85, capi.cpp:146-296):
+
+    quantize_activations_per_token(a)          -> QTensor   (per-token INT8, GPU)
+    quantize_weights(w, bits=4, per_channel)   -> QTensor   (per-channel INT4, GPU prepack)
+    gemm_w4a8_fast(a_q, w_q)                   -> f32 M x N (FastGEMM, GPU)
+    gemm_w4a8_fast_accumulators(a_q, w_q)      -> int32 M x N, before the >>4
+    run_engine(engine, a_dense, a_q, w_q)      -> only ENGINE_FAST; others raise EINVAL
+    dequantize(q)                              -> f32
+
+Every call goes through libodyssey_b200.so; numpy arrays are host buffers.  Errors
+raise :class:`OdyError` with the same status the reference ABI returns.
+"""
+from __future__ import annotations
+
+from ctypes import POINTER, byref, c_float, c_size_t, c_void_p
+
+import numpy as np
+
+from ._lib import (ODY_ENGINE_FAST, ODY_PER_CHANNEL, OdyError, check, lib,  # noqa: F401
+                   ody_gemm_counters)
+
+__all__ = ["Tensor", "QTensor", "quantize_activations_per_token", "quantize_weights",
+           "gemm_w4a8_fast", "gemm_w4a8_fast_accumulators", "run_engine", "dequantize",
+           "import_w4", "import_a8", "counters_fast", "OdyError"]
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(POINTER(c_float))
+
+
+class Tensor:
+    """ody_tensor: a host row-major f32 matrix (ref tensor.hpp:17-41)."""
+
+    def __init__(self, data, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            return
+        arr = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+        if arr.ndim != 2:
+            raise ValueError("Tensor expects a 2-D array")
+        h = c_void_p()
+        check(lib().ody_tensor_create(arr.shape[0], arr.shape[1], _fptr(arr), byref(h)))
+        self._h = h
+
+    @property
+    def shape(self):
+        r, c = c_size_t(), c_size_t()
+        check(lib().ody_tensor_dims(self._h, byref(r), byref(c)))
+        return (r.value, c.value)
+
+    def numpy(self) -> np.ndarray:
+        rows, cols = self.shape
+        p = POINTER(c_float)()
+        check(lib().ody_tensor_data(self._h, byref(p)))
+        if rows * cols == 0:
+            return np.zeros((rows, cols), np.float32)
+        return np.ctypeslib.as_array(p, shape=(rows, cols)).copy()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().ody_tensor_free(h)
+            self._h = None
+
+
+class QTensor:
+    """ody_qtensor: device-resident codes + scales in the kernel layouts."""
+
+    def __init__(self, handle, kind: str):
+        self._h = handle
+        self.kind = kind  # "a8" or "w4"
+
+    @property
+    def shape(self):
+        r, c = c_size_t(), c_size_t()
+        check(lib().ody_qtensor_dims(self._h, byref(r), byref(c)))
+        return (r.value, c.value)
+
+    def export(self):
+        """(codes, scales) in the REFERENCE layouts: a8 -> int8 [rows, cols];
+        w4 -> flat PackedInt4Buffer bytes ((rows*cols+1)//2,) (ref tensor.hpp:43-64)."""
+        rows, cols = self.shape
+        scales = np.empty(rows, np.float32)
+        if self.kind == "a8":
+            codes = np.empty((rows, cols), np.int8)
+        else:
+            codes = np.empty((rows * cols + 1) // 2, np.uint8)
+        check(lib().ody_qtensor_export(self._h, codes.ctypes.data_as(c_void_p),
+                                       scales.ctypes.data_as(c_void_p)))
+        return codes, scales
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().ody_qtensor_free(h)
+            self._h = None
+
+
+def _as_tensor(x) -> Tensor:
+    return x if isinstance(x, Tensor) else Tensor(x)
+
+
+def quantize_activations_per_token(a, bits: int = 8) -> QTensor:
+    """ref quantize.cpp:113-132 (INT8 only, as ody_quantize_activations)."""
+    if bits != 8:
+        raise OdyError(1, "quantize_activations_per_token: the C ABI quantizes INT8 only")
+    t = _as_tensor(a)
+    h = c_void_p()
+    check(lib().ody_quantize_activations(t._h, byref(h)))
+    return QTensor(h, "a8")
+
+
+def quantize_weights(w, bits: int = 4, granularity: int = ODY_PER_CHANNEL, group_size: int = 0,
+                     clip_gamma=None, clip_beta=None) -> QTensor:
+    """ref quantize.cpp:75-111 through ody_quantize_weights (capi.cpp:207-221)."""
+    t = _as_tensor(w)
+    g = b = None
+    if clip_gamma is not None:
+        g = np.ascontiguousarray(clip_gamma, np.float32)
+    if clip_beta is not None:
+        b = np.ascontiguousarray(clip_beta, np.float32)
+    h = c_void_p()
+    check(lib().ody_quantize_weights(t._h, bits, granularity, group_size,
+                                     _fptr(g) if g is not None else None,
+                                     _fptr(b) if b is not None else None, byref(h)))
+    return QTensor(h, "w4")
+
+
+def run_engine(engine: int, a_dense, a_q: QTensor | None, w_q: QTensor, with_counters=False):
+    """ref gemm.cpp:313-333 via ody_gemm; returns f32 [M, N] (and counters)."""
+    dense = _as_tensor(a_dense) if a_dense is not None else None
+    counters = ody_gemm_counters()
+    h = c_void_p()
+    check(lib().ody_gemm(engine, dense._h if dense else None, a_q._h if a_q else None, w_q._h,
+                         byref(counters), byref(h)))
+    out = Tensor(None, _handle=h).numpy()
+    if with_counters:
+        return out, {f: getattr(counters, f) for f, _ in ody_gemm_counters._fields_}
+    return out
+
+
+def gemm_w4a8_fast(a_q: QTensor, w_q: QTensor, with_counters=False):
+    """ref gemm.cpp:251-279."""
+    return run_engine(ODY_ENGINE_FAST, None, a_q, w_q, with_counters)
+
+
+def gemm_w4a8_fast_accumulators(a_q: QTensor, w_q: QTensor) -> np.ndarray:
+    """ref gemm.cpp:229-249: int32 sum a*(16w) per output, before the >>4."""
+    m, _ = a_q.shape
+    n, _ = w_q.shape
+    acc = np.empty((m, n), np.int32)
+    check(lib().ody_gemm_accumulators(a_q._h, w_q._h, acc.ctypes.data_as(c_void_p)))
+    return acc
+
+
+def dequantize(q: QTensor) -> np.ndarray:
+    """ref quantize.cpp:134-146 via ody_dequantize."""
+    h = c_void_p()
+    check(lib().ody_dequantize(q._h, byref(h)))
+    return Tensor(None, _handle=h).numpy()
+
+
+def import_w4(n: int, k: int, flat_nibbles: np.ndarray, scales: np.ndarray) -> QTensor:
+    """Reference-layout packed INT4 payload + scales -> device prepacked qtensor."""
+    flat = np.ascontiguousarray(flat_nibbles, np.uint8)
+    sc = np.ascontiguousarray(scales, np.float32)
+    if flat.size != (n * k + 1) // 2 or sc.size != n:
+        raise OdyError(1, "import_w4: payload or scales size mismatch")
+    h = c_void_p()
+    check(lib().ody_qtensor_import_w4(n, k, flat.ctypes.data_as(c_void_p),
+                                      sc.ctypes.data_as(c_void_p), byref(h)))
+    return QTensor(h, "w4")
+
+
+def import_a8(codes: np.ndarray, scales: np.ndarray) -> QTensor:
+    """Reference-layout per-token INT8 codes + scales -> device qtensor."""
+    c = np.ascontiguousarray(codes, np.int8)
+    sc = np.ascontiguousarray(scales, np.float32)
+    if c.ndim != 2 or sc.size != c.shape[0]:
+        raise OdyError(1, "import_a8: codes/scales shape mismatch")
+    h = c_void_p()
+    check(lib().ody_qtensor_import_a8(c.shape[0], c.shape[1], c.ctypes.data_as(c_void_p),
+                                      sc.ctypes.data_as(c_void_p), byref(h)))
+    return QTensor(h, "a8")
+
+
+def counters_fast(m: int, n: int, k: int) -> dict:
+    """The fast engine's counter formulas (ref gemm.cpp:270-272, test_gemm.cpp:262-267)."""
+    return {"int8_mac_ops": m * n * k, "dequant_events": m * n, "zero_point_sub_ops": 0,
+            "final_scale_ops": m * n}
+

@@ -1,0 +1,670 @@
+// capi.cu -- the C ABI of libodyssey_b200.so (include/odyssey_b200.h).
+//
+// Part 1 mirrors the reference's hot-path C ABI (ref proj/src/capi/capi.cpp:130-296):
+// same status mapping, thread-local last error, exceptions never cross the ABI
+// (ref capi.cpp:45-58), null arguments -> ODY_EINVAL before any work.  Behind it the
+// quantized operands live in HBM in the kernel layouts (layout.h); every arithmetic
+// step runs as an sm_100a kernel.  There is no CPU fallback: if the device or the
+// kernels are unavailable the call fails with ODY_EDEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/odyssey_b200.h"
+#include "kernels.h"
+#include "layout.h"
+
+using namespace odyb200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail : std::runtime_error {
+    ody_status code;
+    Fail(ody_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(ody_status c, const std::string& m) { throw Fail(c, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ODY_EDEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+ody_status guarded(Fn&& fn) {
+    try {
+        fn();
+        g_last_error.clear();
+        return ODY_OK;
+    } catch (const Fail& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of memory";
+        return ODY_EDEVICE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ODY_EINVAL;
+    }
+}
+
+ody_status einval(const char* msg) {
+    g_last_error = msg;
+    return ODY_EINVAL;
+}
+
+// ---------------------------------------------------------------- runtime
+// One library stream for the host-handle API; device memory from the stream-ordered
+// pool (cudaMallocAsync) so per-call temporaries cost no driver round trip.
+struct Runtime {
+    std::mutex mu;          // serialises host-API GEMMs (shared workspace)
+    cudaStream_t stream = nullptr;
+    void* workspace = nullptr;
+    size_t workspace_bytes = 0;
+    int sms = 0;
+    std::string version;
+};
+
+Runtime& rt() {
+    static Runtime* r = [] {
+        auto* x = new Runtime();
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+        if (prop.major != 10) {
+            fail(ODY_EDEVICE, "libodyssey_b200 needs an sm_100 (B200) device, found sm_" +
+                                  std::to_string(prop.major) + std::to_string(prop.minor));
+        }
+        x->sms = prop.multiProcessorCount;
+        cuda_check(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking), "stream");
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        char buf[256];
+        std::snprintf(buf, sizeof(buf), "libodyssey_b200 sm_100a %s (%d SMs)", prop.name,
+                      prop.multiProcessorCount);
+        x->version = buf;
+        return x;
+    }();
+    return *r;
+}
+
+// Pooled pinned host buffers back ody_tensor so H2D/D2H run at full PCIe rate and
+// repeated calls do not pay cudaHostAlloc.
+struct PinnedPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_list;
+    void* get(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        {
+            std::lock_guard<std::mutex> l(mu);
+            auto it = free_list.lower_bound(bytes);
+            if (it != free_list.end() && it->first <= 2 * bytes) {
+                void* p = it->second;
+                free_list.erase(it);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            p = std::malloc(bytes);  // still correct, just pageable
+            if (!p) throw std::bad_alloc();
+            return p;
+        }
+        std::lock_guard<std::mutex> l(mu);
+        sizes[p] = bytes;
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        std::lock_guard<std::mutex> l(mu);
+        auto it = sizes.find(p);
+        if (it == sizes.end()) {
+            std::free(p);
+            return;
+        }
+        free_list.emplace(it->second, p);
+    }
+    std::map<void*, size_t> sizes;
+};
+PinnedPool& pinned() {
+    static PinnedPool* p = new PinnedPool();
+    return *p;
+}
+
+template <typename T>
+struct DevBuf {  // stream-ordered device temporary
+    T* p = nullptr;
+    cudaStream_t st;
+    DevBuf(size_t count, cudaStream_t s) : st(s) {
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), s),
+                   "cudaMallocAsync");
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    T* release() {
+        T* q = p;
+        p = nullptr;
+        return q;
+    }
+};
+
+}  // namespace
+
+// ----------------------------------------------------------------- handles
+struct ody_tensor {
+    size_t rows = 0, cols = 0;
+    float* data = nullptr;  // pinned (pooled) host memory
+    ~ody_tensor() { pinned().put(data); }
+};
+
+enum class QKind { Act8, Weight4 };
+
+struct ody_qtensor {
+    QKind kind;
+    size_t rows = 0, cols = 0;
+    void* codes = nullptr;  // device, kernel layout
+    float* scales = nullptr;  // device
+    ~ody_qtensor() {
+        cudaStream_t st = rt().stream;
+        if (codes) cudaFreeAsync(codes, st);
+        if (scales) cudaFreeAsync(scales, st);
+    }
+};
+
+namespace {
+
+ody_tensor* new_tensor(size_t rows, size_t cols) {
+    auto* t = new ody_tensor();
+    t->rows = rows;
+    t->cols = cols;
+    t->data = static_cast<float*>(pinned().get(rows * cols * sizeof(float)));
+    return t;
+}
+
+void sync(cudaStream_t st, const char* what) {
+    cuda_check(cudaGetLastError(), what);
+    cuda_check(cudaStreamSynchronize(st), what);
+}
+
+void check_fast_inputs(const ody_qtensor* a_q, const ody_qtensor* w_q) {
+    // ref gemm.cpp:206-216
+    if (a_q->kind != QKind::Act8)
+        fail(ODY_EINVAL, "GEMM: activations must be symmetric per-token INT8");
+    if (w_q->kind != QKind::Weight4)
+        fail(ODY_EINVAL, "gemm_w4a8_fast: weights must be per-channel 4-bit");
+    if (a_q->cols != w_q->cols) fail(ODY_EINVAL, "gemm_w4a8_fast: inner dims disagree");
+    if (w_q->cols > kMaxK)
+        fail(ODY_EINVAL, "GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
+    if (a_q->rows > 0x7fffffff || w_q->rows > 0x7fffffff)
+        fail(ODY_EINVAL, "GEMM: dimension exceeds int32 range");
+}
+
+void run_gemm(const ody_qtensor* a_q, const ody_qtensor* w_q, float* out_dev, int32_t* acc_dev,
+              cudaStream_t st) {
+    Runtime& r = rt();
+    const size_t need = gemm_workspace_bytes(static_cast<int>(a_q->rows), static_cast<int>(w_q->rows),
+                                             static_cast<int>(w_q->cols), r.sms);
+    if (r.workspace_bytes < need) {
+        if (r.workspace) cuda_check(cudaFree(r.workspace), "cudaFree");
+        r.workspace = nullptr;
+        cuda_check(cudaMalloc(&r.workspace, need), "cudaMalloc workspace");
+        cuda_check(cudaMemset(r.workspace, 0, need), "cudaMemset workspace");
+        r.workspace_bytes = need;
+    }
+    GemmArgs g = {};
+    g.qa = static_cast<const int8_t*>(a_q->codes);
+    g.sa = a_q->scales;
+    g.wp = static_cast<const uint8_t*>(w_q->codes);
+    g.sw = w_q->scales;
+    g.out = out_dev;
+    g.out_dtype = kDtypeF32;
+    g.acc_out = acc_dev;
+    g.workspace = r.workspace;
+    g.workspace_bytes = r.workspace_bytes;
+    g.M = static_cast<int>(a_q->rows);
+    g.N = static_cast<int>(w_q->rows);
+    g.K = static_cast<int>(w_q->cols);
+    g.max_ctas = r.sms;
+    g.pdl = false;
+    cuda_check(launch_w4a8_gemm(g, st), "w4a8_gemm launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+// ================================================================ part 1
+const char* ody_last_error(void) { return g_last_error.c_str(); }
+
+void ody_string_free(char* s) { delete[] s; }
+
+void ody_set_threads(int n) { (void)n; }  // no host worker threads on the GPU path
+
+ody_status ody_tensor_create(size_t rows, size_t cols, const float* data, ody_tensor** out) {
+    if (!data || !out) return einval("ody_tensor_create: null argument");
+    return guarded([&] {
+        for (size_t i = 0; i < rows * cols; ++i) {  // ref tensor.cpp:21-27
+            if (!std::isfinite(data[i])) fail(ODY_EINVAL, "DenseTensor: non-finite value");
+        }
+        ody_tensor* t = new_tensor(rows, cols);
+        std::memcpy(t->data, data, rows * cols * sizeof(float));
+        *out = t;
+    });
+}
+
+void ody_tensor_free(ody_tensor* t) { delete t; }
+
+ody_status ody_tensor_dims(const ody_tensor* t, size_t* rows, size_t* cols) {
+    if (!t || !rows || !cols) return einval("ody_tensor_dims: null argument");
+    *rows = t->rows;
+    *cols = t->cols;
+    return ODY_OK;
+}
+
+ody_status ody_tensor_data(const ody_tensor* t, const float** data) {
+    if (!t || !data) return einval("ody_tensor_data: null argument");
+    *data = t->data;
+    return ODY_OK;
+}
+
+void ody_qtensor_free(ody_qtensor* q) {
+    if (!q) return;
+    try {
+        delete q;
+    } catch (...) {
+    }
+}
+
+ody_status ody_qtensor_dims(const ody_qtensor* q, size_t* rows, size_t* cols) {
+    if (!q || !rows || !cols) return einval("ody_qtensor_dims: null argument");
+    *rows = q->rows;
+    *cols = q->cols;
+    return ODY_OK;
+}
+
+ody_status ody_quantize_weights(const ody_tensor* w, int bits, ody_granularity granularity,
+                                size_t group_size, const float* clip_gamma,
+                                const float* clip_beta, ody_qtensor** out) {
+    if (!w || !out) return einval("ody_quantize_weights: null argument");
+    return guarded([&] {
+        // validation order of ref quantize.cpp:75-83 / tensor.cpp:86-110
+        if (w->rows * w->cols == 0) fail(ODY_EINVAL, "quantize_weights: empty tensor");
+        if (granularity != ODY_PER_CHANNEL && granularity != ODY_PER_GROUP)
+            fail(ODY_EINVAL, "quantize_weights: granularity must be per_channel or per_group");
+        if (bits != 4 && bits != 8) fail(ODY_EINVAL, "QuantScheme: bits must be 4 or 8");
+        if (granularity == ODY_PER_GROUP && (group_size == 0 || w->cols % group_size != 0))
+            fail(ODY_EINVAL, "QuantScheme: group size " + std::to_string(group_size) +
+                                 " does not divide axis length " + std::to_string(w->cols));
+        for (const float* arr : {clip_gamma, clip_beta}) {
+            if (!arr) continue;
+            for (size_t i = 0; i < w->rows; ++i)
+                if (!(arr[i] > 0.0f && arr[i] <= 1.0f))
+                    fail(ODY_EINVAL, std::string("QuantScheme: ") +
+                                         (arr == clip_gamma ? "clip_gamma" : "clip_beta") +
+                                         " outside (0,1]");
+        }
+        if (bits != 4 || granularity != ODY_PER_CHANNEL)
+            fail(ODY_EINVAL,
+                 "quantize_weights: the B200 FastGEMM path takes bits=4, per_channel weights");
+        if (w->rows > 0x7fffffff || w->cols > 0x7fffffff) fail(ODY_EINVAL, "quantize_weights: too large");
+        Runtime& r = rt();
+        cudaStream_t st = r.stream;
+        const size_t n = w->rows, k = w->cols;
+        DevBuf<float> wd(n * k, st);
+        cuda_check(cudaMemcpyAsync(wd.p, w->data, n * k * 4, cudaMemcpyHostToDevice, st), "H2D w");
+        DevBuf<float> gd(clip_gamma ? n : 0, st), bd(clip_beta ? n : 0, st);
+        if (clip_gamma) cuda_check(cudaMemcpyAsync(gd.p, clip_gamma, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+        if (clip_beta) cuda_check(cudaMemcpyAsync(bd.p, clip_beta, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+        DevBuf<uint8_t> packed(w4_packed_bytes(n, k), st);
+        DevBuf<float> scales(n, st);
+        DevBuf<int> err(1, st);
+        cuda_check(cudaMemsetAsync(err.p, 0, sizeof(int), st), "memset");
+        cuda_check(launch_w4_quant_prepack(wd.p, static_cast<int>(n), static_cast<int>(k), 4,
+                                           clip_gamma ? gd.p : nullptr, clip_beta ? bd.p : nullptr,
+                                           packed.p, scales.p, err.p, st),
+                   "w4 quantize launch");
+        int herr = 0;
+        cuda_check(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        sync(st, "ody_quantize_weights");
+        if (herr) fail(ODY_EINVAL, "compute_scale_symmetric: gamma/beta outside (0,1]");
+        auto* q = new ody_qtensor();
+        q->kind = QKind::Weight4;
+        q->rows = n;
+        q->cols = k;
+        q->codes = packed.release();
+        q->scales = scales.release();
+        *out = q;
+    });
+}
+
+ody_status ody_quantize_activations(const ody_tensor* a, ody_qtensor** out) {
+    if (!a || !out) return einval("ody_quantize_activations: null argument");
+    return guarded([&] {
+        if (a->rows * a->cols == 0)
+            fail(ODY_EINVAL, "quantize_activations_per_token: empty tensor");
+        if (a->rows > 0x7fffffff || a->cols > 0x7fffffff) fail(ODY_EINVAL, "too large");
+        Runtime& r = rt();
+        cudaStream_t st = r.stream;
+        const size_t m = a->rows, k = a->cols;
+        DevBuf<float> xd(m * k, st);
+        cuda_check(cudaMemcpyAsync(xd.p, a->data, m * k * 4, cudaMemcpyHostToDevice, st), "H2D a");
+        DevBuf<int8_t> q(a8_bytes(m, k), st);
+        DevBuf<float> s(m, st);
+        cuda_check(launch_act_quant(xd.p, kDtypeF32, k, static_cast<int>(m), static_cast<int>(k),
+                                    q.p, s.p, nullptr, nullptr, false, st),
+                   "act_quant launch");
+        sync(st, "ody_quantize_activations");
+        auto* qt = new ody_qtensor();
+        qt->kind = QKind::Act8;
+        qt->rows = m;
+        qt->cols = k;
+        qt->codes = q.release();
+        qt->scales = s.release();
+        *out = qt;
+    });
+}
+
+ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out) {
+    if (!q || !out) return einval("ody_dequantize: null argument");
+    return guarded([&] {
+        cudaStream_t st = rt().stream;
+        const size_t r = q->rows, c = q->cols;
+        DevBuf<float> d(r * c, st);
+        if (q->kind == QKind::Act8)
+            cuda_check(launch_a8_unpack(static_cast<const int8_t*>(q->codes), q->scales,
+                                        static_cast<int>(r), static_cast<int>(c), nullptr, d.p, st),
+                       "dequant launch");
+        else
+            cuda_check(launch_w4_dequant(static_cast<const uint8_t*>(q->codes), q->scales,
+                                         static_cast<int>(r), static_cast<int>(c), d.p, st),
+                       "dequant launch");
+        ody_tensor* t = new_tensor(r, c);
+        cudaError_t e = cudaMemcpyAsync(t->data, d.p, r * c * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            delete t;
+            cuda_check(e, "ody_dequantize");
+        }
+        *out = t;
+    });
+}
+
+ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q,
+                    const ody_qtensor* w_q, ody_gemm_counters* counters, ody_tensor** out) {
+    if (!w_q || !out) return einval("ody_gemm: null argument");
+    return guarded([&] {
+        // ref capi.cpp:276-283
+        if (engine < ODY_ENGINE_W4A16 || engine > ODY_ENGINE_W8A8)
+            fail(ODY_EINVAL, "bad engine enum");
+        if (engine == ODY_ENGINE_W4A16 && !a_dense)
+            fail(ODY_EINVAL, "ody_gemm: w4a16 engine needs a_dense");
+        if (engine != ODY_ENGINE_W4A16 && !a_q)
+            fail(ODY_EINVAL, "ody_gemm: engine needs quantized activations");
+        if (engine != ODY_ENGINE_FAST)
+            fail(ODY_EINVAL, "ody_gemm: only ODY_ENGINE_FAST is implemented on the B200 path");
+        check_fast_inputs(a_q, w_q);
+        Runtime& r = rt();
+        std::lock_guard<std::mutex> lock(r.mu);
+        cudaStream_t st = r.stream;
+        const size_t m = a_q->rows, n = w_q->rows, k = w_q->cols;
+        DevBuf<float> od(m * n, st);
+        run_gemm(a_q, w_q, od.p, nullptr, st);
+        ody_tensor* t = new_tensor(m, n);
+        cudaError_t e = cudaMemcpyAsync(t->data, od.p, m * n * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            delete t;
+            cuda_check(e, "ody_gemm");
+        }
+        if (counters) {  // ref gemm.cpp:270-272 -- analytic, identical to the CPU engine
+            counters->int8_mac_ops = static_cast<uint64_t>(m) * n * k;
+            counters->dequant_events = static_cast<uint64_t>(m) * n;
+            counters->zero_point_sub_ops = 0;
+            counters->final_scale_ops = static_cast<uint64_t>(m) * n;
+        }
+        *out = t;
+    });
+}
+
+// ================================================================ part 2
+size_t ody_dev_a8_bytes(size_t m, size_t k) { return a8_bytes(m, k); }
+size_t ody_dev_w4_bytes(size_t n, size_t k) { return w4_packed_bytes(n, k); }
+size_t ody_dev_workspace_bytes(size_t m, size_t n, size_t k) {
+    return gemm_workspace_bytes(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0);
+}
+
+ody_status ody_dev_act_quant(const void* x, ody_dtype dtype, size_t ldx, size_t m, size_t k,
+                             void* q, float* s, const float* absmax_in, float* absmax_out,
+                             int pdl, void* stream) {
+    if (!x || !q || !s) return einval("ody_dev_act_quant: null argument");
+    if (m == 0 || k == 0) return einval("quantize_activations_per_token: empty tensor");
+    if (ldx < k) return einval("ody_dev_act_quant: ldx < k");
+    return guarded([&] {
+        cuda_check(launch_act_quant(x, dtype, ldx, static_cast<int>(m), static_cast<int>(k),
+                                    static_cast<int8_t*>(q), s, absmax_in, absmax_out, pdl != 0,
+                                    static_cast<cudaStream_t>(stream)),
+                   "act_quant launch");
+    });
+}
+
+ody_status ody_dev_row_absmax(const void* x, ody_dtype dtype, size_t ldx, size_t m, size_t k,
+                              float* absmax, void* stream) {
+    if (!x || !absmax) return einval("ody_dev_row_absmax: null argument");
+    if (m == 0 || k == 0) return einval("ody_dev_row_absmax: empty tensor");
+    return guarded([&] {
+        cuda_check(launch_row_absmax(x, dtype, ldx, static_cast<int>(m), static_cast<int>(k), absmax,
+                                     static_cast<cudaStream_t>(stream)),
+                   "row_absmax launch");
+    });
+}
+
+ody_status ody_dev_w4_quantize(const float* w, size_t n, size_t k, const float* gamma,
+                               const float* beta, void* w_packed, float* s_w, void* stream) {
+    if (!w || !w_packed || !s_w) return einval("ody_dev_w4_quantize: null argument");
+    if (n == 0 || k == 0) return einval("quantize_weights: empty tensor");
+    return guarded([&] {
+        cuda_check(launch_w4_quant_prepack(w, static_cast<int>(n), static_cast<int>(k), 4, gamma,
+                                           beta, static_cast<uint8_t*>(w_packed), s_w, nullptr,
+                                           static_cast<cudaStream_t>(stream)),
+                   "w4 quantize launch");
+    });
+}
+
+ody_status ody_dev_w4_prepack(const void* flat, size_t n, size_t k, void* w_packed, void* stream) {
+    if (!flat || !w_packed) return einval("ody_dev_w4_prepack: null argument");
+    return guarded([&] {
+        cuda_check(launch_w4_prepack_flat(static_cast<const uint8_t*>(flat), static_cast<int>(n),
+                                          static_cast<int>(k), static_cast<uint8_t*>(w_packed),
+                                          static_cast<cudaStream_t>(stream)),
+                   "w4 prepack launch");
+    });
+}
+
+ody_status ody_dev_w4_unpack(const void* w_packed, size_t n, size_t k, void* flat, void* stream) {
+    if (!flat || !w_packed) return einval("ody_dev_w4_unpack: null argument");
+    return guarded([&] {
+        cuda_check(launch_w4_unpack_flat(static_cast<const uint8_t*>(w_packed), static_cast<int>(n),
+                                         static_cast<int>(k), static_cast<uint8_t*>(flat),
+                                         static_cast<cudaStream_t>(stream)),
+                   "w4 unpack launch");
+    });
+}
+
+ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_packed,
+                             const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                             void* out, int32_t* acc_out, void* workspace, size_t workspace_bytes,
+                             int max_ctas, int pdl, void* stream) {
+    if (!q || !s_a || !w_packed || !s_w || (!out && !acc_out) || !workspace)
+        return einval("ody_dev_w4a8_gemm: null argument");
+    if (m == 0 || n == 0 || k == 0) return einval("ody_dev_w4a8_gemm: empty operand");
+    if (k > kMaxK) return einval("GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
+    if (out_dtype < ODY_DTYPE_F32 || out_dtype > ODY_DTYPE_BF16) return einval("bad out dtype");
+    return guarded([&] {
+        GemmArgs g = {};
+        g.qa = static_cast<const int8_t*>(q);
+        g.sa = s_a;
+        g.wp = static_cast<const uint8_t*>(w_packed);
+        g.sw = s_w;
+        g.out = out;
+        g.out_dtype = static_cast<int>(out_dtype);
+        g.acc_out = acc_out;
+        g.workspace = workspace;
+        g.workspace_bytes = workspace_bytes;
+        g.M = static_cast<int>(m);
+        g.N = static_cast<int>(n);
+        g.K = static_cast<int>(k);
+        g.max_ctas = max_ctas;
+        g.pdl = pdl != 0;
+        if (workspace_bytes < gemm_workspace_bytes(g.M, g.N, g.K, max_ctas))
+            fail(ODY_EINVAL, "ody_dev_w4a8_gemm: workspace too small");
+        cuda_check(launch_w4a8_gemm(g, static_cast<cudaStream_t>(stream)), "w4a8_gemm launch");
+    });
+}
+
+ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream) {
+    if (!workspace) return einval("ody_dev_workspace_init: null argument");
+    return guarded([&] {
+        cuda_check(cudaMemsetAsync(workspace, 0, bytes, static_cast<cudaStream_t>(stream)),
+                   "workspace memset");
+    });
+}
+
+ody_status ody_dev_a8_unpack(const void* q, const float* s, size_t m, size_t k, int8_t* codes,
+                             float* dequant, void* stream) {
+    if (!q || (!codes && !dequant) || (dequant && !s)) return einval("ody_dev_a8_unpack: null argument");
+    return guarded([&] {
+        cuda_check(launch_a8_unpack(static_cast<const int8_t*>(q), s, static_cast<int>(m),
+                                    static_cast<int>(k), codes, dequant,
+                                    static_cast<cudaStream_t>(stream)),
+                   "a8 unpack launch");
+    });
+}
+
+// ================================================================ part 3
+ody_status ody_qtensor_export(const ody_qtensor* q, void* codes_or_nibbles, float* scales) {
+    if (!q) return einval("ody_qtensor_export: null argument");
+    return guarded([&] {
+        cudaStream_t st = rt().stream;
+        const size_t r = q->rows, c = q->cols;
+        if (codes_or_nibbles) {
+            if (q->kind == QKind::Act8) {
+                DevBuf<int8_t> d(r * c, st);
+                cuda_check(launch_a8_unpack(static_cast<const int8_t*>(q->codes), q->scales,
+                                            static_cast<int>(r), static_cast<int>(c), d.p, nullptr, st),
+                           "a8 unpack");
+                cuda_check(cudaMemcpyAsync(codes_or_nibbles, d.p, r * c, cudaMemcpyDeviceToHost, st), "D2H");
+                sync(st, "ody_qtensor_export");
+            } else {
+                const size_t nb = (r * c + 1) / 2;
+                DevBuf<uint8_t> d(nb, st);
+                cuda_check(launch_w4_unpack_flat(static_cast<const uint8_t*>(q->codes),
+                                                 static_cast<int>(r), static_cast<int>(c), d.p, st),
+                           "w4 unpack");
+                cuda_check(cudaMemcpyAsync(codes_or_nibbles, d.p, nb, cudaMemcpyDeviceToHost, st), "D2H");
+                sync(st, "ody_qtensor_export");
+            }
+        }
+        if (scales) {
+            cuda_check(cudaMemcpyAsync(scales, q->scales, r * 4, cudaMemcpyDeviceToHost, st), "D2H");
+            sync(st, "ody_qtensor_export");
+        }
+    });
+}
+
+ody_status ody_qtensor_import_w4(size_t n, size_t k, const void* flat, const float* scales,
+                                 ody_qtensor** out) {
+    if (!flat || !scales || !out) return einval("ody_qtensor_import_w4: null argument");
+    if (n == 0 || k == 0) return einval("ody_qtensor_import_w4: empty tensor");
+    return guarded([&] {
+        for (size_t i = 0; i < n; ++i)  // ref tensor.cpp:161-165
+            if (!(scales[i] > 0.0f) || !std::isfinite(scales[i]))
+                fail(ODY_EINVAL, "QuantizedTensor: non-positive scale");
+        cudaStream_t st = rt().stream;
+        const size_t nb = (n * k + 1) / 2;
+        DevBuf<uint8_t> fd(nb, st);
+        cuda_check(cudaMemcpyAsync(fd.p, flat, nb, cudaMemcpyHostToDevice, st), "H2D");
+        DevBuf<uint8_t> packed(w4_packed_bytes(n, k), st);
+        DevBuf<float> sd(n, st);
+        cuda_check(cudaMemcpyAsync(sd.p, scales, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(launch_w4_prepack_flat(fd.p, static_cast<int>(n), static_cast<int>(k), packed.p, st),
+                   "w4 prepack");
+        sync(st, "ody_qtensor_import_w4");
+        auto* q = new ody_qtensor();
+        q->kind = QKind::Weight4;
+        q->rows = n;
+        q->cols = k;
+        q->codes = packed.release();
+        q->scales = sd.release();
+        *out = q;
+    });
+}
+
+ody_status ody_qtensor_import_a8(size_t m, size_t k, const int8_t* codes, const float* scales,
+                                 ody_qtensor** out) {
+    if (!codes || !scales || !out) return einval("ody_qtensor_import_a8: null argument");
+    if (m == 0 || k == 0) return einval("ody_qtensor_import_a8: empty tensor");
+    return guarded([&] {
+        for (size_t i = 0; i < m; ++i)
+            if (!(scales[i] > 0.0f) || !std::isfinite(scales[i]))
+                fail(ODY_EINVAL, "QuantizedTensor: non-positive scale");
+        // layout transform of imported codes (import utility, not the hot path)
+        const size_t mp = pad_m(m), bytes = a8_bytes(m, k);
+        std::vector<int8_t> host(bytes, 0);
+        for (size_t t = 0; t < m; ++t)
+            for (size_t kk = 0; kk < k; ++kk) host[a8_offset(t, kk, mp)] = codes[t * k + kk];
+        cudaStream_t st = rt().stream;
+        DevBuf<int8_t> q(bytes, st);
+        DevBuf<float> sd(m, st);
+        cuda_check(cudaMemcpyAsync(q.p, host.data(), bytes, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(sd.p, scales, m * 4, cudaMemcpyHostToDevice, st), "H2D");
+        sync(st, "ody_qtensor_import_a8");
+        auto* qt = new ody_qtensor();
+        qt->kind = QKind::Act8;
+        qt->rows = m;
+        qt->cols = k;
+        qt->codes = q.release();
+        qt->scales = sd.release();
+        *out = qt;
+    });
+}
+
+ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q, int32_t* acc) {
+    if (!a_q || !w_q || !acc) return einval("ody_gemm_accumulators: null argument");
+    return guarded([&] {
+        check_fast_inputs(a_q, w_q);
+        Runtime& r = rt();
+        std::lock_guard<std::mutex> lock(r.mu);
+        cudaStream_t st = r.stream;
+        const size_t m = a_q->rows, n = w_q->rows;
+        DevBuf<int32_t> ad(m * n, st);
+        run_gemm(a_q, w_q, nullptr, ad.p, st);
+        cuda_check(cudaMemcpyAsync(acc, ad.p, m * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        sync(st, "ody_gemm_accumulators");
+    });
+}
+
+const char* ody_b200_version(void) {
+    try {
+        return rt().version.c_str();
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return "libodyssey_b200 (no sm_100 device)";
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,424 @@
+// gemm_kernel.cu -- K3+K4: the W4A8 FastGEMM core with its fused dequantizing epilogue.
+//
+// Reference semantics (ref gemm.cpp:251-279):
+//     acc  = sum_k a[i][k] * (16 * w[j][k])        (int32, exact)
+//     acc >>= 4                                     (exact: every addend is a multiple of 16)
+//     out[i][j] = float(acc) * (sa[i] * sw[j])
+//
+// B200 mapping (swap-AB, weights are the MMA "A" operand, tokens the MMA "N"):
+//   * producer warp: 1-D bulk copies (cp.async.bulk -> UBLKCP) of one 8 KiB packed-INT4
+//     weight block (128 rows x 128 k) and the matching activation k-block
+//     (BN tokens x 128 B, pre-swizzled SWIZZLE_128B) into an S-stage smem ring;
+//   * converter warps (2 groups x 4 warps, one warp per TMEM sub-partition): read the
+//     packed block from smem, widen SINT4 -> S8 with the paper's high-nibble trick
+//     ((w<<4)&0xF0F0F0F0 and w&0xF0F0F0F0 -- lanes hold value*16, no per-group scale
+//     multiply), and tcgen05.st the int8 lanes straight into TMEM as the A operand;
+//   * MMA warp (one elected thread): tcgen05.mma.kind::i8 with A from TMEM, B from
+//     smem, int32 accumulators D in TMEM (double-buffered);
+//   * epilogue warps: tcgen05.ld D, >>4, *(sa*sw) with IEEE RN multiplies, store
+//     f32/f16/bf16 -- or, for stream-K partial tiles, red.add.s32 into an L2-resident
+//     workspace; the CTA that completes a tile's K range finalises it (integer
+//     addition is associative, so split-K is bit-exact) and re-zeroes the workspace.
+//   * scheduling: persistent grid of <= #SMs CTAs; full waves of (n_tile, m_tile)
+//     tiles are data-parallel, the remainder (all tiles for decode shapes) is split
+//     stream-K over 128-k units, so every SM streams the same number of weight bytes.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "kernels.h"
+#include "layout.h"
+#include "ptx.cuh"
+
+namespace odyb200 {
+
+namespace {
+
+constexpr int kNumThreads = 512;   // 16 warps
+constexpr int kWarpProducer = 0;
+constexpr int kWarpMma = 1;
+constexpr int kWarpAlloc = 2;
+constexpr int kWarpConv0 = 4;      // warps 4..11: two converter groups of 4
+constexpr int kConvGroups = 2;
+constexpr int kWarpEpi0 = 12;      // warps 12..15
+constexpr int kAStages = 4;        // TMEM A stages (32 columns each)
+constexpr int kTmemCols = 512;
+constexpr int kAColBase = 256;     // A stages live at columns 256..383
+constexpr int kSmemBudget = 200 * 1024;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kBBytes = BN * 128;                   // activation k-block tile
+    static constexpr int kStageBytes = kBBytes + kWBlockBytes; // B first (1024-aligned)
+    static constexpr int kStages = std::min(16, kSmemBudget / kStageBytes);
+    static constexpr int kBarrierBytes = 1024;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kBarrierBytes + 1024;  // +align
+    // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
+    static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                       (static_cast<uint32_t>(BN >> 3) << 17) |
+                                       (static_cast<uint32_t>(128 >> 4) << 24);
+    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 128, "BN");
+    static_assert(kBBytes % 1024 == 0, "swizzle atom alignment");
+};
+
+struct Params {
+    const int8_t* qa;
+    const float* sa;
+    const uint8_t* wp;
+    const float* sw;
+    void* out;
+    int32_t* acc_out;
+    int32_t* ws_acc;
+    uint32_t* ws_cnt;
+    int out_dtype;
+    int M, N, K, Mp;
+    int kblocks, m_tiles, tiles, dp_tiles, sk_units;
+    int pdl;
+};
+
+// Walks this CTA's segments: data-parallel tiles first, then its stream-K unit range.
+struct SegIter {
+    int tile, kb0, kb1;
+    int dp_next, u, u_end;
+    __device__ void init(const Params& p) {
+        const int P = gridDim.x, b = blockIdx.x;
+        dp_next = b;
+        const long long su = p.sk_units;
+        u = static_cast<int>(su * b / P);
+        u_end = static_cast<int>(su * (b + 1) / P);
+    }
+    __device__ bool next(const Params& p) {
+        if (dp_next < p.dp_tiles) {
+            tile = dp_next;
+            kb0 = 0;
+            kb1 = p.kblocks;
+            dp_next += gridDim.x;
+            return true;
+        }
+        if (u >= u_end) return false;
+        const int t = u / p.kblocks;
+        tile = p.dp_tiles + t;
+        kb0 = u - t * p.kblocks;
+        kb1 = min(p.kblocks, kb0 + (u_end - u));
+        u += kb1 - kb0;
+        return true;
+    }
+};
+
+__device__ __forceinline__ uint64_t b_desc(uint32_t smem_addr) {
+    // K-major SWIZZLE_128B: start>>4, LBO unused, SBO = 1024 B (8 rows x 128 B),
+    // version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+    return static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(64) << 32) |
+           (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+
+__device__ __forceinline__ void store_out(const Params& p, int t, int n, int32_t acc) {
+    const size_t idx = static_cast<size_t>(t) * p.N + n;
+    if (p.acc_out) p.acc_out[idx] = acc;
+    if (p.out) {
+        const int32_t sh = acc >> 4;  // exact (ref gemm.cpp:269)
+        const float v = __fmul_rn(__int2float_rn(sh), __fmul_rn(__ldg(p.sa + t), __ldg(p.sw + n)));
+        if (p.out_dtype == kDtypeF32)
+            static_cast<float*>(p.out)[idx] = v;
+        else if (p.out_dtype == kDtypeF16)
+            static_cast<__half*>(p.out)[idx] = __float2half_rn(v);
+        else
+            static_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(v);
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params p) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* stages = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* w_full = bars;
+    uint64_t* w_empty = w_full + C::kStages;
+    uint64_t* a_full = w_empty + C::kStages;
+    uint64_t* a_empty = a_full + kAStages;
+    uint64_t* d_full = a_empty + kAStages;
+    uint64_t* d_empty = d_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+    volatile uint32_t* fin_flag = tmem_slot + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::kStages; ++i) {
+            mbar_init(&w_full[i], 1);
+            mbar_init(&w_empty[i], 4 + 1);  // 4 converter warps + MMA commit
+        }
+        for (int i = 0; i < kAStages; ++i) {
+            mbar_init(&a_full[i], 4);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&d_full[i], 1);
+            mbar_init(&d_empty[i], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == kWarpAlloc) {
+        tmem_alloc(tmem_slot, kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    SegIter it;
+    it.init(p);
+
+    if (warp == kWarpProducer) {
+        if (lane == 0) {
+            const uint64_t pol_w = l2_policy_evict_first();
+            const uint64_t pol_a = l2_policy_evict_last();
+            if (p.pdl) pdl_wait();
+            int u = 0;
+            while (it.next(p)) {
+                const int nt = it.tile / p.m_tiles, mt = it.tile % p.m_tiles;
+                const uint8_t* wsrc = p.wp + (static_cast<size_t>(nt) * p.kblocks) * kWBlockBytes;
+                const int8_t* asrc = p.qa + static_cast<size_t>(mt) * BN * 128;
+                for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
+                    const int s = u % C::kStages;
+                    mbar_wait(&w_empty[s], ((u / C::kStages) & 1) ^ 1);
+                    uint8_t* st = stages + s * C::kStageBytes;
+                    mbar_expect_tx(&w_full[s], C::kStageBytes);
+                    bulk_g2s(st, asrc + static_cast<size_t>(kb) * p.Mp * 128, C::kBBytes, &w_full[s],
+                             pol_a);
+                    bulk_g2s(st + C::kBBytes, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
+                             kWBlockBytes, &w_full[s], pol_w);
+                }
+            }
+        }
+    } else if (warp == kWarpMma) {
+        if (lane == 0) {
+            int u = 0, j = 0;
+            const uint32_t stage_base = smem_u32(stages);
+            while (it.next(p)) {
+                const int db = j & 1;
+                mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + db * BN;
+                for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
+                    const int s = u % C::kStages;
+                    const int as = u % kAStages;
+                    mbar_wait(&w_full[s], (u / C::kStages) & 1);
+                    mbar_wait(&a_full[as], (u / kAStages) & 1);
+                    tc_fence_after();
+                    const uint32_t b_addr = stage_base + s * C::kStageBytes;
+                    const uint32_t a_tmem = tmem + kAColBase + as * 32;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b_addr + 32 * c), C::kIdesc,
+                                  (kb > it.kb0 || c > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&a_empty[as]);
+                    mma_commit(&w_empty[s]);
+                }
+                mma_commit(&d_full[db]);
+                ++j;
+            }
+        }
+    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kConvGroups) {
+        const int g = (warp - kWarpConv0) / 4;
+        const int q = warp & 3;  // TMEM sub-partition: lanes 32q..32q+31
+        const int r = 32 * q + lane;
+        const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
+        int u = 0;
+        while (it.next(p)) {
+            for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
+                if ((u % kConvGroups) != g) continue;
+                const int s = u % C::kStages;
+                const int as = u % kAStages;
+                mbar_wait(&w_full[s], (u / C::kStages) & 1);
+                const uint4* src = reinterpret_cast<const uint4*>(stages + s * C::kStageBytes +
+                                                                  C::kBBytes + r * 16);
+                uint32_t lanes8[32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 v = src[c * (2048 / 16)];
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        lanes8[c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k = 8jj+0..3
+                        lanes8[c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k = 8jj+4..7
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&w_empty[s]);
+                mbar_wait(&a_empty[as], ((u / kAStages) & 1) ^ 1);
+                tc_fence_after();
+                tmem_st_32x32b_x32(t_lane + kAColBase + as * 32, lanes8);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[as]);
+            }
+        }
+    } else if (warp >= kWarpEpi0) {
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
+        if (p.pdl) pdl_wait();
+        int j = 0;
+        while (it.next(p)) {
+            const int db = j & 1;
+            mbar_wait(&d_full[db], (j >> 1) & 1);
+            tc_fence_after();
+            const int nt = it.tile / p.m_tiles, mt = it.tile % p.m_tiles;
+            const int n = nt * kTileN + r;
+            const int t0 = mt * BN;
+            const bool full = (it.kb0 == 0 && it.kb1 == p.kblocks);
+            const int skt = it.tile - p.dp_tiles;
+            int32_t* ws = p.ws_acc + static_cast<size_t>(skt) * BN * kTileN;
+#pragma unroll 1
+            for (int tc = 0; tc < BN; tc += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(t_lane + db * BN + tc, v);
+                tmem_wait_ld();
+                if (full) {
+                    if (n < p.N) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int t = t0 + tc + i;
+                            if (t < p.M) store_out(p, t, n, static_cast<int32_t>(v[i]));
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_add_s32(ws + (tc + i) * kTileN + r, static_cast<int32_t>(v[i]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_empty[db]);
+            if (!full) {
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (warp == kWarpEpi0 && lane == 0) {
+                    const uint32_t add = static_cast<uint32_t>(it.kb1 - it.kb0);
+                    const uint32_t old = atomicAdd(p.ws_cnt + skt, add);
+                    *fin_flag = (old + add == static_cast<uint32_t>(p.kblocks)) ? 1u : 0u;
+                }
+                named_bar_sync(1, 128);
+                if (*fin_flag) {
+                    __threadfence();
+                    for (int tt = 0; tt < BN; ++tt) {
+                        int32_t* cell = ws + tt * kTileN + r;
+                        const int32_t acc = __ldcg(cell);
+                        __stcg(cell, 0);
+                        const int t = t0 + tt;
+                        if (t < p.M && n < p.N) store_out(p, t, n, acc);
+                    }
+                    if (warp == kWarpEpi0 && lane == 0) p.ws_cnt[skt] = 0u;
+                }
+                named_bar_sync(1, 128);
+            }
+            ++j;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
+}
+
+template <int BN>
+cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
+    using C = Cfg<BN>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(w4a8_gemm_kernel<BN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNumThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, w4a8_gemm_kernel<BN>, p);
+}
+
+int pick_bn(int M) {
+    if (M <= 16) return 16;
+    if (M <= 32) return 32;
+    if (M <= 64) return 64;
+    return 128;
+}
+
+}  // namespace
+
+int device_sm_count() {
+    static int sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
+    return sms;
+}
+
+size_t gemm_workspace_bytes(int M, int N, int K, int num_sms) {
+    (void)N;
+    (void)K;
+    const int bn = pick_bn(M);
+    const size_t P = static_cast<size_t>(num_sms > 0 ? num_sms : device_sm_count());
+    return round_up(P * sizeof(uint32_t), 256) + P * bn * kTileN * sizeof(int32_t);
+}
+
+cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
+    const int bn = pick_bn(a.M);
+    Params p = {};
+    p.qa = a.qa;
+    p.sa = a.sa;
+    p.wp = a.wp;
+    p.sw = a.sw;
+    p.out = a.out;
+    p.acc_out = a.acc_out;
+    p.out_dtype = a.out_dtype;
+    p.M = a.M;
+    p.N = a.N;
+    p.K = a.K;
+    p.Mp = static_cast<int>(pad_m(a.M));
+    p.kblocks = static_cast<int>(pad_k(a.K) / kBlockK);
+    const int n_tiles = static_cast<int>(pad_n(a.N) / kTileN);
+    p.m_tiles = (a.M + bn - 1) / bn;
+    p.tiles = n_tiles * p.m_tiles;
+    const int sms = a.max_ctas > 0 ? a.max_ctas : device_sm_count();
+    const long long units = static_cast<long long>(p.tiles) * p.kblocks;
+    const int P = static_cast<int>(std::min<long long>(sms, units));
+    p.dp_tiles = (p.tiles / P) * P;
+    p.sk_units = (p.tiles - p.dp_tiles) * p.kblocks;
+    if (a.workspace_bytes < gemm_workspace_bytes(a.M, a.N, a.K, sms)) return cudaErrorInvalidValue;
+    p.ws_cnt = static_cast<uint32_t*>(a.workspace);
+    p.ws_acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(a.workspace) +
+                                          round_up(static_cast<size_t>(sms) * sizeof(uint32_t), 256));
+    p.pdl = a.pdl ? 1 : 0;
+    switch (bn) {
+        case 16: return launch_bn<16>(p, P, a.pdl, st);
+        case 32: return launch_bn<32>(p, P, a.pdl, st);
+        case 64: return launch_bn<64>(p, P, a.pdl, st);
+        default: return launch_bn<128>(p, P, a.pdl, st);
+    }
+}
+
+}  // namespace odyb200

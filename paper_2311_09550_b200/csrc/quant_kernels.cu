@@ -1,0 +1,395 @@
+// quant_kernels.cu -- K1 (per-token INT8 activation quantization) and K2 (per-channel
+// INT4 weight quantization + prepack into the w4 tile layout), plus the layout
+// converters used by checkpoint ingest/export and the parity suite.
+//
+// Bit-exactness contract with the reference (ref quantize.cpp:12-47,113-132):
+//   S = max(|g*max|,|b*min|) / qmax  (IEEE f32 division), S <= 0 -> 2^-24
+//   code = clamp(roundf(x / S))       (IEEE division, round half away from zero)
+// Built WITHOUT --use_fast_math so '/' is IEEE round-to-nearest and no FTZ.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+#include "layout.h"
+#include "ptx.cuh"
+
+namespace odyb200 {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ref quantize.cpp:12-18
+__device__ __forceinline__ int32_t clamp_code(float x, int32_t lo, int32_t hi) {
+    float r = roundf(x);
+    if (r < static_cast<float>(lo)) return lo;
+    if (r > static_cast<float>(hi)) return hi;
+    return static_cast<int32_t>(r);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+constexpr int kActThreads = 128;
+
+// Load 16 consecutive row elements starting at k0 (zero beyond K).
+template <typename T>
+__device__ __forceinline__ void load16(const T* __restrict__ row, int k0, int K, float (&v)[16]) {
+    if (k0 + 16 <= K && (reinterpret_cast<uintptr_t>(row + k0) & 15) == 0) {
+        constexpr int kPer = 16 / sizeof(T);
+#pragma unroll
+        for (int i = 0; i < 16; i += kPer) {
+            uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + k0 + i));
+            const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[i + j] = to_f32(e[j]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = (k0 + i < K) ? to_f32(row[k0 + i]) : 0.0f;
+    }
+}
+
+// K1: one CTA per token row.  Pass 1 absmax (warp-shuffle + smem), pass 2
+// divide/round/clamp and 128-bit stores into the swizzled a8 k-block layout.
+// absmax_in (optional) supplies a precomputed row max (row-parallel TP: the
+// all-reduced global max of a K-sharded row).  absmax_out (optional) exports it.
+template <typename T>
+__global__ void __launch_bounds__(kActThreads)
+act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int Mp,
+                 int8_t* __restrict__ q, float* __restrict__ s,
+                 const float* __restrict__ absmax_in, float* __restrict__ absmax_out,
+                 int pdl) {
+    if (pdl) pdl_wait();
+    const int t = blockIdx.x;
+    const T* row = x + static_cast<size_t>(t) * ldx;
+    __shared__ float red[kActThreads / 32];
+    __shared__ float s_shared;
+    const int nchunks = Kp / 16;
+
+    float scale;
+    if (absmax_in) {
+        scale = absmax_in[t] / 127.0f;
+    } else {
+        float mx = 0.0f;
+        for (int c = threadIdx.x; c < nchunks; c += kActThreads) {
+            if (c * 16 >= K) break;
+            float v[16];
+            load16(row, c * 16, K, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fabsf(v[i]));
+        }
+        mx = warp_max(mx);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float m = red[0];
+#pragma unroll
+            for (int i = 1; i < kActThreads / 32; ++i) m = fmaxf(m, red[i]);
+            s_shared = m;
+            if (absmax_out) absmax_out[t] = m;
+        }
+        __syncthreads();
+        // max(|max|,|min|) == max|x| for finite rows (ref quantize.cpp:27-33)
+        scale = s_shared / 127.0f;
+    }
+    if (!(scale > 0.0f)) scale = kMinScale;
+    if (threadIdx.x == 0) s[t] = scale;
+    if (pdl) pdl_launch_dependents();
+
+    for (int c = threadIdx.x; c < nchunks; c += kActThreads) {
+        float v[16];
+        load16(row, c * 16, K, v);
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                int32_t code = clamp_code(v[i * 4 + b] / scale, -128, 127);
+                acc |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * b);
+            }
+            w[i] = acc;
+        }
+        const size_t off = a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, Mp);
+        *reinterpret_cast<uint4*>(q + off) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// Per-row scale for per-channel weights: ref quantize.cpp:22-35.  One warp per row.
+__global__ void w_scale_kernel(const float* __restrict__ w, int N, int K, int bits,
+                               const float* __restrict__ gamma, const float* __restrict__ beta,
+                               float* __restrict__ s, int* __restrict__ err) {
+    const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= N) return;
+    const float* r = w + static_cast<size_t>(row) * K;
+    float mx = r[0], mn = r[0];
+    for (int k = lane; k < K; k += 32) {
+        mx = fmaxf(mx, r[k]);
+        mn = fminf(mn, r[k]);
+    }
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    if (lane == 0) {
+        const float g = gamma ? gamma[row] : 1.0f;
+        const float b = beta ? beta[row] : 1.0f;
+        if (!(g > 0.0f && g <= 1.0f && b > 0.0f && b <= 1.0f)) atomicExch(err, 1);
+        const float qmax = static_cast<float>((1 << (bits - 1)) - 1);
+        float sc = fmaxf(fabsf(__fmul_rn(g, mx)), fabsf(__fmul_rn(b, mn))) / qmax;
+        s[row] = sc > 0.0f ? sc : kMinScale;
+    }
+}
+
+// K2 (quantize + prepack): one thread per (row, 32-k chunk); writes one 16-byte
+// row chunk of the w4 tile layout.  Rows >= N and k >= K are zero codes.
+__global__ void w4_quant_prepack_kernel(const float* __restrict__ w, int N, int K, int Np, int Kp,
+                                        const float* __restrict__ s, uint8_t* __restrict__ out) {
+    const size_t chunks_per_row = Kp / 32;
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(Np) * chunks_per_row) return;
+    const int r = static_cast<int>(idx / chunks_per_row);
+    const int cc = static_cast<int>(idx % chunks_per_row);
+    int8_t code[32];
+    if (r < N) {
+        const float sc = s[r];
+        const float* row = w + static_cast<size_t>(r) * K;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const int k = cc * 32 + e;
+            code[e] = k < K ? static_cast<int8_t>(clamp_code(row[k] / sc, -8, 7)) : int8_t(0);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) code[e] = 0;
+    }
+    uint32_t word[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t lo = static_cast<uint32_t>(code[8 * j + b]) & 0xFu;
+            const uint32_t hi = static_cast<uint32_t>(code[8 * j + 4 + b]) & 0xFu;
+            v |= (lo | (hi << 4)) << (8 * b);
+        }
+        word[j] = v;
+    }
+    int high;
+    const size_t off = w4_offset(r, static_cast<size_t>(cc) * 32, Kp / kBlockK, &high);
+    *reinterpret_cast<uint4*>(out + off) = make_uint4(word[0], word[1], word[2], word[3]);
+}
+
+// K2 (prepack only): reference flat PackedInt4Buffer (ref tensor.hpp:43-64) -> tile layout.
+__global__ void w4_prepack_flat_kernel(const uint8_t* __restrict__ flat, int N, int K, int Np,
+                                       int Kp, uint8_t* __restrict__ out) {
+    const size_t chunks_per_row = Kp / 32;
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(Np) * chunks_per_row) return;
+    const int r = static_cast<int>(idx / chunks_per_row);
+    const int cc = static_cast<int>(idx % chunks_per_row);
+    uint32_t nib[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+        const int k = cc * 32 + e;
+        if (r < N && k < K) {
+            const size_t i = static_cast<size_t>(r) * K + k;
+            const uint8_t byte = flat[i / 2];
+            nib[e] = (i % 2 == 0) ? (byte & 0xFu) : (byte >> 4);
+        } else {
+            nib[e] = 0;
+        }
+    }
+    uint32_t word[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v |= (nib[8 * j + b] | (nib[8 * j + 4 + b] << 4)) << (8 * b);
+        word[j] = v;
+    }
+    int high;
+    const size_t off = w4_offset(r, static_cast<size_t>(cc) * 32, Kp / kBlockK, &high);
+    *reinterpret_cast<uint4*>(out + off) = make_uint4(word[0], word[1], word[2], word[3]);
+}
+
+__device__ __forceinline__ uint32_t w4_nibble(const uint8_t* __restrict__ packed, size_t i, int K,
+                                              size_t kblocks) {
+    const size_t r = i / K, k = i % K;
+    int high;
+    const size_t off = w4_offset(r, k, kblocks, &high);
+    const uint8_t b = packed[off];
+    return high ? (b >> 4) : (b & 0xFu);
+}
+
+// Tile layout -> reference flat PackedInt4Buffer bytes (odd tail high nibble 0).
+__global__ void w4_unpack_flat_kernel(const uint8_t* __restrict__ packed, int N, int K, int Kp,
+                                      uint8_t* __restrict__ flat) {
+    const size_t count = static_cast<size_t>(N) * K;
+    const size_t nbytes = (count + 1) / 2;
+    const size_t b = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nbytes) return;
+    const size_t kblocks = Kp / kBlockK;
+    uint32_t lo = w4_nibble(packed, 2 * b, K, kblocks);
+    uint32_t hi = (2 * b + 1 < count) ? w4_nibble(packed, 2 * b + 1, K, kblocks) : 0u;
+    flat[b] = static_cast<uint8_t>(lo | (hi << 4));
+}
+
+// Dequantize weights: out[r][k] = code * S_r  (ref quantize.cpp:134-146).
+__global__ void w4_dequant_kernel(const uint8_t* __restrict__ packed, const float* __restrict__ s,
+                                  int N, int K, int Kp, float* __restrict__ out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<size_t>(N) * K) return;
+    uint32_t nib = w4_nibble(packed, i, K, Kp / kBlockK);
+    const int code = nib >= 8 ? static_cast<int>(nib) - 16 : static_cast<int>(nib);
+    out[i] = static_cast<float>(code) * s[i / K];
+}
+
+// Activation codes -> row-major int8 (and optional dequantized f32).
+__global__ void a8_unpack_kernel(const int8_t* __restrict__ q, const float* __restrict__ s, int M,
+                                 int K, int Mp, int8_t* __restrict__ codes,
+                                 float* __restrict__ deq) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<size_t>(M) * K) return;
+    const size_t t = i / K, k = i % K;
+    const int8_t c = q[a8_offset(t, k, Mp)];
+    if (codes) codes[i] = c;
+    if (deq) deq[i] = static_cast<float>(c) * s[t];
+}
+
+// Row absmax only (for row-parallel TP: local max before the MAX all-reduce).
+template <typename T>
+__global__ void __launch_bounds__(kActThreads)
+row_absmax_kernel(const T* __restrict__ x, size_t ldx, int K, float* __restrict__ out) {
+    const T* row = x + static_cast<size_t>(blockIdx.x) * ldx;
+    __shared__ float red[kActThreads / 32];
+    float mx = 0.0f;
+    for (int k0 = threadIdx.x * 16; k0 < K; k0 += kActThreads * 16) {
+        float v[16];
+        load16(row, k0, K, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fabsf(v[i]));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = red[0];
+        for (int i = 1; i < kActThreads / 32; ++i) m = fmaxf(m, red[i]);
+        out[blockIdx.x] = m;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K, int8_t* q,
+                             float* s, const float* absmax_in, float* absmax_out, bool pdl,
+                             cudaStream_t st) {
+    const int Kp = static_cast<int>(pad_k(K)), Mp = static_cast<int>(pad_m(M));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(M);
+    cfg.blockDim = dim3(kActThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const int p = pdl ? 1 : 0;
+    switch (dtype) {
+        case kDtypeF32:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<float>, static_cast<const float*>(x),
+                                      ldx, M, K, Kp, Mp, q, s, absmax_in, absmax_out, p);
+        case kDtypeF16:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__half>,
+                                      static_cast<const __half*>(x), ldx, M, K, Kp, Mp, q, s,
+                                      absmax_in, absmax_out, p);
+        case kDtypeBF16:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__nv_bfloat16>,
+                                      static_cast<const __nv_bfloat16*>(x), ldx, M, K, Kp, Mp, q,
+                                      s, absmax_in, absmax_out, p);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_row_absmax(const void* x, int dtype, size_t ldx, int M, int K, float* out,
+                              cudaStream_t st) {
+    switch (dtype) {
+        case kDtypeF32:
+            row_absmax_kernel<float><<<M, kActThreads, 0, st>>>(static_cast<const float*>(x), ldx,
+                                                                K, out);
+            break;
+        case kDtypeF16:
+            row_absmax_kernel<__half><<<M, kActThreads, 0, st>>>(static_cast<const __half*>(x),
+                                                                 ldx, K, out);
+            break;
+        case kDtypeBF16:
+            row_absmax_kernel<__nv_bfloat16><<<M, kActThreads, 0, st>>>(
+                static_cast<const __nv_bfloat16*>(x), ldx, K, out);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_w4_quant_prepack(const float* w, int N, int K, int bits, const float* gamma,
+                                    const float* beta, uint8_t* packed, float* s, int* err,
+                                    cudaStream_t st) {
+    const int Np = static_cast<int>(pad_n(N)), Kp = static_cast<int>(pad_k(K));
+    w_scale_kernel<<<(N + 7) / 8, 256, 0, st>>>(w, N, K, bits, gamma, beta, s, err);
+    const size_t total = static_cast<size_t>(Np) * (Kp / 32);
+    w4_quant_prepack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        w, N, K, Np, Kp, s, packed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_w4_prepack_flat(const uint8_t* flat, int N, int K, uint8_t* packed,
+                                   cudaStream_t st) {
+    const int Np = static_cast<int>(pad_n(N)), Kp = static_cast<int>(pad_k(K));
+    const size_t total = static_cast<size_t>(Np) * (Kp / 32);
+    w4_prepack_flat_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        flat, N, K, Np, Kp, packed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_w4_unpack_flat(const uint8_t* packed, int N, int K, uint8_t* flat,
+                                  cudaStream_t st) {
+    const size_t nbytes = (static_cast<size_t>(N) * K + 1) / 2;
+    w4_unpack_flat_kernel<<<static_cast<unsigned>((nbytes + 255) / 256), 256, 0, st>>>(
+        packed, N, K, static_cast<int>(pad_k(K)), flat);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_w4_dequant(const uint8_t* packed, const float* s, int N, int K, float* out,
+                              cudaStream_t st) {
+    const size_t total = static_cast<size_t>(N) * K;
+    w4_dequant_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        packed, s, N, K, static_cast<int>(pad_k(K)), out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_a8_unpack(const int8_t* q, const float* s, int M, int K, int8_t* codes,
+                             float* deq, cudaStream_t st) {
+    const size_t total = static_cast<size_t>(M) * K;
+    a8_unpack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        q, s, M, K, static_cast<int>(pad_m(M)), codes, deq);
+    return cudaGetLastError();
+}
+
+}  // namespace odyb200

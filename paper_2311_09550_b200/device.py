@@ -1,0 +1,197 @@
+"""Device-resident, stream-ordered API (torch tensors as HBM buffers).
+
+PyTorch is only plumbing here: it allocates HBM and owns the streams; every
+arithmetic step is one of libodyssey_b200.so's sm_100a kernels, called through the
+C ABI (include/odyssey_b200.h part 2) with raw pointers.
+
+    a = act_quant(x)                     # K1: per-token INT8 (ref quantize.cpp:113-132)
+    w = W4Weight.quantize(w_f32)         # K2: per-channel INT4 + prepack (ref quantize.cpp:75-111)
+    y = w4a8_gemm(a, w, torch.float16)   # K3+K4: FastGEMM + dequant epilogue (ref gemm.cpp:251-279)
+    lin = W4A8Linear.from_float(w_f32); y = lin(x)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import (ODY_DTYPE_BF16, ODY_DTYPE_F16, ODY_DTYPE_F32, OdyError, check, lib)
+
+_DT = {torch.float32: ODY_DTYPE_F32, torch.float16: ODY_DTYPE_F16, torch.bfloat16: ODY_DTYPE_BF16}
+K_MAX = 1 << 17  # ref gemm.cpp:14
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise OdyError(1, f"{name} must be a CUDA tensor (the W4A8 path has no CPU fallback)")
+
+
+@dataclass
+class A8:
+    """Per-token INT8 activations in the a8 k-block layout (csrc/layout.h)."""
+    q: torch.Tensor        # uint8/int8 buffer of ody_dev_a8_bytes(m, k)
+    s: torch.Tensor        # f32 [m]
+    m: int
+    k: int
+
+    def codes(self, stream=None) -> torch.Tensor:
+        """Row-major int8 [m, k] (reference layout) -- inspection only."""
+        out = torch.empty((self.m, self.k), dtype=torch.int8, device=self.q.device)
+        check(lib().ody_dev_a8_unpack(self.q.data_ptr(), self.s.data_ptr(), self.m, self.k,
+                                      out.data_ptr(), None, _stream(stream)))
+        return out
+
+
+@dataclass
+class W4Weight:
+    """Per-channel INT4 weights prepacked in the w4 tile layout (csrc/layout.h)."""
+    packed: torch.Tensor   # uint8 buffer of ody_dev_w4_bytes(n, k)
+    s: torch.Tensor        # f32 [n]
+    n: int
+    k: int
+
+    @staticmethod
+    def quantize(w: torch.Tensor, gamma=None, beta=None, stream=None) -> "W4Weight":
+        """K2 on the device: f32 [n, k] -> codes clamp(round(w/S), -8, 7) + scales."""
+        _require_cuda(w, "w")
+        w = w.contiguous().float()
+        n, k = w.shape
+        if n == 0 or k == 0:
+            raise OdyError(1, "quantize_weights: empty tensor")
+        packed = torch.empty(lib().ody_dev_w4_bytes(n, k), dtype=torch.uint8, device=w.device)
+        s = torch.empty(n, dtype=torch.float32, device=w.device)
+        g = gamma.contiguous().float() if gamma is not None else None
+        b = beta.contiguous().float() if beta is not None else None
+        check(lib().ody_dev_w4_quantize(w.data_ptr(), n, k, g.data_ptr() if g is not None else None,
+                                        b.data_ptr() if b is not None else None, packed.data_ptr(),
+                                        s.data_ptr(), _stream(stream)))
+        return W4Weight(packed, s, n, k)
+
+    @staticmethod
+    def from_flat(flat: torch.Tensor, scales: torch.Tensor, n: int, k: int,
+                  stream=None) -> "W4Weight":
+        """Reference PackedInt4Buffer bytes ((n*k+1)//2) + scales -> prepacked."""
+        _require_cuda(flat, "flat")
+        if flat.numel() != (n * k + 1) // 2 or scales.numel() != n:
+            raise OdyError(1, "from_flat: payload or scales size mismatch")
+        packed = torch.empty(lib().ody_dev_w4_bytes(n, k), dtype=torch.uint8, device=flat.device)
+        check(lib().ody_dev_w4_prepack(flat.contiguous().data_ptr(), n, k, packed.data_ptr(),
+                                       _stream(stream)))
+        return W4Weight(packed, scales.contiguous().float(), n, k)
+
+    def to_flat(self, stream=None) -> torch.Tensor:
+        flat = torch.empty((self.n * self.k + 1) // 2, dtype=torch.uint8, device=self.packed.device)
+        check(lib().ody_dev_w4_unpack(self.packed.data_ptr(), self.n, self.k, flat.data_ptr(),
+                                      _stream(stream)))
+        return flat
+
+
+def act_quant(x: torch.Tensor, absmax: torch.Tensor | None = None, export_absmax: bool = False,
+              pdl: bool = False, stream=None, out: A8 | None = None):
+    """K1: per-token symmetric INT8 of a [m, k] f32/f16/bf16 CUDA tensor.
+
+    ``absmax`` (f32 [m]) overrides the row max (row-parallel TP passes the
+    all-reduced global max).  Returns an :class:`A8` (and the row max if asked)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2:
+        raise OdyError(1, "act_quant expects a 2-D tensor")
+    if x.dtype not in _DT:
+        raise OdyError(1, f"act_quant: unsupported dtype {x.dtype}")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    m, k = x.shape
+    if out is None:
+        q = torch.empty(lib().ody_dev_a8_bytes(m, k), dtype=torch.uint8, device=x.device)
+        s = torch.empty(m, dtype=torch.float32, device=x.device)
+        out = A8(q, s, m, k)
+    amax_out = torch.empty(m, dtype=torch.float32, device=x.device) if export_absmax else None
+    check(lib().ody_dev_act_quant(
+        x.data_ptr(), _DT[x.dtype], x.stride(0), m, k, out.q.data_ptr(), out.s.data_ptr(),
+        absmax.data_ptr() if absmax is not None else None,
+        amax_out.data_ptr() if amax_out is not None else None, int(pdl), _stream(stream)))
+    return (out, amax_out) if export_absmax else out
+
+
+def row_absmax(x: torch.Tensor, stream=None) -> torch.Tensor:
+    _require_cuda(x, "x")
+    x = x if x.stride(1) == 1 else x.contiguous()
+    m, k = x.shape
+    out = torch.empty(m, dtype=torch.float32, device=x.device)
+    check(lib().ody_dev_row_absmax(x.data_ptr(), _DT[x.dtype], x.stride(0), m, k, out.data_ptr(),
+                                   _stream(stream)))
+    return out
+
+
+class Workspace:
+    """Zero-initialised stream-K partial-sum buffer (the kernel leaves it zeroed)."""
+
+    _per_device: dict = {}
+
+    @classmethod
+    def get(cls, m: int, n: int, k: int, device) -> torch.Tensor:
+        dev = torch.device(device)
+        need = lib().ody_dev_workspace_bytes(m, n, k)
+        ws = cls._per_device.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+            cls._per_device[dev] = ws
+        return ws
+
+
+def w4a8_gemm(a: A8, w: W4Weight, out_dtype=torch.float16, out: torch.Tensor | None = None,
+              accumulators: bool = False, max_ctas: int = 0, pdl: bool = False, stream=None,
+              workspace: torch.Tensor | None = None):
+    """K3+K4: y[m, n] = float((sum a*16w) >> 4) * (sa*sw), written as out_dtype.
+
+    With ``accumulators=True`` returns the int32 pre-shift accumulators instead
+    (ref gemm_w4a8_fast_accumulators, gemm.cpp:229-249)."""
+    if a.k != w.k:
+        raise OdyError(1, "gemm_w4a8_fast: inner dims disagree")
+    if w.k > K_MAX:
+        raise OdyError(1, "GEMM: K exceeds the 32-bit accumulator safety bound 2^17")
+    dev = a.q.device
+    ws = workspace if workspace is not None else Workspace.get(a.m, w.n, w.k, dev)
+    acc = None
+    if accumulators:
+        acc = torch.empty((a.m, w.n), dtype=torch.int32, device=dev)
+        y_ptr = None
+    else:
+        if out is None:
+            out = torch.empty((a.m, w.n), dtype=out_dtype, device=dev)
+        y_ptr = out.data_ptr()
+        out_dtype = out.dtype
+    check(lib().ody_dev_w4a8_gemm(
+        a.q.data_ptr(), a.s.data_ptr(), w.packed.data_ptr(), w.s.data_ptr(), a.m, w.n, w.k,
+        _DT[out_dtype], y_ptr, acc.data_ptr() if acc is not None else None, ws.data_ptr(),
+        ws.numel(), max_ctas, int(pdl), _stream(stream)))
+    return acc if accumulators else out
+
+
+class W4A8Linear:
+    """A linear layer on the FastGEMM path: y = x @ W^T with W4 per-channel weights
+    and dynamic per-token A8 activations (the paper's W4A8 linear)."""
+
+    def __init__(self, weight: W4Weight, out_dtype=torch.float16):
+        self.weight = weight
+        self.out_dtype = out_dtype
+
+    @classmethod
+    def from_float(cls, w: torch.Tensor, out_dtype=torch.float16, gamma=None, beta=None):
+        return cls(W4Weight.quantize(w, gamma, beta), out_dtype)
+
+    @property
+    def in_features(self):
+        return self.weight.k
+
+    @property
+    def out_features(self):
+        return self.weight.n
+
+    def __call__(self, x: torch.Tensor, pdl: bool = False) -> torch.Tensor:
+        a = act_quant(x, pdl=pdl)
+        return w4a8_gemm(a, self.weight, self.out_dtype, pdl=pdl)
