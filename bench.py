@@ -1,0 +1,511 @@
+"""bench.py -- W4A8 FastGEMM on B200: LLaMA-13B decoder-layer linears at decode M.
+
+Workload (BASELINE.json configs[1], "LLaMA-13B linear shapes decode sweep M=1..64 on
+1xB200"): one STEP is one decoder layer's linear stack at decode batch M (default 16):
+    act_quant(x[M,5120])  -> qkv     GEMM (N=15360, K=5120)
+    act_quant(h[M,5120])  -> o       GEMM (N=5120,  K=5120)
+    act_quant(h[M,5120])  -> gate_up GEMM (N=27648, K=5120)
+    act_quant(g[M,13824]) -> down    GEMM (N=5120,  K=13824)
+i.e. 8 sm_100a kernel launches streaming 158.6 MB of INT4 weights.  Attention / norm /
+SiLU are outside the metric, so the step's inputs are fixed
+synthetic fp16 activations.
+
+value  = algorithmic HBM bytes of the step / device time (CUDA events, CUDA-graph
+         replay, max over ranks), GB/s.  Bytes per GEMM = N*K/2 + M*K + 4N + 4M + 2*M*N;
+         per act-quant = 2*M*K + M*K + 4M.
+e2e    = the same bytes / wall time of the reference-facing C ABI with HOST buffers
+         (ody_tensor_create -> ody_quantize_activations -> ody_gemm(FAST) -> host f32),
+         H2D of the f32 activations and D2H of the f32 outputs inside the timed region.
+L2     : every step streams 158.6 MB of weights (> 126 MB L2) and steps rotate over
+         4 distinct weight copies (634 MB), so no weight byte is an L2 hit.
+N > 1  : Megatron TP of the same layer (qkv/gate_up column-, o/down row-parallel with
+         the bit-exact int32 NCCL all-reduce); strong scaling (total work fixed).
+--impl reference: the reference's own CPU engine (oracle/_ref/libodyssey_ref.so, its
+         C ABI: ody_quantize_activations + ody_gemm(ODY_ENGINE_FAST)) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HIDDEN, INTER = 5120, 13824
+LAYERS = [("qkv", 3 * HIDDEN, HIDDEN), ("o", HIDDEN, HIDDEN), ("gate_up", 2 * INTER, HIDDEN),
+          ("down", HIDDEN, INTER)]
+METRIC = "W4A8 GEMM HBM GB/s (LLaMA-13B decoder-layer linears, decode)"
+
+
+def gemm_bytes(m, n, k):
+    return n * k // 2 + m * k + 4 * n + 4 * m + 2 * m * n
+
+
+def actq_bytes(m, k):
+    return 2 * m * k + m * k + 4 * m
+
+
+def step_bytes(m, world=1):
+    tot = 0
+    for _, n, k in LAYERS:
+        tot += gemm_bytes(m, n, k) + actq_bytes(m, k)
+    return tot
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        try:  # NVML: ~1 ms per query, so even a short timed region gets many samples
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                    ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                    ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                    ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx), hex(r)] +
+                                 ["Active" if r & b else "Not Active" for _, b in bits])
+                self._stop.wait(0.002)
+            return
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            pass
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "error": getattr(self, "err", None)}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------- B200 arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_09550_b200 import device as dev
+    from paper_2311_09550_b200._lib import lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m = args.m
+    torch.manual_seed(1234)
+    copies = args.copies
+
+    # ---- weights: synthetic 0.1*N(0,1) f32, quantized + prepacked on the device ----
+    layers = []  # per copy: list of (name, W4Weight or tp layer)
+    if world == 1:
+        for _ in range(copies):
+            per = []
+            for name, n, k in LAYERS:
+                w = torch.randn((n, k), device="cuda") * 0.1
+                per.append((name, dev.W4Weight.quantize(w)))
+                del w
+            layers.append(per)
+    else:
+        from paper_2311_09550_b200.tp import TPDecoderLinears
+        for _ in range(copies):
+            ws = [torch.randn((n, k), device="cuda") * 0.1 for _, n, k in LAYERS]
+            layers.append(TPDecoderLinears(*ws))
+            del ws
+    torch.cuda.synchronize()
+
+    xs = {k: (torch.randn((m, k), device="cuda") * 2).to(torch.float16) for k in (HIDDEN, INTER)}
+    a_buf = {k: dev.A8(torch.empty(lib().ody_dev_a8_bytes(m, k), dtype=torch.uint8, device="cuda"),
+                       torch.empty(m, dtype=torch.float32, device="cuda"), m, k)
+             for k in (HIDDEN, INTER)}
+    outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
+    ws_buf = dev.Workspace.get(max(m, 1), 27648, INTER, "cuda")
+    stream = torch.cuda.Stream()
+    launches_per_step = 0
+
+    def step(copy_idx, pdl):
+        nonlocal launches_per_step
+        if world == 1:
+            cnt = 0
+            for name, w in layers[copy_idx]:
+                a = a_buf[w.k]
+                dev.act_quant(xs[w.k], out=a, pdl=pdl, stream=stream)
+                dev.w4a8_gemm(a, w, out=outs[name], pdl=pdl, stream=stream, workspace=ws_buf)
+                cnt += 2
+            launches_per_step = cnt
+        else:
+            layers[copy_idx](xs[HIDDEN])
+
+    # ---- warmup (eager), then capture one graph per weight copy ----
+    with torch.cuda.stream(stream):
+        for i in range(max(args.warmup, 1)):
+            step(i % copies, args.pdl)
+    torch.cuda.synchronize()
+    graphs = []
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
+        for c in range(copies):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(c, args.pdl)
+            graphs.append(g)
+        for i in range(args.warmup):
+            with torch.cuda.stream(stream):
+                graphs[i % copies].replay()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for i in range(args.steps):
+                if use_graph:
+                    graphs[i % copies].replay()
+                else:
+                    step(i % copies, args.pdl)
+            end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_bytes = step_bytes(m)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "s8 x s4(widened to s8) -> s32 accum, fp16 io",
+        "data": "synthetic: x fp16 2*N(0,1), W f32 0.1*N(0,1) quantized on device",
+        "config": {"workload": "llama13b_decoder_layer_linears_decode", "M": m,
+                   "layers": {nm: [n, k] for nm, n, k in LAYERS}, "hidden": HIDDEN,
+                   "intermediate": INTER, "parallelism": f"tp{world}" if world > 1 else "single",
+                   "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
+                   "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
+                   "cuda_graph": use_graph, "pdl": bool(args.pdl)},
+        "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * args.steps if world == 1 else None,
+    }
+
+    if rank == 0 and world == 1:
+        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m)
+        result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
+        result["e2e"] = e2e_c_abi(args, m)
+        if not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline(args, m)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def _graph_time(fn, stream, reps, warm=3):
+    import torch
+    with torch.cuda.stream(stream):
+        for _ in range(warm):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    with torch.cuda.stream(stream):
+        g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m):
+    """Dominant kernel = the FastGEMM (HBM-bound at decode).  Its average launch
+    duration is timed with CUDA events on its own stream over graph replays that
+    rotate all weight copies (each launch streams fresh weights from HBM)."""
+    hbm, kind = peaks()
+    per = {}
+    tot_bytes = 0.0
+    tot_ms = 0.0
+    for li, (name, n, k) in enumerate(LAYERS):
+        ws = [layers[c][li][1] for c in range(len(layers))]
+
+        def fn(ws=ws, name=name, k=k):
+            for w in ws:
+                dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=ws_buf)
+
+        ms = _graph_time(fn, stream, reps=max(5, args.steps // 2)) / len(ws)
+        b = gemm_bytes(m, n, k)
+        per[name] = {"N": n, "K": k, "us": round(ms * 1e3, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1),
+                     "frac": round(b / (ms * 1e-3) / 1e9 / hbm, 4)}
+        tot_bytes += b
+        tot_ms += ms
+    achieved = tot_bytes / (tot_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(f"M{m}")
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
+            "kernel": "w4a8_gemm_kernel (avg over the 4 layer shapes, bytes-weighted)",
+            "per_shape": per,
+            "algorithmic_bytes_per_launch": {nm: gemm_bytes(m, n, k) for nm, n, k in LAYERS}}
+
+
+def decode_sweep(args, dev, layers, stream):
+    """GB/s of each layer GEMM for M = 1..64 (configs[1] sweep)."""
+    import torch
+    from paper_2311_09550_b200._lib import lib
+    hbm, _ = peaks()
+    res = {}
+    for m in (1, 2, 4, 8, 16, 32, 64):
+        ws_buf = dev.Workspace.get(m, 27648, INTER, "cuda")
+        row = {}
+        for li, (name, n, k) in enumerate(LAYERS):
+            x = (torch.randn((m, k), device="cuda")).to(torch.float16)
+            a = dev.act_quant(x)
+            out = torch.empty((m, n), dtype=torch.float16, device="cuda")
+            ws = [layers[c][li][1] for c in range(len(layers))]
+
+            def fn(ws=ws):
+                for w in ws:
+                    dev.w4a8_gemm(a, w, out=out, stream=stream, workspace=ws_buf)
+
+            ms = _graph_time(fn, stream, reps=10) / len(ws)
+            gbs = gemm_bytes(m, n, k) / (ms * 1e-3) / 1e9
+            row[name] = {"us": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3)}
+        res[f"M{m}"] = row
+    _ = lib
+    return res
+
+
+def e2e_c_abi(args, m):
+    """Through the reference-facing C ABI with host buffers (api.py over ody_*)."""
+    import numpy as np
+
+    from paper_2311_09550_b200 import api
+    rs = np.random.default_rng(7)
+    wq = []
+    for _, n, k in LAYERS:  # offline weight quantization (not timed, as in the reference flow)
+        w = (rs.standard_normal((n, k), dtype=np.float32) * 0.1).astype(np.float32)
+        wq.append(api.quantize_weights(w))
+        del w
+    xs = {k: (rs.standard_normal((m, k), dtype=np.float32) * 2) for k in (HIDDEN, INTER)}
+    h2d = sum(m * k * 4 for _, _, k in LAYERS)
+    d2h = sum(m * n * 4 for _, n, _ in LAYERS)
+
+    def one():
+        for (_, n, k), w in zip(LAYERS, wq):
+            aq = api.quantize_activations_per_token(api.Tensor(xs[k]))
+            api.gemm_w4a8_fast(aq, w)
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    reps = max(5, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(step_bytes(m) / dt / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 4),
+            "path": "C ABI ody_tensor_create/ody_quantize_activations/ody_gemm(FAST), host f32 in/out",
+            "timing": "host wall clock (the C-ABI calls are synchronous)"}
+
+
+# --------------------------------------------------------------- CPU reference
+class CpuReference:
+    """The reference's CPU engine on the layer shapes, inputs prepared once.
+
+    kind "reference": oracle/_ref/libodyssey_ref.so (the reference compiled from its
+    own sources, driven through its C ABI); else "port": the pinned C restatement."""
+
+    def __init__(self, m, threads, layers):
+        from oracle.oracle import REF_SO, Oracle, RefCAPI
+        self.m, self.threads = m, threads
+        self.orc = Oracle()
+        self.ref = RefCAPI() if os.path.exists(REF_SO) else None
+        self.kind = "reference" if self.ref is not None else "port"
+        os.environ["ODYSSEY_THREADS"] = str(threads)
+        if self.ref is not None:
+            self.ref.L.ody_set_threads(threads)
+        self.prep = {}
+        for name, n, k in LAYERS:
+            if name not in layers:
+                continue
+            a, w = self.orc.bench_inputs(1, m, n, k)
+            if self.ref is not None:
+                ah, wh = self.ref.tensor(a), self.ref.tensor(w)
+                wq = self.ref.quantize_weights(wh)  # offline, untimed
+                self.ref.free_tensor(wh)
+                self.prep[name] = (n, k, ah, wq)
+            else:
+                _, packed, sw = self.orc.quantize_weights(w)
+                self.prep[name] = (n, k, a, (packed, sw))
+
+    def run(self, name):
+        """One act quant + FAST GEMM of layer `name`; returns (bytes, seconds)."""
+        n, k, a, wq = self.prep[name]
+        m = self.m
+        if self.ref is not None:
+            t0 = time.perf_counter()
+            aq = self.ref.quantize_activations(a)
+            self.ref.gemm_fast(aq, wq, m, n)
+            dt = time.perf_counter() - t0
+            self.ref.free_qtensor(aq)
+        else:
+            packed, sw = wq
+            t0 = time.perf_counter()
+            codes, sa = self.orc.quantize_activations(a)
+            self.orc.fast_gemm(codes, sa, packed, sw, m, n, k, threads=self.threads)
+            dt = time.perf_counter() - t0
+        return gemm_bytes(m, n, k) + actq_bytes(m, k), dt
+
+
+def cpu_baseline(args, m):
+    threads = os.cpu_count() or 1
+    names = ["o", "down"]
+    cpu = CpuReference(m, threads, names)
+    cpu.run("o")  # warm
+    b = s = 0
+    for nm in names:
+        bb, ss = cpu.run(nm)
+        b += bb
+        s += ss
+    return {"value": round(b / s / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": cpu.kind,
+            "sample": f"one pass of the {'+'.join(names)} linears (act quant + FAST GEMM) at M={m}, "
+                      f"f32 host inputs, ODYSSEY_THREADS={threads}; the reference parallelises over "
+                      f"M rows only and unpacks nibbles serially (ref gemm.cpp:219-225)",
+            "seconds": round(s, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    m = args.m
+    threads = os.cpu_count() or 1
+    cpu = CpuReference(m, threads, [nm for nm, _, _ in LAYERS])
+    kind = cpu.kind
+    for i in range(args.warmup):
+        cpu.run(LAYERS[i % len(LAYERS)][0])
+    times, tot_b = [], 0
+    for i in range(args.steps):
+        b, s = cpu.run(LAYERS[i % len(LAYERS)][0])
+        times.append(s)
+        tot_b += b
+    secs = sum(times)
+    value = tot_b / secs / 1e9
+    sample = (f"each step = one of the layer's 4 linears in rotation (act quant + FAST GEMM, "
+              f"M={m}), reference C ABI on {threads} host threads")
+    out = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "s8 x s4 -> s32 (CPU)",
+           "data": "synthetic: ref Rng(seed^0x9d2c5680) a~N(0,1), w~0.1 N(0,1)",
+           "config": {"workload": "llama13b_decoder_layer_linears_decode", "M": m,
+                      "layers": {nm: [n, k] for nm, n, k in LAYERS}},
+           "impl": "reference",
+           "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+                            "sample": sample},
+           "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--m", type=int, default=16, help="decode batch (tokens) per step")
+    ap.add_argument("--copies", type=int, default=4, help="distinct weight copies rotated")
+    ap.add_argument("--sweep", action="store_true", help="also report the M=1..64 GEMM sweep")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

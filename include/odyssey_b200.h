@@ -123,6 +123,16 @@ ody_status ody_dev_row_absmax(const void* x, ody_dtype dtype, size_t ldx, size_t
  * gamma/beta optional per-row device arrays. bits must be 4. */
 ody_status ody_dev_w4_quantize(const float* w, size_t n, size_t k, const float* gamma,
                                const float* beta, void* w_packed, float* s_w, void* stream);
+/* K2 with caller-supplied per-row scales (device array s_w, n floats): only the codes
+ * clamp(round(w/s), -8, 7) are produced.  Row-parallel TP quantizes each K-shard with
+ * the scale of the FULL row so the shards concatenate to the unsharded codes. */
+ody_status ody_dev_w4_quantize_with_scales(const float* w, size_t n, size_t k, const float* s_w,
+                                           void* w_packed, void* stream);
+/* K4 alone: out = float(acc >> 4) * (s_a[i] * s_w[j]) from int32 accumulators (the
+ * row-parallel TP epilogue after the bit-exact int32 SUM all-reduce). */
+ody_status ody_dev_dequant_epilogue(const int32_t* acc, const float* s_a, const float* s_w,
+                                    size_t m, size_t n, ody_dtype out_dtype, void* out,
+                                    void* stream);
 /* K2 prepack only: reference flat PackedInt4Buffer bytes ((n*k+1)/2, element 2i low
  * nibble) -> tile layout; and the inverse for export / parity. */
 ody_status ody_dev_w4_prepack(const void* flat_nibbles, size_t n, size_t k, void* w_packed,
@@ -140,6 +150,13 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
                              void* out, int32_t* acc_out, void* workspace,
                              size_t workspace_bytes, int max_ctas, int pdl, void* stream);
 ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream);
+/* Diagnostics: when buf (device, >= 8 * #CTAs u64) is non-NULL, subsequent
+ * ody_dev_w4a8_gemm launches record a per-CTA %globaltimer timeline into it:
+ * [entry, setup done, first data at MMA, last MMA commit, epilogue done, exit,
+ *  producer done, units | segments << 32].  NULL disables (the default). */
+void ody_dev_set_trace(void* buf);
+/* Diagnostics: act-quant launches record [entry, exit] %globaltimer per CTA (NULL = off). */
+void ody_dev_set_act_trace(void* buf);
 
 /* Inspection: activation codes back to row-major int8 (and/or dequantized f32). */
 ody_status ody_dev_a8_unpack(const void* q, const float* s, size_t m, size_t k, int8_t* codes,

@@ -300,3 +300,11 @@ uint64_t oracle_fnv1a(const void* data, size_t bytes) {
     }
     return h;
 }
+
+/* quantize.cpp:37-47 with the scale supplied by the caller: the row-parallel TP
+ * restatement (scale of the full row applied to a K-shard). */
+void oracle_quantize_with_scale(const float* x, size_t n, int bits, float scale, int8_t* codes) {
+    const int32_t lo = -(1 << (bits - 1));
+    const int32_t hi = (1 << (bits - 1)) - 1;
+    for (size_t i = 0; i < n; ++i) codes[i] = (int8_t)clamp_code(x[i] / scale, lo, hi);
+}

@@ -61,6 +61,7 @@ class Oracle:
         L.oracle_gemm_w4a8_fast.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                             c_size_t, c_size_t, c_int, c_void_p]
         L.oracle_dequantize_rows.argtypes = [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p]
+        L.oracle_quantize_with_scale.argtypes = [c_void_p, c_size_t, c_int, c_float, c_void_p]
         L.oracle_fnv1a.argtypes = [c_void_p, c_size_t]
         L.oracle_fnv1a.restype = c_uint64
         self.L = L
@@ -104,6 +105,15 @@ class Oracle:
         if rc:
             raise ValueError("oracle_quantize_symmetric: invalid argument")
         return codes, np.float32(s.value)
+
+    def quantize_with_scales(self, x: np.ndarray, scales: np.ndarray, bits: int) -> np.ndarray:
+        """Per-row codes clamp(round(x/S_r)) under given scales."""
+        x = np.ascontiguousarray(x, np.float32)
+        codes = np.empty(x.shape, np.int8)
+        for r in range(x.shape[0]):
+            self.L.oracle_quantize_with_scale(x[r].ctypes.data, x.shape[1], bits, float(scales[r]),
+                                              codes[r].ctypes.data)
+        return codes
 
     def quantize_activations(self, a: np.ndarray):
         a = np.ascontiguousarray(a, np.float32)

@@ -56,12 +56,18 @@ SIGNATURES = {
     "ody_dev_row_absmax": (c_int, [c_void_p, c_int, c_size_t, c_size_t, c_size_t, c_void_p, c_void_p]),
     "ody_dev_w4_quantize": (c_int, [c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p]),
+    "ody_dev_w4_quantize_with_scales": (c_int, [c_void_p, c_size_t, c_size_t, c_void_p, c_void_p,
+                                                c_void_p]),
+    "ody_dev_dequant_epilogue": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_int,
+                                         c_void_p, c_void_p]),
     "ody_dev_w4_prepack": (c_int, [c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]),
     "ody_dev_w4_unpack": (c_int, [c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]),
     "ody_dev_w4a8_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t,
                                   c_size_t, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_int,
                                   c_int, c_void_p]),
     "ody_dev_workspace_init": (c_int, [c_void_p, c_size_t, c_void_p]),
+    "ody_dev_set_trace": (None, [c_void_p]),
+    "ody_dev_set_act_trace": (None, [c_void_p]),
     "ody_dev_a8_unpack": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p,
                                   c_void_p]),
     "ody_qtensor_export": (c_int, [c_void_p, c_void_p, c_void_p]),

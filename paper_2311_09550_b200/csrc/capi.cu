@@ -27,6 +27,7 @@ using namespace odyb200;
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long* g_trace = nullptr;  // ody_dev_set_trace (diagnostics only)
 
 struct Fail : std::runtime_error {
     ody_status code;
@@ -485,6 +486,32 @@ ody_status ody_dev_w4_quantize(const float* w, size_t n, size_t k, const float* 
     });
 }
 
+ody_status ody_dev_w4_quantize_with_scales(const float* w, size_t n, size_t k, const float* s_w,
+                                           void* w_packed, void* stream) {
+    if (!w || !w_packed || !s_w) return einval("ody_dev_w4_quantize_with_scales: null argument");
+    if (n == 0 || k == 0) return einval("quantize_weights: empty tensor");
+    return guarded([&] {
+        cuda_check(launch_w4_quant_prepack(w, static_cast<int>(n), static_cast<int>(k), 4, nullptr,
+                                           nullptr, static_cast<uint8_t*>(w_packed),
+                                           const_cast<float*>(s_w), nullptr,
+                                           static_cast<cudaStream_t>(stream), true),
+                   "w4 quantize launch");
+    });
+}
+
+ody_status ody_dev_dequant_epilogue(const int32_t* acc, const float* s_a, const float* s_w,
+                                    size_t m, size_t n, ody_dtype out_dtype, void* out,
+                                    void* stream) {
+    if (!acc || !s_a || !s_w || !out) return einval("ody_dev_dequant_epilogue: null argument");
+    if (out_dtype < ODY_DTYPE_F32 || out_dtype > ODY_DTYPE_BF16) return einval("bad out dtype");
+    return guarded([&] {
+        cuda_check(launch_dequant_epilogue(acc, s_a, s_w, static_cast<int>(m), static_cast<int>(n),
+                                           static_cast<int>(out_dtype), out,
+                                           static_cast<cudaStream_t>(stream)),
+                   "epilogue launch");
+    });
+}
+
 ody_status ody_dev_w4_prepack(const void* flat, size_t n, size_t k, void* w_packed, void* stream) {
     if (!flat || !w_packed) return einval("ody_dev_w4_prepack: null argument");
     return guarded([&] {
@@ -530,11 +557,15 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
         g.K = static_cast<int>(k);
         g.max_ctas = max_ctas;
         g.pdl = pdl != 0;
+        g.trace = g_trace;
         if (workspace_bytes < gemm_workspace_bytes(g.M, g.N, g.K, max_ctas))
             fail(ODY_EINVAL, "ody_dev_w4a8_gemm: workspace too small");
         cuda_check(launch_w4a8_gemm(g, static_cast<cudaStream_t>(stream)), "w4a8_gemm launch");
     });
 }
+
+void ody_dev_set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
+void ody_dev_set_act_trace(void* buf) { set_act_trace(static_cast<unsigned long long*>(buf)); }
 
 ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream) {
     if (!workspace) return einval("ody_dev_workspace_init: null argument");

@@ -6,22 +6,24 @@
 //     out[i][j] = float(acc) * (sa[i] * sw[j])
 //
 // B200 mapping (swap-AB, weights are the MMA "A" operand, tokens the MMA "N"):
-//   * producer warp: 1-D bulk copies (cp.async.bulk -> UBLKCP) of one 8 KiB packed-INT4
-//     weight block (128 rows x 128 k) and the matching activation k-block
-//     (BN tokens x 128 B, pre-swizzled SWIZZLE_128B) into an S-stage smem ring;
+//   * producer warp: 1-D bulk copies (cp.async.bulk -> UBLKCP) of up to two 8 KiB
+//     packed-INT4 weight blocks (128 rows x 128 k each, contiguous) and the matching
+//     activation k-blocks (BN tokens x 128 B, pre-swizzled SWIZZLE_128B) into an S-stage
+//     smem ring.  A "unit" is one or two k-blocks;
 //   * converter warps (2 groups x 4 warps, one warp per TMEM sub-partition): read the
-//     packed block from smem, widen SINT4 -> S8 with the paper's high-nibble trick
+//     packed blocks from smem, widen SINT4 -> S8 with the paper's high-nibble trick
 //     ((w<<4)&0xF0F0F0F0 and w&0xF0F0F0F0 -- lanes hold value*16, no per-group scale
 //     multiply), and tcgen05.st the int8 lanes straight into TMEM as the A operand;
-//   * MMA warp (one elected thread): tcgen05.mma.kind::i8 with A from TMEM, B from
-//     smem, int32 accumulators D in TMEM (double-buffered);
-//   * epilogue warps: tcgen05.ld D, >>4, *(sa*sw) with IEEE RN multiplies, store
-//     f32/f16/bf16 -- or, for stream-K partial tiles, red.add.s32 into an L2-resident
-//     workspace; the CTA that completes a tile's K range finalises it (integer
-//     addition is associative, so split-K is bit-exact) and re-zeroes the workspace.
+//   * MMA warp (one elected lane, warp-uniform control flow): tcgen05.mma.kind::i8 with
+//     A from TMEM, B from smem, int32 accumulators in TMEM (double-buffered, split over
+//     independent chains so back-to-back MMAs do not serialise on one accumulator);
+//   * epilogue warps: tcgen05.ld D, sum chains, >>4, *(sa*sw) with IEEE RN multiplies,
+//     store f32/f16/bf16 -- or, for stream-K partial tiles, red.add.s32 into an
+//     L2-resident workspace; the CTA that completes a tile's K range finalises it
+//     (integer addition is associative, so split-K is bit-exact) and re-zeroes it.
 //   * scheduling: persistent grid of <= #SMs CTAs; full waves of (n_tile, m_tile)
 //     tiles are data-parallel, the remainder (all tiles for decode shapes) is split
-//     stream-K over 128-k units, so every SM streams the same number of weight bytes.
+//     stream-K over 128-k blocks, so every SM streams the same number of weight bytes.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -44,16 +46,29 @@ constexpr int kWarpAlloc = 2;
 constexpr int kWarpConv0 = 4;      // warps 4..11: two converter groups of 4
 constexpr int kConvGroups = 2;
 constexpr int kWarpEpi0 = 12;      // warps 12..15
-constexpr int kAStages = 4;        // TMEM A stages (32 columns each)
+constexpr int kUnitBlocks = 2;     // k-blocks per pipeline unit (256 k, 16 KiB of weights)
+constexpr int kAStages = 4;        // TMEM A stages (64 columns each)
+constexpr int kAStageCols = kUnitBlocks * kBlockK / 4;
 constexpr int kTmemCols = 512;
-constexpr int kAColBase = 256;     // A stages live at columns 256..383
+constexpr int kAColBase = 256;     // A stages live at columns 256..511
 constexpr int kSmemBudget = 200 * 1024;
+// diagnostics layout of the trace buffer (ody_dev_set_trace)
+constexpr int kTraceCta = 8;                         // [cta][8] globaltimer slots
+constexpr int kTraceUnits = 148 * kTraceCta;         // CTA 0: per-unit converter clock64 x4
+constexpr int kTraceEpi = kTraceUnits + 64 * 4;      // per CTA, per segment epilogue x4
+constexpr int kTraceMma = kTraceEpi + 148 * 16;      // CTA 0: per-unit MMA clock64 x4
+static_assert(kAColBase + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
 
 template <int BN>
 struct Cfg {
-    static constexpr int kBBytes = BN * 128;                   // activation k-block tile
-    static constexpr int kStageBytes = kBBytes + kWBlockBytes; // B first (1024-aligned)
-    static constexpr int kStages = std::min(16, kSmemBudget / kStageBytes);
+    static constexpr int kBBytes = BN * 128;                          // one activation k-block
+    static constexpr int kStageBytes = kUnitBlocks * (kBBytes + kWBlockBytes);
+    static constexpr int kWOff = kUnitBlocks * kBBytes;               // weights after B tiles
+    static constexpr int kStages = std::min(12, kSmemBudget / kStageBytes);
+    // Accumulator chains (chunk c -> chain c % kChains, summed in the epilogue).  The
+    // tensor pipe pipelines dependent kind::i8 accumulations (measured: 10 cycles per
+    // 128x16x32 MMA with 1 or 4 chains, tools/mma_bench.cu), so one chain suffices.
+    static constexpr int kChains = 1;
     static constexpr int kBarrierBytes = 1024;
     static constexpr int kSmemBytes = kStages * kStageBytes + kBarrierBytes + 1024;  // +align
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
@@ -61,7 +76,7 @@ struct Cfg {
                                        (static_cast<uint32_t>(BN >> 3) << 17) |
                                        (static_cast<uint32_t>(128 >> 4) << 24);
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 128, "BN");
-    static_assert(kBBytes % 1024 == 0, "swizzle atom alignment");
+    static_assert(kBBytes % 1024 == 0 && kStageBytes % 1024 == 0, "swizzle atom alignment");
 };
 
 struct Params {
@@ -77,18 +92,24 @@ struct Params {
     int M, N, K, Mp;
     int kblocks, m_tiles, tiles, dp_tiles, sk_units;
     int pdl;
+    unsigned long long* trace;  // optional timeline, see ody_dev_set_trace
 };
 
-// Walks this CTA's segments: data-parallel tiles first, then its stream-K unit range.
+// Walks this CTA's segments: data-parallel tiles first, then its stream-K block range.
+// The stream-K range is walked BACKWARDS, so a CTA's final segment is the one that
+// holds the last k-block of its tile: that CTA is the tile's owner, and the other
+// contributors covered the tile's first blocks as the FIRST work of their own ranges,
+// i.e. long before the owner finishes.  The owner then only adds their (already
+// published) partial sums to its own accumulators -- no fixup after the mainloop.
 struct SegIter {
     int tile, kb0, kb1;
-    int dp_next, u, u_end;
+    int dp_next, u_lo, u;
     __device__ void init(const Params& p) {
         const int P = gridDim.x, b = blockIdx.x;
         dp_next = b;
         const long long su = p.sk_units;
-        u = static_cast<int>(su * b / P);
-        u_end = static_cast<int>(su * (b + 1) / P);
+        u_lo = static_cast<int>(su * b / P);
+        u = static_cast<int>(su * (b + 1) / P);
     }
     __device__ bool next(const Params& p) {
         if (dp_next < p.dp_tiles) {
@@ -98,12 +119,13 @@ struct SegIter {
             dp_next += gridDim.x;
             return true;
         }
-        if (u >= u_end) return false;
-        const int t = u / p.kblocks;
+        if (u <= u_lo) return false;
+        const int t = (u - 1) / p.kblocks;
+        const int base = t * p.kblocks;
         tile = p.dp_tiles + t;
-        kb0 = u - t * p.kblocks;
-        kb1 = min(p.kblocks, kb0 + (u_end - u));
-        u += kb1 - kb0;
+        kb0 = max(u_lo, base) - base;
+        kb1 = u - base;
+        u = base + kb0;
         return true;
     }
 };
@@ -115,12 +137,14 @@ __device__ __forceinline__ uint64_t b_desc(uint32_t smem_addr) {
            (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
 }
 
-__device__ __forceinline__ void store_out(const Params& p, int t, int n, int32_t acc) {
+// sa_t / sw_n are loaded before the accumulators are ready (off the critical path).
+__device__ __forceinline__ void store_out(const Params& p, int t, int n, int32_t acc, float sa_t,
+                                          float sw_n) {
     const size_t idx = static_cast<size_t>(t) * p.N + n;
     if (p.acc_out) p.acc_out[idx] = acc;
     if (p.out) {
         const int32_t sh = acc >> 4;  // exact (ref gemm.cpp:269)
-        const float v = __fmul_rn(__int2float_rn(sh), __fmul_rn(__ldg(p.sa + t), __ldg(p.sw + n)));
+        const float v = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa_t, sw_n));
         if (p.out_dtype == kDtypeF32)
             static_cast<float*>(p.out)[idx] = v;
         else if (p.out_dtype == kDtypeF16)
@@ -146,14 +170,21 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     uint64_t* d_empty = d_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
     volatile uint32_t* fin_flag = tmem_slot + 1;
+    const uint32_t stage_base = smem_u32(stages);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    unsigned long long* trc = p.trace;
+    if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 0] = globaltimer();
+    // PDL: let the next kernel in the stream get scheduled immediately; it only
+    // prefetches independent data before its own griddepcontrol.wait, which waits
+    // for this grid's completion (and memory flush), so this is always safe.
+    if (p.pdl) pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::kStages; ++i) {
             mbar_init(&w_full[i], 1);
-            mbar_init(&w_empty[i], 4 + 1);  // 4 converter warps + MMA commit
+            mbar_init(&w_empty[i], 1);  // MMA commit (converters finished reading before MMA)
         }
         for (int i = 0; i < kAStages; ++i) {
             mbar_init(&a_full[i], 4);
@@ -172,7 +203,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = lds32(smem_u32(tmem_slot));
+    if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 1] = globaltimer();
 
     SegIter it;
     it.init(p);
@@ -181,52 +213,97 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         if (lane == 0) {
             const uint64_t pol_w = l2_policy_evict_first();
             const uint64_t pol_a = l2_policy_evict_last();
-            if (p.pdl) pdl_wait();
+            // Weights do not depend on the previous kernel: with PDL, stream the first
+            // ring's worth of weight blocks while the producer of the activations is
+            // still finishing, then wait for it and fetch the activation tiles.
+            int pre = 0;
+            if (p.pdl) {
+                SegIter ip = it;
+                bool more = true;
+                while (more && pre < C::kStages && ip.next(p)) {
+                    const int nt = ip.tile / p.m_tiles;
+                    for (int kb = ip.kb0; kb < ip.kb1; kb += kUnitBlocks) {
+                        if (pre >= C::kStages) {
+                            more = false;
+                            break;
+                        }
+                        const int nb = min(kUnitBlocks, ip.kb1 - kb);
+                        mbar_expect_tx(&w_full[pre], nb * (C::kBBytes + kWBlockBytes));
+                        bulk_g2s(stages + pre * C::kStageBytes + C::kWOff,
+                                 p.wp + (static_cast<size_t>(nt) * p.kblocks + kb) * kWBlockBytes,
+                                 nb * kWBlockBytes, &w_full[pre], pol_w);
+                        ++pre;
+                    }
+                }
+                pdl_wait();
+            }
             int u = 0;
             while (it.next(p)) {
                 const int nt = it.tile / p.m_tiles, mt = it.tile % p.m_tiles;
                 const uint8_t* wsrc = p.wp + (static_cast<size_t>(nt) * p.kblocks) * kWBlockBytes;
                 const int8_t* asrc = p.qa + static_cast<size_t>(mt) * BN * 128;
-                for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
+                for (int kb = it.kb0; kb < it.kb1; kb += kUnitBlocks, ++u) {
+                    const int nb = min(kUnitBlocks, it.kb1 - kb);
                     const int s = u % C::kStages;
-                    mbar_wait(&w_empty[s], ((u / C::kStages) & 1) ^ 1);
                     uint8_t* st = stages + s * C::kStageBytes;
-                    mbar_expect_tx(&w_full[s], C::kStageBytes);
-                    bulk_g2s(st, asrc + static_cast<size_t>(kb) * p.Mp * 128, C::kBBytes, &w_full[s],
-                             pol_a);
-                    bulk_g2s(st + C::kBBytes, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
-                             kWBlockBytes, &w_full[s], pol_w);
+                    if (u >= pre) {
+                        mbar_wait(&w_empty[s], ((u / C::kStages) & 1) ^ 1);
+                        mbar_expect_tx(&w_full[s], nb * (C::kBBytes + kWBlockBytes));
+                        bulk_g2s(st + C::kWOff, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
+                                 nb * kWBlockBytes, &w_full[s], pol_w);
+                    }
+                    for (int b = 0; b < nb; ++b)
+                        bulk_g2s(st + b * C::kBBytes, asrc + static_cast<size_t>(kb + b) * p.Mp * 128,
+                                 C::kBBytes, &w_full[s], pol_a);
                 }
             }
+            if (trc) trc[blockIdx.x * kTraceCta + 6] = globaltimer();
         }
     } else if (warp == kWarpMma) {
-        if (lane == 0) {
-            int u = 0, j = 0;
-            const uint32_t stage_base = smem_u32(stages);
-            while (it.next(p)) {
-                const int db = j & 1;
-                mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
+        // Whole warp runs the (warp-uniform) loop; one elected lane issues tcgen05.
+        int u = 0, j = 0;
+        while (it.next(p)) {
+            const int db = j & 1;
+            mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + db * C::kChains * BN;
+            for (int kb = it.kb0; kb < it.kb1; kb += kUnitBlocks, ++u) {
+                const int nb = min(kUnitBlocks, it.kb1 - kb);
+                const int s = u % C::kStages;
+                const int as = u % kAStages;
+                const bool mtr = trc && blockIdx.x == 0 && u < 64 && lane == 0;
+                if (mtr) trc[kTraceMma + u * 4 + 0] = clock64();
+                // a_full(u) is arrived by converters that already observed w_full(u)
+                // (the B tile shares that stage barrier), so one wait covers both.
+                mbar_wait(&a_full[as], (u / kAStages) & 1);
+                if (mtr) trc[kTraceMma + u * 4 + 1] = clock64();
+                if (u == 0 && trc && lane == 0) trc[blockIdx.x * kTraceCta + 2] = globaltimer();
+                if (mtr) trc[kTraceUnits + u * 4 + 3] = clock64();
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + db * BN;
-                for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
-                    const int s = u % C::kStages;
-                    const int as = u % kAStages;
-                    mbar_wait(&w_full[s], (u / C::kStages) & 1);
-                    mbar_wait(&a_full[as], (u / kAStages) & 1);
-                    tc_fence_after();
-                    const uint32_t b_addr = stage_base + s * C::kStageBytes;
-                    const uint32_t a_tmem = tmem + kAColBase + as * 32;
+                const uint32_t b_addr = stage_base + s * C::kStageBytes;
+                const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
+                if (elect_one()) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b_addr + 32 * c), C::kIdesc,
-                                  (kb > it.kb0 || c > 0) ? 1u : 0u);
+                    for (int c = 0; c < 4 * kUnitBlocks; ++c) {
+                        if (c < 4 * nb)
+                            mma_i8_ts(d_tmem + (c % C::kChains) * BN, a_tmem + 8 * c,
+                                      b_desc(b_addr + (c / 4) * C::kBBytes + 32 * (c % 4)),
+                                      C::kIdesc, (kb > it.kb0 || c >= C::kChains) ? 1u : 0u);
                     }
                     mma_commit(&a_empty[as]);
                     mma_commit(&w_empty[s]);
                 }
-                mma_commit(&d_full[db]);
-                ++j;
+                __syncwarp();
+                if (mtr) trc[kTraceMma + u * 4 + 2] = clock64();
             }
+            if (elect_one()) mma_commit(&d_full[db]);
+            __syncwarp();
+            ++j;
+        }
+        if (trc && lane == 0) {
+            trc[blockIdx.x * kTraceCta + 3] = globaltimer();
+            trc[blockIdx.x * kTraceCta + 7] =
+                static_cast<unsigned long long>(u) | (static_cast<unsigned long long>(j) << 32);
         }
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kConvGroups) {
         const int g = (warp - kWarpConv0) / 4;
@@ -235,36 +312,52 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
         int u = 0;
         while (it.next(p)) {
-            for (int kb = it.kb0; kb < it.kb1; ++kb, ++u) {
+            for (int kb = it.kb0; kb < it.kb1; kb += kUnitBlocks, ++u) {
                 if ((u % kConvGroups) != g) continue;
+                const int nb = min(kUnitBlocks, it.kb1 - kb);
                 const int s = u % C::kStages;
                 const int as = u % kAStages;
                 mbar_wait(&w_full[s], (u / C::kStages) & 1);
-                const uint4* src = reinterpret_cast<const uint4*>(stages + s * C::kStageBytes +
-                                                                  C::kBBytes + r * 16);
-                uint32_t lanes8[32];
+                const bool tr = trc && blockIdx.x == 0 && u < 64 && q == 0 && lane == 0;
+                if (tr) trc[kTraceUnits + u * 4 + 0] = clock64();
+                const uint32_t src = stage_base + s * C::kStageBytes + C::kWOff + r * 16;
+                uint32_t lanes8[kUnitBlocks][32];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint4 v = src[c * (2048 / 16)];
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                for (int b = 0; b < kUnitBlocks; ++b) {
+                    if (b < nb) {
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        lanes8[c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k = 8jj+0..3
-                        lanes8[c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k = 8jj+4..7
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 v = lds128(src + b * kWBlockBytes + c * 2048);
+                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) {
+                                lanes8[b][c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k 8jj+0..3
+                                lanes8[b][c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k 8jj+4..7
+                            }
+                        }
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&w_empty[s]);
                 mbar_wait(&a_empty[as], ((u / kAStages) & 1) ^ 1);
+                if (tr) trc[kTraceUnits + u * 4 + 1] = clock64();
                 tc_fence_after();
-                tmem_st_32x32b_x32(t_lane + kAColBase + as * 32, lanes8);
+                const uint32_t dst = t_lane + kAColBase + as * kAStageCols;
+                tmem_st_32x32b_x32(dst, lanes8[0]);
+                if (nb > 1) tmem_st_32x32b_x32(dst + 32, lanes8[1]);
                 tmem_wait_st();
+                if (tr) trc[kTraceUnits + u * 4 + 2] = clock64();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[as]);
             }
         }
     } else if (warp >= kWarpEpi0) {
+        // Epilogue.  Three segment kinds:
+        //   full     -- this CTA owns all k-blocks of the tile: store directly;
+        //   partial  -- publish int32 partials (red.add into the zeroed workspace), then
+        //               a release increment of the tile's block counter;
+        //   owner    -- holds the tile's last k-block (always its final segment): wait
+        //               for counter == kb0 (the other contributors' blocks), add their
+        //               partials to its own accumulators, store, re-zero the workspace.
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
@@ -272,25 +365,72 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         int j = 0;
         while (it.next(p)) {
             const int db = j & 1;
-            mbar_wait(&d_full[db], (j >> 1) & 1);
-            tc_fence_after();
             const int nt = it.tile / p.m_tiles, mt = it.tile % p.m_tiles;
             const int n = nt * kTileN + r;
             const int t0 = mt * BN;
             const bool full = (it.kb0 == 0 && it.kb1 == p.kblocks);
+            const bool owner = !full && it.kb1 == p.kblocks;
             const int skt = it.tile - p.dp_tiles;
             int32_t* ws = p.ws_acc + static_cast<size_t>(skt) * BN * kTileN;
-#pragma unroll 1
+            const bool etr = trc && warp == kWarpEpi0 && lane == 0 && j < 4;
+            unsigned long long* et = trc + kTraceEpi + (blockIdx.x * 4 + j) * 4;
+            constexpr int kPre = BN < 32 ? BN : 32;  // partial columns prefetched in registers
+            int32_t pre[kPre];
+            if (owner) {
+                // Usually already satisfied: the other contributors processed this tile's
+                // head as the first work of their ranges.
+                if (warp == kWarpEpi0 && lane == 0) {
+                    const uint32_t want = static_cast<uint32_t>(it.kb0);
+                    while (ld_acquire_u32(p.ws_cnt + skt) < want) __nanosleep(64);
+                }
+                named_bar_sync(1, 128);
+                fence_acq_rel_gpu();
+#pragma unroll
+                for (int i = 0; i < kPre; ++i) pre[i] = __ldcg(ws + i * kTileN + r);
+                if (etr) et[2] = globaltimer();
+            }
+            // scales for this tile, fetched while the MMAs finish
+            const float sw_n = (full || owner) && n < p.N ? __ldg(p.sw + n) : 0.0f;
+            float sa_pre[kPre];
+#pragma unroll
+            for (int i = 0; i < kPre; ++i)
+                sa_pre[i] = (full || owner) && t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f;
+            mbar_wait(&d_full[db], (j >> 1) & 1);
+            if (etr) et[0] = globaltimer();
+            tc_fence_after();
+#pragma unroll
             for (int tc = 0; tc < BN; tc += 16) {
                 uint32_t v[16];
-                tmem_ld_32x32b_x16(t_lane + db * BN + tc, v);
+                tmem_ld_32x32b_x16(t_lane + db * C::kChains * BN + tc, v);
+#pragma unroll
+                for (int ch = 1; ch < C::kChains; ++ch) {
+                    uint32_t w[16];
+                    tmem_ld_32x32b_x16(t_lane + (db * C::kChains + ch) * BN + tc, w);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] += w[i];  // exact int32 (mod 2^32)
+                }
                 tmem_wait_ld();
-                if (full) {
+                if (full || owner) {
+                    if (owner) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int c = tc + i;
+                            const int32_t part = c < kPre ? pre[c < kPre ? c : 0]
+                                                          : __ldcg(ws + c * kTileN + r);
+                            v[i] += static_cast<uint32_t>(part);
+                            __stcg(ws + c * kTileN + r, 0);
+                        }
+                    }
                     if (n < p.N) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int t = t0 + tc + i;
-                            if (t < p.M) store_out(p, t, n, static_cast<int32_t>(v[i]));
+                            if (t < p.M) {
+                                const float sa_t = tc + i < kPre ? sa_pre[tc + i < kPre ? tc + i : 0]
+                                                                 : __ldg(p.sa + t);
+                                store_out(p, t, n, static_cast<int32_t>(v[i]), sa_t, sw_n);
+                            }
                         }
                     }
                 } else {
@@ -302,36 +442,26 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[db]);
-            if (!full) {
-                __threadfence();
+            if (etr) et[1] = globaltimer();
+            if (!full && !owner) {
+                __threadfence();  // this thread's partials are visible before the count
                 named_bar_sync(1, 128);
-                if (warp == kWarpEpi0 && lane == 0) {
-                    const uint32_t add = static_cast<uint32_t>(it.kb1 - it.kb0);
-                    const uint32_t old = atomicAdd(p.ws_cnt + skt, add);
-                    *fin_flag = (old + add == static_cast<uint32_t>(p.kblocks)) ? 1u : 0u;
-                }
-                named_bar_sync(1, 128);
-                if (*fin_flag) {
-                    __threadfence();
-                    for (int tt = 0; tt < BN; ++tt) {
-                        int32_t* cell = ws + tt * kTileN + r;
-                        const int32_t acc = __ldcg(cell);
-                        __stcg(cell, 0);
-                        const int t = t0 + tt;
-                        if (t < p.M && n < p.N) store_out(p, t, n, acc);
-                    }
-                    if (warp == kWarpEpi0 && lane == 0) p.ws_cnt[skt] = 0u;
-                }
-                named_bar_sync(1, 128);
+                if (warp == kWarpEpi0 && lane == 0)
+                    red_release_add_u32(p.ws_cnt + skt, static_cast<uint32_t>(it.kb1 - it.kb0));
+            } else if (owner) {
+                if (warp == kWarpEpi0 && lane == 0) p.ws_cnt[skt] = 0u;
             }
+            if (etr) et[3] = globaltimer() | (static_cast<unsigned long long>(owner) << 63);
             ++j;
         }
+        if (trc && warp == kWarpEpi0 && lane == 0) trc[blockIdx.x * kTraceCta + 4] = globaltimer();
     }
 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
+    if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 5] = globaltimer();
 }
 
 template <int BN>
@@ -413,6 +543,7 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     p.ws_acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(a.workspace) +
                                           round_up(static_cast<size_t>(sms) * sizeof(uint32_t), 256));
     p.pdl = a.pdl ? 1 : 0;
+    p.trace = a.trace;
     switch (bn) {
         case 16: return launch_bn<16>(p, P, a.pdl, st);
         case 32: return launch_bn<32>(p, P, a.pdl, st);

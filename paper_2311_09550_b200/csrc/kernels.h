@@ -14,13 +14,19 @@ enum : int { kDtypeF32 = 0, kDtypeF16 = 1, kDtypeBF16 = 2 };
 cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K, int8_t* q,
                              float* s, const float* absmax_in, float* absmax_out, bool pdl,
                              cudaStream_t st);
+void set_act_trace(unsigned long long* buf);  // diagnostics: per-CTA entry/exit globaltimer
 cudaError_t launch_row_absmax(const void* x, int dtype, size_t ldx, int M, int K, float* out,
                               cudaStream_t st);
 
 // K2: per-channel INT4 quantization + prepack; flat-nibble prepack / unpack; dequant.
+// scales_given: s already holds the per-row scales (row-parallel TP shards quantize
+// with the scale of the FULL row), only the codes are produced.
 cudaError_t launch_w4_quant_prepack(const float* w, int N, int K, int bits, const float* gamma,
                                     const float* beta, uint8_t* packed, float* s, int* err,
-                                    cudaStream_t st);
+                                    cudaStream_t st, bool scales_given = false);
+// int32 accumulators -> float(acc>>4)*(sa*sw) as f32/f16/bf16 (row-parallel TP epilogue).
+cudaError_t launch_dequant_epilogue(const int32_t* acc, const float* sa, const float* sw, int M,
+                                    int N, int out_dtype, void* out, cudaStream_t st);
 cudaError_t launch_w4_prepack_flat(const uint8_t* flat, int N, int K, uint8_t* packed,
                                    cudaStream_t st);
 cudaError_t launch_w4_unpack_flat(const uint8_t* packed, int N, int K, uint8_t* flat,
@@ -44,6 +50,7 @@ struct GemmArgs {
     int M, N, K;
     int max_ctas;         // 0 = number of SMs
     bool pdl;             // programmatic dependent launch
+    unsigned long long* trace;  // optional: 8 globaltimer slots per CTA (diagnostics)
 };
 size_t gemm_workspace_bytes(int M, int N, int K, int num_sms);
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st);

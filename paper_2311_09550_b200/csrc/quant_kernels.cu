@@ -9,6 +9,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "layout.h"
 #include "ptx.cuh"
@@ -65,69 +67,95 @@ __device__ __forceinline__ void load16(const T* __restrict__ row, int k0, int K,
     }
 }
 
-// K1: one CTA per token row.  Pass 1 absmax (warp-shuffle + smem), pass 2
-// divide/round/clamp and 128-bit stores into the swizzled a8 k-block layout.
-// absmax_in (optional) supplies a precomputed row max (row-parallel TP: the
-// all-reduced global max of a K-sharded row).  absmax_out (optional) exports it.
-template <typename T>
-__global__ void __launch_bounds__(kActThreads)
+// Exact fast path for clamp(roundf(fl(x / S))): with r = RN(1/S), q' = RN(x * r) is
+// within |x/S| * 1.8e-7 <= 2.3e-5 of fl(x/S) (|x/S| <= 127.0001 since S = max|x|/127).
+// roundf(q') can only differ from roundf(fl(x/S)) when a half-integer lies within that
+// distance, so those rare elements (and a non-finite r) take the IEEE division.
+__device__ __forceinline__ int32_t quant_code_i8(float x, float scale, float rcp, bool exact) {
+    const float qa = __fmul_rn(x, rcp);
+    const float a = fabsf(qa);
+    const float f = a - truncf(a);
+    if (exact || fabsf(f - 0.5f) < 6.0e-5f) return clamp_code(x / scale, -128, 127);
+    return clamp_code(qa, -128, 127);
+}
+
+// K1: per-token INT8 quantization, one CTA of NT threads per token row; every thread
+// keeps its MC 16-element chunks in registers across both passes.  Pass 1: row
+// max|x| (warp shuffle -> smem).  Pass 2: codes clamp(roundf(x/S)) (exact fast path
+// above), one 128-bit store per chunk into the swizzled a8 k-block layout.
+// absmax_in (optional) supplies the row max (row-parallel TP: the all-reduced global
+// max of a K-sharded row); absmax_out (optional) exports it.  With PDL the kernel
+// lets its consumer launch immediately and waits for its producer before touching x.
+template <typename T, int NT, int MC>
+__global__ void __launch_bounds__(NT)
 act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int Mp,
                  int8_t* __restrict__ q, float* __restrict__ s,
                  const float* __restrict__ absmax_in, float* __restrict__ absmax_out,
-                 int pdl) {
-    if (pdl) pdl_wait();
+                 int pdl, unsigned long long* __restrict__ trace) {
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8] = globaltimer();
+    if (pdl) {
+        pdl_launch_dependents();  // let the consumer GEMM start streaming its weights now
+        pdl_wait();
+    }
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8 + 2] = globaltimer();
     const int t = blockIdx.x;
     const T* row = x + static_cast<size_t>(t) * ldx;
-    __shared__ float red[kActThreads / 32];
-    __shared__ float s_shared;
+    __shared__ float red[NT / 32];
     const int nchunks = Kp / 16;
 
+    float v[MC][16];
+    float mx = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MC; ++i) {
+        const int c = threadIdx.x + i * NT;
+        if (c < nchunks) {
+            load16(row, c * 16, K, v[i]);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(v[i][e]));
+        }
+    }
     float scale;
     if (absmax_in) {
         scale = absmax_in[t] / 127.0f;
     } else {
-        float mx = 0.0f;
-        for (int c = threadIdx.x; c < nchunks; c += kActThreads) {
-            if (c * 16 >= K) break;
-            float v[16];
-            load16(row, c * 16, K, v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fabsf(v[i]));
-        }
         mx = warp_max(mx);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            float m = red[0];
+        float m = red[0];
 #pragma unroll
-            for (int i = 1; i < kActThreads / 32; ++i) m = fmaxf(m, red[i]);
-            s_shared = m;
-            if (absmax_out) absmax_out[t] = m;
-        }
-        __syncthreads();
+        for (int i = 1; i < NT / 32; ++i) m = fmaxf(m, red[i]);
         // max(|max|,|min|) == max|x| for finite rows (ref quantize.cpp:27-33)
-        scale = s_shared / 127.0f;
+        scale = m / 127.0f;
+        if (threadIdx.x == 0 && absmax_out) absmax_out[t] = m;
     }
     if (!(scale > 0.0f)) scale = kMinScale;
     if (threadIdx.x == 0) s[t] = scale;
-    if (pdl) pdl_launch_dependents();
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8 + 3] = globaltimer();
+    const float rcp = 1.0f / scale;
+    const bool exact = !(rcp < INFINITY);
 
-    for (int c = threadIdx.x; c < nchunks; c += kActThreads) {
-        float v[16];
-        load16(row, c * 16, K, v);
-        uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            uint32_t acc = 0;
+    for (int i = 0; i < MC; ++i) {
+        const int c = threadIdx.x + i * NT;
+        if (c < nchunks) {
+            uint32_t w[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                int32_t code = clamp_code(v[i * 4 + b] / scale, -128, 127);
-                acc |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * b);
+            for (int j = 0; j < 4; ++j) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int32_t code = quant_code_i8(v[i][j * 4 + b], scale, rcp, exact);
+                    acc |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * b);
+                }
+                w[j] = acc;
             }
-            w[i] = acc;
+            const size_t off = a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, Mp);
+            *reinterpret_cast<uint4*>(q + off) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        const size_t off = a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, Mp);
-        *reinterpret_cast<uint4*>(q + off) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    if (trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace[blockIdx.x * 8 + 1] = globaltimer();
     }
 }
 
@@ -272,6 +300,23 @@ __global__ void a8_unpack_kernel(const int8_t* __restrict__ q, const float* __re
     if (deq) deq[i] = static_cast<float>(c) * s[t];
 }
 
+// Dequantizing epilogue on int32 accumulators (row-parallel TP: after the int32 SUM
+// all-reduce of the K-sharded partial accumulators).  ref gemm.cpp:269-273.
+__global__ void dequant_epilogue_kernel(const int32_t* __restrict__ acc, const float* __restrict__ sa,
+                                        const float* __restrict__ sw, int M, int N, int out_dtype,
+                                        void* __restrict__ out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<size_t>(M) * N) return;
+    const int t = static_cast<int>(i / N), n = static_cast<int>(i % N);
+    const float v = __fmul_rn(__int2float_rn(acc[i] >> 4), __fmul_rn(sa[t], sw[n]));
+    if (out_dtype == kDtypeF32)
+        static_cast<float*>(out)[i] = v;
+    else if (out_dtype == kDtypeF16)
+        static_cast<__half*>(out)[i] = __float2half_rn(v);
+    else
+        static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+}
+
 // Row absmax only (for row-parallel TP: local max before the MAX all-reduce).
 template <typename T>
 __global__ void __launch_bounds__(kActThreads)
@@ -295,15 +340,41 @@ row_absmax_kernel(const T* __restrict__ x, size_t ldx, int K, float* __restrict_
     }
 }
 
+unsigned long long* g_act_trace = nullptr;  // diagnostics: [cta][entry, exit]
+
 }  // namespace
+
+void set_act_trace(unsigned long long* buf) { g_act_trace = buf; }
+
+template <int NT, int MC>
+cudaError_t launch_act_quant_cfg(cudaLaunchConfig_t& cfg, const void* x, int dtype, size_t ldx,
+                                 int M, int K, int Kp, int Mp, int8_t* q, float* s,
+                                 const float* absmax_in, float* absmax_out, int p) {
+    cfg.blockDim = dim3(NT);
+    switch (dtype) {
+        case kDtypeF32:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<float, NT, MC>,
+                                      static_cast<const float*>(x), ldx, M, K, Kp, Mp, q, s,
+                                      absmax_in, absmax_out, p, g_act_trace);
+        case kDtypeF16:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__half, NT, MC>,
+                                      static_cast<const __half*>(x), ldx, M, K, Kp, Mp, q, s,
+                                      absmax_in, absmax_out, p, g_act_trace);
+        case kDtypeBF16:
+            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__nv_bfloat16, NT, MC>,
+                                      static_cast<const __nv_bfloat16*>(x), ldx, M, K, Kp, Mp, q,
+                                      s, absmax_in, absmax_out, p, g_act_trace);
+    }
+    return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K, int8_t* q,
                              float* s, const float* absmax_in, float* absmax_out, bool pdl,
                              cudaStream_t st) {
     const int Kp = static_cast<int>(pad_k(K)), Mp = static_cast<int>(pad_m(M));
+    const int chunks = Kp / 16;  // 16-element chunks per row, held in registers
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(M);
-    cfg.blockDim = dim3(kActThreads);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -311,20 +382,25 @@ cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K,
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     const int p = pdl ? 1 : 0;
-    switch (dtype) {
-        case kDtypeF32:
-            return cudaLaunchKernelEx(&cfg, act_quant_kernel<float>, static_cast<const float*>(x),
-                                      ldx, M, K, Kp, Mp, q, s, absmax_in, absmax_out, p);
-        case kDtypeF16:
-            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__half>,
-                                      static_cast<const __half*>(x), ldx, M, K, Kp, Mp, q, s,
-                                      absmax_in, absmax_out, p);
-        case kDtypeBF16:
-            return cudaLaunchKernelEx(&cfg, act_quant_kernel<__nv_bfloat16>,
-                                      static_cast<const __nv_bfloat16*>(x), ldx, M, K, Kp, Mp, q,
-                                      s, absmax_in, absmax_out, p);
-    }
-    return cudaErrorInvalidValue;
+    if (chunks <= 128)
+        return launch_act_quant_cfg<128, 1>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                            absmax_out, p);
+    if (chunks <= 256)
+        return launch_act_quant_cfg<256, 1>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                            absmax_out, p);
+    if (chunks <= 512)
+        return launch_act_quant_cfg<512, 1>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                            absmax_out, p);
+    if (chunks <= 1024)
+        return launch_act_quant_cfg<512, 2>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                            absmax_out, p);
+    if (chunks <= 4096)
+        return launch_act_quant_cfg<512, 8>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                            absmax_out, p);
+    if (chunks <= 8192)
+        return launch_act_quant_cfg<1024, 8>(cfg, x, dtype, ldx, M, K, Kp, Mp, q, s, absmax_in,
+                                             absmax_out, p);
+    return cudaErrorInvalidValue;  // K > 131072 (beyond the reference's 2^17 bound)
 }
 
 cudaError_t launch_row_absmax(const void* x, int dtype, size_t ldx, int M, int K, float* out,
@@ -350,9 +426,9 @@ cudaError_t launch_row_absmax(const void* x, int dtype, size_t ldx, int M, int K
 
 cudaError_t launch_w4_quant_prepack(const float* w, int N, int K, int bits, const float* gamma,
                                     const float* beta, uint8_t* packed, float* s, int* err,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, bool scales_given) {
     const int Np = static_cast<int>(pad_n(N)), Kp = static_cast<int>(pad_k(K));
-    w_scale_kernel<<<(N + 7) / 8, 256, 0, st>>>(w, N, K, bits, gamma, beta, s, err);
+    if (!scales_given) w_scale_kernel<<<(N + 7) / 8, 256, 0, st>>>(w, N, K, bits, gamma, beta, s, err);
     const size_t total = static_cast<size_t>(Np) * (Kp / 32);
     w4_quant_prepack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
         w, N, K, Np, Kp, s, packed);
@@ -381,6 +457,14 @@ cudaError_t launch_w4_dequant(const uint8_t* packed, const float* s, int N, int 
     const size_t total = static_cast<size_t>(N) * K;
     w4_dequant_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
         packed, s, N, K, static_cast<int>(pad_k(K)), out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_epilogue(const int32_t* acc, const float* sa, const float* sw, int M,
+                                    int N, int out_dtype, void* out, cudaStream_t st) {
+    const size_t total = static_cast<size_t>(M) * N;
+    dequant_epilogue_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        acc, sa, sw, M, N, out_dtype, out);
     return cudaGetLastError();
 }
 

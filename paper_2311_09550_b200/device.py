@@ -73,6 +73,19 @@ class W4Weight:
         return W4Weight(packed, s, n, k)
 
     @staticmethod
+    def quantize_with_scales(w: torch.Tensor, scales: torch.Tensor, stream=None) -> "W4Weight":
+        """Codes of ``w`` under given per-row scales (a K-shard of a row-parallel layer
+        quantized with its FULL row's scale)."""
+        _require_cuda(w, "w")
+        w = w.contiguous().float()
+        n, k = w.shape
+        s = scales.contiguous().float().clone()
+        packed = torch.empty(lib().ody_dev_w4_bytes(n, k), dtype=torch.uint8, device=w.device)
+        check(lib().ody_dev_w4_quantize_with_scales(w.data_ptr(), n, k, s.data_ptr(),
+                                                    packed.data_ptr(), _stream(stream)))
+        return W4Weight(packed, s, n, k)
+
+    @staticmethod
     def from_flat(flat: torch.Tensor, scales: torch.Tensor, n: int, k: int,
                   stream=None) -> "W4Weight":
         """Reference PackedInt4Buffer bytes ((n*k+1)//2) + scales -> prepacked."""
@@ -170,6 +183,17 @@ def w4a8_gemm(a: A8, w: W4Weight, out_dtype=torch.float16, out: torch.Tensor | N
         _DT[out_dtype], y_ptr, acc.data_ptr() if acc is not None else None, ws.data_ptr(),
         ws.numel(), max_ctas, int(pdl), _stream(stream)))
     return acc if accumulators else out
+
+
+def dequant_epilogue(acc: torch.Tensor, sa: torch.Tensor, sw: torch.Tensor, out_dtype=torch.float16,
+                     stream=None) -> torch.Tensor:
+    """K4 alone on int32 accumulators: float(acc >> 4) * (sa[i] * sw[j])."""
+    _require_cuda(acc, "acc")
+    m, n = acc.shape
+    out = torch.empty((m, n), dtype=out_dtype, device=acc.device)
+    check(lib().ody_dev_dequant_epilogue(acc.contiguous().data_ptr(), sa.data_ptr(), sw.data_ptr(),
+                                         m, n, _DT[out_dtype], out.data_ptr(), _stream(stream)))
+    return out
 
 
 class W4A8Linear:

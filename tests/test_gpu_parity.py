@@ -208,6 +208,30 @@ def test_input_dtypes_bit_exact(oracle, torch_cuda, dev):
         assert np.array_equal(bits_of(aq.s.cpu().numpy()), bits_of(sa))
 
 
+def test_act_quant_rounding_boundaries(oracle, torch_cuda, dev):
+    """Adversarial K1 inputs: x/S lands on / next to every half-integer, where the
+    reciprocal fast path must defer to IEEE division to stay bit-exact."""
+    torch = torch_cuda
+    rs = np.random.default_rng(11)
+    rows = []
+    for r in range(64):
+        absmax = np.float32(rs.uniform(0.01, 100.0))
+        S = np.float32(absmax / np.float32(127.0))
+        half = (np.arange(-127, 127, dtype=np.float32) + np.float32(0.5)) * S
+        row = np.concatenate([half, np.nextafter(half, np.float32(np.inf)),
+                              np.nextafter(half, np.float32(-np.inf)),
+                              rs.uniform(-absmax, absmax, 256).astype(np.float32)])
+        row = np.clip(row, -absmax, absmax).astype(np.float32)
+        row[0] = absmax
+        rows.append(row)
+    x = np.stack(rows).astype(np.float32)
+    codes, sa = oracle.quantize_activations(x)
+    aq = dev.act_quant(torch.from_numpy(x).cuda())
+    assert np.array_equal(bits_of(aq.s.cpu().numpy()), bits_of(sa))
+    got = aq.codes().cpu().numpy()
+    assert np.array_equal(got, codes), int((got != codes).sum())
+
+
 def test_absmax_override_row_parallel(oracle, torch_cuda, dev):
     """K-sharded row quantized with the global max gives the full-row codes."""
     torch = torch_cuda
