@@ -177,7 +177,7 @@ def run_b200(args):
                        torch.empty(m, dtype=torch.float32, device="cuda"), m, k)
              for k in (HIDDEN, INTER)}
     outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
-    ws_buf = dev.Workspace.get(max(m, 1), 27648, INTER, "cuda")
+    ws_buf = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
     stream = torch.cuda.Stream()
     launches_per_step = 0
 
@@ -333,7 +333,7 @@ def decode_sweep(args, dev, layers, stream):
     hbm, _ = peaks()
     res = {}
     for m in (1, 2, 4, 8, 16, 32, 64):
-        ws_buf = dev.Workspace.get(m, 27648, INTER, "cuda")
+        ws_buf = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
         row = {}
         for li, (name, n, k) in enumerate(LAYERS):
             x = (torch.randn((m, k), device="cuda")).to(torch.float16)

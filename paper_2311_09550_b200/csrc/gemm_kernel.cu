@@ -29,7 +29,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "kernels.h"
 #include "layout.h"
@@ -43,6 +45,7 @@ constexpr int kNumThreads = 512;   // 16 warps
 constexpr int kWarpProducer = 0;
 constexpr int kWarpMma = 1;
 constexpr int kWarpAlloc = 2;
+constexpr int kWarpFixup = 3;      // gathers other CTAs' stream-K partials for owned tiles
 constexpr int kWarpConv0 = 4;      // warps 4..11: two converter groups of 4
 constexpr int kConvGroups = 2;
 constexpr int kWarpEpi0 = 12;      // warps 12..15
@@ -56,7 +59,8 @@ constexpr int kSmemBudget = 200 * 1024;
 constexpr int kTraceCta = 8;                         // [cta][8] globaltimer slots
 constexpr int kTraceUnits = 148 * kTraceCta;         // CTA 0: per-unit converter clock64 x4
 constexpr int kTraceEpi = kTraceUnits + 64 * 4;      // per CTA, per segment epilogue x4
-constexpr int kTraceMma = kTraceEpi + 148 * 16;      // CTA 0: per-unit MMA clock64 x4
+constexpr int kTraceMma = kTraceEpi + 148 * 16;
+constexpr int kTraceDbg = kTraceMma + 64 * 4;    // per CTA: epilogue clock64 checkpoints  // (epi: 3 segs x 4 + fixup slot 15)      // CTA 0: per-unit MMA clock64 x4
 static_assert(kAColBase + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
 
 template <int BN>
@@ -64,13 +68,21 @@ struct Cfg {
     static constexpr int kBBytes = BN * 128;                          // one activation k-block
     static constexpr int kStageBytes = kUnitBlocks * (kBBytes + kWBlockBytes);
     static constexpr int kWOff = kUnitBlocks * kBBytes;               // weights after B tiles
-    static constexpr int kStages = std::min(12, kSmemBudget / kStageBytes);
+    // Owned stream-K tile: the fixup warp bulk-copies the other contributors' partial
+    // sums (kSlotBytes each, kStageSlots at a time) into smem and adds them into
+    // fix_buf.  For BN=128 (prefill remainder tiles) the owner reads them directly.
+    static constexpr int kSlotBytes = BN * kTileN * 4;
+    static constexpr bool kBulkFix = BN <= 64;
+    static constexpr int kStageSlots = BN == 16 ? 4 : (BN == 32 ? 2 : 1);
+    static constexpr int kFixBytes = kBulkFix ? kSlotBytes * (1 + kStageSlots) : 0;
+    static constexpr int kStages = std::min(12, (kSmemBudget - kFixBytes) / kStageBytes);
     // Accumulator chains (chunk c -> chain c % kChains, summed in the epilogue).  The
     // tensor pipe pipelines dependent kind::i8 accumulations (measured: 10 cycles per
     // 128x16x32 MMA with 1 or 4 chains, tools/mma_bench.cu), so one chain suffices.
     static constexpr int kChains = 1;
     static constexpr int kBarrierBytes = 1024;
-    static constexpr int kSmemBytes = kStages * kStageBytes + kBarrierBytes + 1024;  // +align
+    static constexpr int kSmemBytes =
+        kStages * kStageBytes + kFixBytes + kBarrierBytes + 1024;  // +align
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                        (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -86,11 +98,14 @@ struct Params {
     const float* sw;
     void* out;
     int32_t* acc_out;
-    int32_t* ws_acc;
-    uint32_t* ws_cnt;
+    int32_t* ws_slots;   // [sk tile][contributor slot][BN][128] int32 partial sums
+    uint32_t* ws_cnt;    // [sk tile] k-blocks published by non-owners (owner resets to 0)
+    int max_contrib;     // contributor slots per stream-K tile
     int out_dtype;
     int M, N, K, Mp;
     int kblocks, m_tiles, tiles, dp_tiles, sk_units;
+    int split;           // 0: stream-K; >= 1: DP waves + remainder tiles split over
+                         // clusters of `split` CTAs, reduced through DSMEM
     int pdl;
     unsigned long long* trace;  // optional timeline, see ody_dev_set_trace
 };
@@ -101,17 +116,43 @@ struct Params {
 // contributors covered the tile's first blocks as the FIRST work of their own ranges,
 // i.e. long before the owner finishes.  The owner then only adds their (already
 // published) partial sums to its own accumulators -- no fixup after the mainloop.
+//
+// "DP + cluster split" mode (p.split >= 1, decode widths): full waves of tiles are
+// data-parallel; each remaining tile r goes to cluster r, whose S CTAs each take 1/S of
+// its k-blocks and reduce through distributed shared memory -- no global fixup at all.
 struct SegIter {
     int tile, kb0, kb1;
     int dp_next, u_lo, u;
+    int split_left;  // DP+split mode: the remainder segment of this CTA not yet returned
+    bool is_split;   // the current segment is a cluster-split remainder segment
     __device__ void init(const Params& p) {
         const int P = gridDim.x, b = blockIdx.x;
         dp_next = b;
         const long long su = p.sk_units;
         u_lo = static_cast<int>(su * b / P);
         u = static_cast<int>(su * (b + 1) / P);
+        split_left = (p.split >= 1 && b / p.split < p.tiles - p.dp_tiles) ? 1 : 0;
+        is_split = false;
     }
     __device__ bool next(const Params& p) {
+        is_split = false;
+        if (dp_next < p.dp_tiles) {
+            tile = dp_next;
+            kb0 = 0;
+            kb1 = p.kblocks;
+            dp_next += gridDim.x;
+            return true;
+        }
+        if (p.split >= 1) {  // rank r of cluster c owns k-blocks [r*kb/S, (r+1)*kb/S) of tile c
+            if (!split_left) return false;
+            split_left = 0;
+            const int r = blockIdx.x % p.split;
+            tile = p.dp_tiles + blockIdx.x / p.split;
+            kb0 = r * p.kblocks / p.split;
+            kb1 = (r + 1) * p.kblocks / p.split;
+            is_split = p.split > 1;
+            return true;
+        }
         if (dp_next < p.dp_tiles) {
             tile = dp_next;
             kb0 = 0;
@@ -129,6 +170,17 @@ struct SegIter {
         return true;
     }
 };
+
+// Stream-K partition: CTA b owns units [lo(b), lo(b+1)).
+__device__ __forceinline__ int sk_lo(const Params& p, int b) {
+    return static_cast<int>(static_cast<long long>(p.sk_units) * b / gridDim.x);
+}
+__device__ __forceinline__ int sk_cta_of_unit(const Params& p, int u) {
+    int b = static_cast<int>(static_cast<long long>(u) * gridDim.x / p.sk_units);
+    while (b + 1 < static_cast<int>(gridDim.x) && sk_lo(p, b + 1) <= u) ++b;
+    while (b > 0 && sk_lo(p, b) > u) --b;
+    return b;
+}
 
 __device__ __forceinline__ uint64_t b_desc(uint32_t smem_addr) {
     // K-major SWIZZLE_128B: start>>4, LBO unused, SBO = 1024 B (8 rows x 128 B),
@@ -161,15 +213,19 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* stages = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    int32_t* fix_buf = reinterpret_cast<int32_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kFixBytes);
     uint64_t* w_full = bars;
     uint64_t* w_empty = w_full + C::kStages;
     uint64_t* a_full = w_empty + C::kStages;
     uint64_t* a_empty = a_full + kAStages;
     uint64_t* d_full = a_empty + kAStages;
     uint64_t* d_empty = d_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-    volatile uint32_t* fin_flag = tmem_slot + 1;
+    uint64_t* fix_full = d_empty + 2;
+    uint64_t* fix_tx = fix_full + 1;
+    uint64_t* recv_full = fix_tx + 1;  // cluster split-K: partials of ranks 1..S-1 landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 1);
     const uint32_t stage_base = smem_u32(stages);
 
     const int warp = threadIdx.x >> 5;
@@ -194,6 +250,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], 4);
         }
+        mbar_init(fix_full, 1);
+        mbar_init(fix_tx, 1);
+        mbar_init(recv_full, p.split > 1 ? 4 * (p.split - 1) : 1);
         fence_mbar_init();
     }
     if (warp == kWarpAlloc) {
@@ -202,6 +261,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     }
     tc_fence_before();
     __syncthreads();
+    if (p.split > 1) cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
     tc_fence_after();
     const uint32_t tmem = lds32(smem_u32(tmem_slot));
     if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 1] = globaltimer();
@@ -350,17 +410,75 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                 if (lane == 0) mbar_arrive(&a_full[as]);
             }
         }
+    } else if (warp == kWarpFixup) {
+        // Gather the partial sums other CTAs published for the tile this CTA owns (its
+        // first stream-K segment in forward order, when that segment ends the tile and
+        // does not start it).  Runs concurrently with the mainloop: bulk copies bring the
+        // contributors' slots into smem and the warp adds them into fix_buf, so when the
+        // owner's accumulators are ready only one smem add remains.
+        const int b = blockIdx.x;
+        if (C::kBulkFix && p.sk_units > 0) {
+            const int lo = sk_lo(p, b), hi = sk_lo(p, b + 1);
+            const int t = lo / p.kblocks;
+            const int kb0 = lo - t * p.kblocks;
+            if (hi > lo && kb0 > 0 && hi >= (t + 1) * p.kblocks) {
+                const int bf = sk_cta_of_unit(p, t * p.kblocks);
+                const int nslots = b - bf;
+                if (p.pdl) pdl_wait();  // the previous launch has released the workspace
+                if (lane == 0) {
+                    while (ld_acquire_u32(p.ws_cnt + t) < static_cast<uint32_t>(kb0)) __nanosleep(64);
+                    fence_proxy_async_global();  // generic-proxy writes -> async-proxy reads
+                }
+                __syncwarp();
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(
+                    p.ws_slots + static_cast<size_t>(t) * p.max_contrib * BN * kTileN);
+                uint8_t* stage_slots = reinterpret_cast<uint8_t*>(fix_buf) + C::kSlotBytes;
+                const uint32_t fb = smem_u32(fix_buf), sb = smem_u32(stage_slots);
+                constexpr int n4 = C::kSlotBytes / 16;
+                uint32_t phase = 0;
+                for (int c0 = 0; c0 < nslots; c0 += C::kStageSlots) {
+                    const int nb = min(C::kStageSlots, nslots - c0);
+                    if (lane == 0) {
+                        mbar_expect_tx(fix_tx, nb * C::kSlotBytes);
+                        for (int i = 0; i < nb; ++i)
+                            bulk_g2s(stage_slots + i * C::kSlotBytes,
+                                     src + static_cast<size_t>(c0 + i) * C::kSlotBytes, C::kSlotBytes,
+                                     fix_tx, l2_policy_evict_first());
+                    }
+                    mbar_wait(fix_tx, phase);
+                    phase ^= 1;
+                    for (int i = lane; i < n4; i += 32) {
+                        uint4 acc = c0 == 0 ? make_uint4(0, 0, 0, 0) : lds128(fb + i * 16);
+                        for (int k = 0; k < nb; ++k) {
+                            const uint4 v = lds128(sb + k * C::kSlotBytes + i * 16);
+                            acc.x += v.x;
+                            acc.y += v.y;
+                            acc.z += v.z;
+                            acc.w += v.w;
+                        }
+                        sts128(fb + i * 16, acc);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    p.ws_cnt[t] = 0u;  // every contribution is consumed
+                    mbar_arrive(fix_full);
+                }
+                if (trc && lane == 0) trc[kTraceEpi + blockIdx.x * 16 + 15] = globaltimer();
+            }
+        }
     } else if (warp >= kWarpEpi0) {
         // Epilogue.  Three segment kinds:
-        //   full     -- this CTA owns all k-blocks of the tile: store directly;
-        //   partial  -- publish int32 partials (red.add into the zeroed workspace), then
-        //               a release increment of the tile's block counter;
-        //   owner    -- holds the tile's last k-block (always its final segment): wait
-        //               for counter == kb0 (the other contributors' blocks), add their
-        //               partials to its own accumulators, store, re-zero the workspace.
+        //   full     -- all k-blocks of the tile are this CTA's: store directly;
+        //   partial  -- publish the int32 partial sums into this CTA's slot of the tile
+        //               (plain stores), then a release increment of the tile's counter;
+        //   owner    -- holds the tile's last k-block (its final segment): add the other
+        //               contributors' sum (gathered into smem by the fixup warp) to its
+        //               own accumulators and store.
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
+        const uint32_t fix_base = smem_u32(fix_buf);
         if (p.pdl) pdl_wait();
         int j = 0;
         while (it.next(p)) {
@@ -368,35 +486,46 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             const int nt = it.tile / p.m_tiles, mt = it.tile % p.m_tiles;
             const int n = nt * kTileN + r;
             const int t0 = mt * BN;
-            const bool full = (it.kb0 == 0 && it.kb1 == p.kblocks);
-            const bool owner = !full && it.kb1 == p.kblocks;
+            const bool csplit = it.is_split;
+            const int crank = csplit ? static_cast<int>(blockIdx.x % p.split) : 0;
+            const bool full = csplit ? crank == 0 : (it.kb0 == 0 && it.kb1 == p.kblocks);
+            const bool owner = !csplit && !full && it.kb1 == p.kblocks;
             const int skt = it.tile - p.dp_tiles;
-            int32_t* ws = p.ws_acc + static_cast<size_t>(skt) * BN * kTileN;
-            const bool etr = trc && warp == kWarpEpi0 && lane == 0 && j < 4;
-            unsigned long long* et = trc + kTraceEpi + (blockIdx.x * 4 + j) * 4;
-            constexpr int kPre = BN < 32 ? BN : 32;  // partial columns prefetched in registers
-            int32_t pre[kPre];
-            if (owner) {
-                // Usually already satisfied: the other contributors processed this tile's
-                // head as the first work of their ranges.
-                if (warp == kWarpEpi0 && lane == 0) {
-                    const uint32_t want = static_cast<uint32_t>(it.kb0);
-                    while (ld_acquire_u32(p.ws_cnt + skt) < want) __nanosleep(64);
-                }
-                named_bar_sync(1, 128);
-                fence_acq_rel_gpu();
-#pragma unroll
-                for (int i = 0; i < kPre; ++i) pre[i] = __ldcg(ws + i * kTileN + r);
-                if (etr) et[2] = globaltimer();
-            }
+            const bool etr = trc && warp == kWarpEpi0 && lane == 0 && j < 3;
+            unsigned long long* et = trc + kTraceEpi + blockIdx.x * 16 + j * 4;
             // scales for this tile, fetched while the MMAs finish
+            constexpr int kPre = BN < 32 ? BN : 32;
             const float sw_n = (full || owner) && n < p.N ? __ldg(p.sw + n) : 0.0f;
             float sa_pre[kPre];
 #pragma unroll
             for (int i = 0; i < kPre; ++i)
                 sa_pre[i] = (full || owner) && t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f;
+            int32_t* slot = nullptr;
+            if (!full && !owner && !csplit) {
+                const int c = blockIdx.x - sk_cta_of_unit(p, skt * p.kblocks);
+                slot = p.ws_slots + (static_cast<size_t>(skt) * p.max_contrib + c) * BN * kTileN;
+            }
             mbar_wait(&d_full[db], (j >> 1) & 1);
             if (etr) et[0] = globaltimer();
+            if (owner && C::kBulkFix) {
+                mbar_wait(fix_full, 0);
+                if (etr) et[2] = globaltimer();
+            }
+            if (csplit && crank == 0) {
+                mbar_wait_cluster(recv_full, 0);
+                if (etr) et[2] = globaltimer();
+            }
+            int nslots_direct = 0;
+            const int32_t* slots_direct = nullptr;
+            if (owner && !C::kBulkFix) {  // BN=128: read the other contributors' slots here
+                if (warp == kWarpEpi0 && lane == 0)
+                    while (ld_acquire_u32(p.ws_cnt + skt) < static_cast<uint32_t>(it.kb0))
+                        __nanosleep(64);
+                named_bar_sync(1, 128);
+                fence_acq_rel_gpu();
+                nslots_direct = blockIdx.x - sk_cta_of_unit(p, skt * p.kblocks);
+                slots_direct = p.ws_slots + static_cast<size_t>(skt) * p.max_contrib * BN * kTileN;
+            }
             tc_fence_after();
 #pragma unroll
             for (int tc = 0; tc < BN; tc += 16) {
@@ -411,17 +540,30 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                     for (int i = 0; i < 16; ++i) v[i] += w[i];  // exact int32 (mod 2^32)
                 }
                 tmem_wait_ld();
+                if (etr && tc == 0) trc[kTraceDbg + blockIdx.x * 4 + 0] = clock64();
                 if (full || owner) {
-                    if (owner) {
+                    if (csplit) {
+                        for (int c = 0; c < p.split - 1; ++c) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int c = tc + i;
-                            const int32_t part = c < kPre ? pre[c < kPre ? c : 0]
-                                                          : __ldcg(ws + c * kTileN + r);
-                            v[i] += static_cast<uint32_t>(part);
-                            __stcg(ws + c * kTileN + r, 0);
+                            for (int i = 0; i < 16; ++i)
+                                v[i] += lds32(fix_base + ((c * BN + tc + i) * kTileN + r) * 4);
                         }
                     }
+                    if (owner && C::kBulkFix) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            v[i] += lds32(fix_base + ((tc + i) * kTileN + r) * 4);
+                    } else if (owner) {
+                        for (int c = 0; c < nslots_direct; ++c) {
+                            const int32_t* sl = slots_direct + static_cast<size_t>(c) * BN * kTileN;
+                            int32_t w[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) w[i] = __ldcg(sl + (tc + i) * kTileN + r);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) v[i] += static_cast<uint32_t>(w[i]);
+                        }
+                    }
+                    if (etr && tc == 0) trc[kTraceDbg + blockIdx.x * 4 + 1] = clock64();
                     if (n < p.N) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
@@ -433,22 +575,34 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                             }
                         }
                     }
+                } else if (csplit) {  // rank > 0: partials into rank 0's smem (DSMEM)
+                    const uint32_t dst0 =
+                        mapa_shared(fix_base + (((crank - 1) * BN + tc) * kTileN + r) * 4, 0);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) st_dsmem_u32(dst0 + i * kTileN * 4, v[i]);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        red_add_s32(ws + (tc + i) * kTileN + r, static_cast<int32_t>(v[i]));
+                        __stcg(slot + (tc + i) * kTileN + r, static_cast<int32_t>(v[i]));
                 }
             }
+            if (etr) trc[kTraceDbg + blockIdx.x * 4 + 2] = clock64();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[db]);
+            if (etr) trc[kTraceDbg + blockIdx.x * 4 + 3] = clock64();
             if (etr) et[1] = globaltimer();
-            if (!full && !owner) {
+            if (csplit && crank > 0) {
+                fence_acq_rel_cluster();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(recv_full), 0));
+            } else if (!full && !owner) {
                 __threadfence();  // this thread's partials are visible before the count
                 named_bar_sync(1, 128);
                 if (warp == kWarpEpi0 && lane == 0)
                     red_release_add_u32(p.ws_cnt + skt, static_cast<uint32_t>(it.kb1 - it.kb0));
-            } else if (owner) {
+            } else if (owner && !C::kBulkFix) {
+                named_bar_sync(1, 128);  // all 128 threads read their slots
                 if (warp == kWarpEpi0 && lane == 0) p.ws_cnt[skt] = 0u;
             }
             if (etr) et[3] = globaltimer() | (static_cast<unsigned long long>(owner) << 63);
@@ -466,6 +620,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
 
 template <int BN>
 cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
+    static_assert(Cfg<BN>::kFixBytes == 0 || Cfg<BN>::kFixBytes >= Cfg<BN>::kSlotBytes, "fix region");
     using C = Cfg<BN>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -479,11 +634,22 @@ cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
     cfg.blockDim = dim3(kNumThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.split > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = p.split;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, w4a8_gemm_kernel<BN>, p);
 }
 
@@ -506,17 +672,97 @@ int device_sm_count() {
     return sms;
 }
 
+// Workspace = [fixed counter region | contributor slots].  The counter region never moves
+// with the shape, so slot data of one launch can never land on another's counters.
+constexpr size_t kCounterBytes = 4096;  // up to 1024 stream-K tiles (<= #CTAs)
+
+// Stream-K geometry shared by the launcher and the workspace sizing.
+struct SkPlan {
+    int bn, kblocks, m_tiles, tiles, P, dp_tiles, sk_units, sk_tiles, max_contrib, split;
+};
+
+// Largest cluster split S with (S-1) partial tiles fitting the receive region.
+static int max_split_for_bn(int bn) {
+    switch (bn) {
+        case 16: return Cfg<16>::kFixBytes / Cfg<16>::kSlotBytes + 1;
+        case 32: return Cfg<32>::kFixBytes / Cfg<32>::kSlotBytes + 1;
+        case 64: return Cfg<64>::kFixBytes / Cfg<64>::kSlotBytes + 1;
+        default: return 1;
+    }
+}
+
+static SkPlan plan_for(int M, int N, int K, int sms) {
+    SkPlan s = {};
+    s.bn = pick_bn(M);
+    s.kblocks = static_cast<int>(pad_k(K) / kBlockK);
+    const int n_tiles = static_cast<int>(pad_n(N) / kTileN);
+    s.m_tiles = (M + s.bn - 1) / s.bn;
+    s.tiles = n_tiles * s.m_tiles;
+    const long long units = static_cast<long long>(s.tiles) * s.kblocks;
+    s.split = 0;
+    static const char* mode_env = std::getenv("ODY_GEMM_SCHED");  // "sk" forces stream-K
+    const bool force_sk = mode_env && std::string(mode_env) == "sk";
+    const int max_split = std::min({max_split_for_bn(s.bn), 8, std::max(1, s.kblocks / 2)});
+    if (!force_sk && max_split >= 1 && s.bn <= 64) {
+        // DP waves over P' = floor(P/S)*S CTAs, then the R remaining tiles each split over
+        // a cluster of S = min(P'/R, max) CTAs.  Choose S to minimise the busiest CTA's
+        // k-blocks (DP waves * kb + kb / S).
+        int best_s = 1;
+        double best_cost = 1e30;
+        for (int S = 1; S <= max_split; ++S) {
+            const int Pp = (sms / S) * S;
+            const int W = s.tiles / Pp;
+            const int R = s.tiles - W * Pp;
+            if (R * S > Pp) continue;
+            const double cost = W * s.kblocks + (R > 0 ? static_cast<double>(s.kblocks) / S : 0.0);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best_s = S;
+            }
+        }
+        const int Pp = (sms / best_s) * best_s;
+        const int W = s.tiles / Pp;
+        const int R = s.tiles - W * Pp;
+        s.split = best_s;
+        s.dp_tiles = W * Pp;
+        s.P = W > 0 ? Pp : R * best_s;
+        s.sk_units = 0;
+        s.sk_tiles = 0;
+        s.max_contrib = 1;
+        return s;
+    }
+    s.P = static_cast<int>(std::min<long long>(sms, units));
+    s.dp_tiles = (s.tiles / s.P) * s.P;
+    s.sk_tiles = s.tiles - s.dp_tiles;
+    s.sk_units = s.sk_tiles * s.kblocks;
+    s.max_contrib = 1;
+    if (s.sk_units > 0) {
+        auto lo = [&](int b) { return static_cast<int>(static_cast<long long>(s.sk_units) * b / s.P); };
+        auto cta_of = [&](int u) {
+            int b = static_cast<int>(static_cast<long long>(u) * s.P / s.sk_units);
+            while (b + 1 < s.P && lo(b + 1) <= u) ++b;
+            while (b > 0 && lo(b) > u) --b;
+            return b;
+        };
+        for (int t = 0; t < s.sk_tiles; ++t) {
+            const int c = cta_of((t + 1) * s.kblocks - 1) - cta_of(t * s.kblocks);
+            s.max_contrib = std::max(s.max_contrib, c);
+        }
+    }
+    return s;
+}
+
 size_t gemm_workspace_bytes(int M, int N, int K, int num_sms) {
-    (void)N;
-    (void)K;
-    const int bn = pick_bn(M);
-    const size_t P = static_cast<size_t>(num_sms > 0 ? num_sms : device_sm_count());
-    return round_up(P * sizeof(uint32_t), 256) + P * bn * kTileN * sizeof(int32_t);
+    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+    const SkPlan s = plan_for(M, N, K, sms);
+    return kCounterBytes + static_cast<size_t>(std::max(s.sk_tiles, 1)) * s.max_contrib * s.bn *
+                               kTileN * sizeof(int32_t);
 }
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
-    const int bn = pick_bn(a.M);
+    const int sms = a.max_ctas > 0 ? a.max_ctas : device_sm_count();
+    const SkPlan s = plan_for(a.M, a.N, a.K, sms);
     Params p = {};
     p.qa = a.qa;
     p.sa = a.sa;
@@ -529,26 +775,24 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     p.N = a.N;
     p.K = a.K;
     p.Mp = static_cast<int>(pad_m(a.M));
-    p.kblocks = static_cast<int>(pad_k(a.K) / kBlockK);
-    const int n_tiles = static_cast<int>(pad_n(a.N) / kTileN);
-    p.m_tiles = (a.M + bn - 1) / bn;
-    p.tiles = n_tiles * p.m_tiles;
-    const int sms = a.max_ctas > 0 ? a.max_ctas : device_sm_count();
-    const long long units = static_cast<long long>(p.tiles) * p.kblocks;
-    const int P = static_cast<int>(std::min<long long>(sms, units));
-    p.dp_tiles = (p.tiles / P) * P;
-    p.sk_units = (p.tiles - p.dp_tiles) * p.kblocks;
-    if (a.workspace_bytes < gemm_workspace_bytes(a.M, a.N, a.K, sms)) return cudaErrorInvalidValue;
+    p.kblocks = s.kblocks;
+    p.m_tiles = s.m_tiles;
+    p.tiles = s.tiles;
+    p.dp_tiles = s.dp_tiles;
+    p.sk_units = s.sk_units;
+    p.max_contrib = s.max_contrib;
+    p.split = s.split;
+    if (a.workspace_bytes < gemm_workspace_bytes(a.M, a.N, a.K, sms) || s.sk_tiles > 1024)
+        return cudaErrorInvalidValue;
     p.ws_cnt = static_cast<uint32_t*>(a.workspace);
-    p.ws_acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(a.workspace) +
-                                          round_up(static_cast<size_t>(sms) * sizeof(uint32_t), 256));
+    p.ws_slots = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(a.workspace) + kCounterBytes);
     p.pdl = a.pdl ? 1 : 0;
     p.trace = a.trace;
-    switch (bn) {
-        case 16: return launch_bn<16>(p, P, a.pdl, st);
-        case 32: return launch_bn<32>(p, P, a.pdl, st);
-        case 64: return launch_bn<64>(p, P, a.pdl, st);
-        default: return launch_bn<128>(p, P, a.pdl, st);
+    switch (s.bn) {
+        case 16: return launch_bn<16>(p, s.P, a.pdl, st);
+        case 32: return launch_bn<32>(p, s.P, a.pdl, st);
+        case 64: return launch_bn<64>(p, s.P, a.pdl, st);
+        default: return launch_bn<128>(p, s.P, a.pdl, st);
     }
 }
 

@@ -141,9 +141,18 @@ def row_absmax(x: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 class Workspace:
-    """Zero-initialised stream-K partial-sum buffer (the kernel leaves it zeroed)."""
+    """Stream-K workspace: per-tile counters (zero-initialised; every launch leaves them
+    zero) and contributor slots for int32 partial sums."""
 
     _per_device: dict = {}
+
+    @classmethod
+    def for_shapes(cls, shapes, device) -> torch.Tensor:
+        """One buffer large enough for every (m, n, k) in `shapes`."""
+        ws = None
+        for m, n, k in shapes:
+            ws = cls.get(m, n, k, device)
+        return ws
 
     @classmethod
     def get(cls, m: int, n: int, k: int, device) -> torch.Tensor:

@@ -266,15 +266,22 @@ def test_negative_control_corrupted_tile(oracle, torch_cuda, dev):
     assert not torch.equal(good, bad)
 
 
-def test_workspace_is_left_zeroed(torch_cuda, dev):
+def test_workspace_reuse_across_shapes(torch_cuda, dev):
+    """Stream-K counters are left at zero by every launch: interleaving shapes that
+    share one workspace never leaks partial sums between launches."""
     torch = torch_cuda
-    x = torch.randn((16, 5120), device="cuda")
-    w = torch.randn((15360, 5120), device="cuda") * 0.05
-    aq, wq = dev.act_quant(x), dev.W4Weight.quantize(w)
-    dev.w4a8_gemm(aq, wq)
-    torch.cuda.synchronize()
-    ws = dev.Workspace.get(16, 15360, 5120, "cuda")
-    assert int(ws.count_nonzero()) == 0
+    shapes = [(16, 15360, 5120), (16, 5120, 13824), (3, 5120, 5120), (64, 27648, 5120)]
+    ws = torch.zeros(max(dev.lib().ody_dev_workspace_bytes(*s) for s in shapes), dtype=torch.uint8,
+                     device="cuda")
+    ops = []
+    for m, n, k in shapes:
+        aq = dev.act_quant(torch.randn((m, k), device="cuda"))
+        wq = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.05)
+        ops.append((aq, wq))
+    first = [dev.w4a8_gemm(a, w, accumulators=True, workspace=ws) for a, w in ops]
+    for _ in range(2):
+        for (a, w), ref in zip(reversed(ops), reversed(first)):
+            assert torch.equal(dev.w4a8_gemm(a, w, accumulators=True, workspace=ws), ref)
 
 
 def test_error_paths_match_reference():

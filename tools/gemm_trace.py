@@ -102,7 +102,7 @@ def epi_trace(m=16, n=5120, k=5120):
     wq = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1)
     a = dev.act_quant(x)
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
-    buf = torch.zeros(148 * 8 + 64 * 4 + 148 * 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(148 * 8 + 64 * 4 + 148 * 16 + 256 + 148 * 4, dtype=torch.int64, device="cuda")
     dev.w4a8_gemm(a, wq, out=out)
     torch.cuda.synchronize()
     lib().ody_dev_set_trace(buf.data_ptr())
@@ -111,7 +111,10 @@ def epi_trace(m=16, n=5120, k=5120):
     lib().ody_dev_set_trace(None)
     cta = buf[:148 * 8].view(148, 8).cpu().numpy()
     base = cta[:, 0].min()
-    e = buf[148 * 8 + 256:].view(148, 4, 4).cpu().numpy()
+    e16 = buf[148 * 8 + 256:148 * 8 + 256 + 148 * 16].view(148, 16).cpu().numpy()
+    fix = e16[:, 15].copy()
+    e16[:, 12:] = 0
+    e = e16.reshape(148, 4, 4)
     fin = (e[:, :, 3] >> 63) & 1
     e[:, :, 3] &= (1 << 63) - 1
     rows = []
@@ -120,11 +123,19 @@ def epi_trace(m=16, n=5120, k=5120):
             if e[b, j, 0] == 0:
                 continue
             r = [(v - base) / 1000 if v > 0 else -1 for v in e[b, j]]
-            rows.append((b, j, *r, fin[b, j], (cta[b, 3] - base) / 1000))
+            rows.append((b, j, *r, fin[b, j], (cta[b, 3] - base) / 1000,
+                         (fix[b] - base) / 1000 if fix[b] > 0 else -1))
+    dbg = buf[148 * 8 + 256 + 148 * 16 + 256:].view(148, 4).cpu().numpy()
+    d = dbg[dbg[:, 0] > 0]
+    if len(d):
+        print("epilogue clock deltas (cycles, median/max over CTAs): ld->adds %d/%d adds->stores %d/%d "
+              "stores->arrive %d/%d" % (np.median(d[:, 1] - d[:, 0]), (d[:, 1] - d[:, 0]).max(),
+                                      np.median(d[:, 2] - d[:, 1]), (d[:, 2] - d[:, 1]).max(),
+                                      np.median(d[:, 3] - d[:, 2]), (d[:, 3] - d[:, 2]).max()))
     rows.sort(key=lambda r: -max(r[2:6]))
-    print("cta seg  dfull  stored  cnt_ok  done  owner last_mma   (us, slowest first)")
+    print("cta seg  dfull  stored  fixok  done  owner last_mma fixup_done  (us, slowest first)")
     for r in rows[:20]:
-        print("%3d %3d %6.2f %7.2f %7.2f %6.2f %4d %8.2f" % r)
+        print("%3d %3d %6.2f %7.2f %7.2f %6.2f %4d %8.2f %8.2f" % r)
 
 
 if __name__ == "__main__":

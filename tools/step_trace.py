@@ -26,7 +26,7 @@ def main():
     xs = {k: (torch.randn((m, k), device="cuda") * 2).half() for k in (HIDDEN, INTER)}
     a_buf = {k: dev.act_quant(xs[k]) for k in (HIDDEN, INTER)}
     outs = [torch.empty((m, n), dtype=torch.float16, device="cuda") for _, n, _ in LAYERS]
-    wsb = dev.Workspace.get(m, 27648, INTER, "cuda")
+    wsb = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
     st = torch.cuda.Stream()
     gtr = [torch.zeros(148 * 8 + 4096, dtype=torch.int64, device="cuda") for _ in LAYERS]
     atr = [torch.zeros(8 * 1024, dtype=torch.int64, device="cuda") for _ in LAYERS]
