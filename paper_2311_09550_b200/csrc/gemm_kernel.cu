@@ -711,6 +711,7 @@ static SkPlan plan_for(int M, int N, int K, int sms) {
         double best_cost = 1e30;
         for (int S = 1; S <= max_split; ++S) {
             const int Pp = (sms / S) * S;
+            if (Pp == 0) break;
             const int W = s.tiles / Pp;
             const int R = s.tiles - W * Pp;
             if (R * S > Pp) continue;
