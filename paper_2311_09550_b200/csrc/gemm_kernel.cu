@@ -59,8 +59,9 @@ constexpr int kSmemBudget = 200 * 1024;
 constexpr int kTraceCta = 8;                         // [cta][8] globaltimer slots
 constexpr int kTraceUnits = 148 * kTraceCta;         // CTA 0: per-unit converter clock64 x4
 constexpr int kTraceEpi = kTraceUnits + 64 * 4;      // per CTA, per segment epilogue x4
-constexpr int kTraceMma = kTraceEpi + 148 * 16;
-constexpr int kTraceDbg = kTraceMma + 64 * 4;    // per CTA: epilogue clock64 checkpoints  // (epi: 3 segs x 4 + fixup slot 15)      // CTA 0: per-unit MMA clock64 x4
+constexpr int kTraceMma = kTraceEpi + 148 * 16;      // (epi: 3 segs x 4 + fixup slot 15)
+                                                     // CTA 0: per-unit MMA clock64 x4
+constexpr int kTraceDbg = kTraceMma + 64 * 4;        // per CTA: epilogue clock64 checkpoints
 static_assert(kAColBase + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
 
 template <int BN>
@@ -75,14 +76,22 @@ struct Cfg {
     static constexpr bool kBulkFix = BN <= 64;
     static constexpr int kStageSlots = BN == 16 ? 4 : (BN == 32 ? 2 : 1);
     static constexpr int kFixBytes = kBulkFix ? kSlotBytes * (1 + kStageSlots) : 0;
-    static constexpr int kStages = std::min(12, (kSmemBudget - kFixBytes) / kStageBytes);
+    // Epilogue scales of the first kSegPre segments, prefetched at kernel start: loads
+    // issued during the weight stream queue behind it for microseconds.
+    static constexpr int kSegPre = 4;
+    static constexpr int kScaleBytes = kSegPre * (kTileN + BN) * 4;
+    // Output tile staged in smem and written with bulk async stores (one per token row)
+    // instead of 2-byte scattered stores.
+    static constexpr int kOutBytes = BN <= 64 ? BN * kTileN * 4 : 0;
+    static constexpr int kStages =
+        std::min(12, (kSmemBudget - kFixBytes - kScaleBytes - kOutBytes) / kStageBytes);
     // Accumulator chains (chunk c -> chain c % kChains, summed in the epilogue).  The
     // tensor pipe pipelines dependent kind::i8 accumulations (measured: 10 cycles per
     // 128x16x32 MMA with 1 or 4 chains, tools/mma_bench.cu), so one chain suffices.
     static constexpr int kChains = 1;
     static constexpr int kBarrierBytes = 1024;
     static constexpr int kSmemBytes =
-        kStages * kStageBytes + kFixBytes + kBarrierBytes + 1024;  // +align
+        kStages * kStageBytes + kFixBytes + kScaleBytes + kOutBytes + kBarrierBytes + 1024;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                        (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -104,6 +113,7 @@ struct Params {
     int out_dtype;
     int M, N, K, Mp;
     int kblocks, m_tiles, tiles, dp_tiles, sk_units;
+    int bulk_out;        // outputs may be staged in smem and bulk-stored (16 B aligned rows)
     int split;           // 0: stream-K; >= 1: DP waves + remainder tiles split over
                          // clusters of `split` CTAs, reduced through DSMEM
     int pdl;
@@ -214,8 +224,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* stages = smem;
     int32_t* fix_buf = reinterpret_cast<int32_t*>(smem + C::kStages * C::kStageBytes);
-    uint64_t* bars =
-        reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kFixBytes);
+    float* scl = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes + C::kFixBytes);
+    uint8_t* out_stage = smem + C::kStages * C::kStageBytes + C::kFixBytes + C::kScaleBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kFixBytes +
+                                                 C::kScaleBytes + C::kOutBytes);
     uint64_t* w_full = bars;
     uint64_t* w_empty = w_full + C::kStages;
     uint64_t* a_full = w_empty + C::kStages;
@@ -480,6 +492,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
         const uint32_t fix_base = smem_u32(fix_buf);
         if (p.pdl) pdl_wait();
+        {  // prefetch the scales of the first kSegPre segments before the stream saturates
+            SegIter ip = it;
+            for (int jj = 0; jj < C::kSegPre && ip.next(p); ++jj) {
+                const int nt = ip.tile / p.m_tiles, mt = ip.tile % p.m_tiles;
+                const int n = nt * kTileN + r;
+                float* sc = scl + jj * (kTileN + BN);
+                sc[r] = n < p.N ? __ldg(p.sw + n) : 0.0f;
+                if (r < BN) sc[kTileN + r] = mt * BN + r < p.M ? __ldg(p.sa + mt * BN + r) : 0.0f;
+            }
+            named_bar_sync(1, 128);
+        }
         int j = 0;
         while (it.next(p)) {
             const int db = j & 1;
@@ -495,11 +518,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             unsigned long long* et = trc + kTraceEpi + blockIdx.x * 16 + j * 4;
             // scales for this tile, fetched while the MMAs finish
             constexpr int kPre = BN < 32 ? BN : 32;
-            const float sw_n = (full || owner) && n < p.N ? __ldg(p.sw + n) : 0.0f;
+            const float* sc = scl + j * (kTileN + BN);
+            const bool pref = j < C::kSegPre;
+            const float sw_n = !(full || owner) ? 0.0f
+                               : pref           ? sc[r]
+                               : (n < p.N ? __ldg(p.sw + n) : 0.0f);
             float sa_pre[kPre];
 #pragma unroll
             for (int i = 0; i < kPre; ++i)
-                sa_pre[i] = (full || owner) && t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f;
+                sa_pre[i] = !(full || owner) ? 0.0f
+                            : pref           ? sc[kTileN + i]
+                            : (t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f);
+            const bool stage_out = C::kOutBytes > 0 && p.bulk_out && (full || owner) &&
+                                   (nt + 1) * kTileN <= p.N;
+            const uint32_t ostage = smem_u32(out_stage);
             int32_t* slot = nullptr;
             if (!full && !owner && !csplit) {
                 const int c = blockIdx.x - sk_cta_of_unit(p, skt * p.kblocks);
@@ -564,7 +596,32 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                         }
                     }
                     if (etr && tc == 0) trc[kTraceDbg + blockIdx.x * 4 + 1] = clock64();
-                    if (n < p.N) {
+                    if (stage_out) {
+                        // value of (token tc+i, row r) into the smem tile [token][128 rows]
+                        float val[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float sa_t = tc + i < kPre ? sa_pre[tc + i < kPre ? tc + i : 0]
+                                                             : __ldg(p.sa + min(t0 + tc + i, p.M - 1));
+                            val[i] = __fmul_rn(__int2float_rn(static_cast<int32_t>(v[i]) >> 4),
+                                               __fmul_rn(sa_t, sw_n));  // ref gemm.cpp:269-273
+                        }
+                        const uint32_t e0 = static_cast<uint32_t>(tc * kTileN + r);
+                        if (p.out_dtype == kDtypeF32) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                sts32(ostage + (e0 + i * kTileN) * 4, __float_as_uint(val[i]));
+                        } else if (p.out_dtype == kDtypeF16) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                sts16(ostage + (e0 + i * kTileN) * 2, __half_as_ushort(__float2half_rn(val[i])));
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                sts16(ostage + (e0 + i * kTileN) * 2,
+                                      __bfloat16_as_ushort(__float2bfloat16_rn(val[i])));
+                        }
+                    } else if (n < p.N) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int t = t0 + tc + i;
@@ -590,6 +647,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[db]);
+            if (stage_out) {  // the staged tile leaves as coalesced 16-byte row pieces
+                named_bar_sync(1, 128);
+                const int esz = p.out_dtype == kDtypeF32 ? 4 : 2;
+                const int per_row = kTileN * esz / 16;  // 16-byte pieces per token row
+                const int rows = min(BN, p.M - t0);
+                for (int c = r; c < rows * per_row; c += 128) {
+                    const int t = c / per_row, piece = c % per_row;
+                    const uint4 val = lds128(ostage + (t * kTileN * esz) + piece * 16);
+                    *reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.out) +
+                                              (static_cast<size_t>(t0 + t) * p.N + nt * kTileN) * esz +
+                                              piece * 16) = val;
+                }
+                named_bar_sync(1, 128);  // staging reusable by the next segment
+            }
             if (etr) trc[kTraceDbg + blockIdx.x * 4 + 3] = clock64();
             if (etr) et[1] = globaltimer();
             if (csplit && crank > 0) {
@@ -783,6 +854,13 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     p.sk_units = s.sk_units;
     p.max_contrib = s.max_contrib;
     p.split = s.split;
+    {
+        const size_t esz = a.out_dtype == kDtypeF32 ? 4 : 2;
+        p.bulk_out = (a.out && !a.acc_out && (static_cast<size_t>(a.N) * esz) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
+                         ? 1
+                         : 0;
+    }
     if (a.workspace_bytes < gemm_workspace_bytes(a.M, a.N, a.K, sms) || s.sk_tiles > 1024)
         return cudaErrorInvalidValue;
     p.ws_cnt = static_cast<uint32_t*>(a.workspace);

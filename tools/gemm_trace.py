@@ -110,7 +110,7 @@ def epi_trace(m=16, n=5120, k=5120):
     torch.cuda.synchronize()
     lib().ody_dev_set_trace(None)
     cta = buf[:148 * 8].view(148, 8).cpu().numpy()
-    base = cta[:, 0].min()
+    base = cta[:, 0][cta[:, 0] > 0].min()
     e16 = buf[148 * 8 + 256:148 * 8 + 256 + 148 * 16].view(148, 16).cpu().numpy()
     fix = e16[:, 15].copy()
     e16[:, 12:] = 0
