@@ -44,6 +44,7 @@ METRIC = "W4A8 GEMM HBM GB/s (LLaMA-13B decoder-layer linears, decode)"
 
 
 def gemm_bytes(m, n, k):
+    """Algorithmic HBM bytes of one W4A8 GEMM on quantized A."""
     return n * k // 2 + m * k + 4 * n + 4 * m + 2 * m * n
 
 
@@ -51,11 +52,14 @@ def actq_bytes(m, k):
     return 2 * m * k + m * k + 4 * m
 
 
+def linear_bytes(m, n, k):
+    """Algorithmic HBM bytes of one W4A8 linear from fp16 x: packed INT4 weights,
+    per-channel scales, fp16 activations in, fp16 outputs out, per-token scales."""
+    return n * k // 2 + 4 * n + 2 * m * k + 2 * m * n + 4 * m
+
+
 def step_bytes(m, world=1):
-    tot = 0
-    for _, n, k in LAYERS:
-        tot += gemm_bytes(m, n, k) + actq_bytes(m, k)
-    return tot
+    return sum(linear_bytes(m, n, k) for _, n, k in LAYERS)
 
 
 def peaks():
@@ -78,6 +82,7 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self._stop = threading.Event()
+        self._ready = threading.Event()  # set once the first sample is in (or sampling failed)
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
@@ -95,6 +100,7 @@ class ClockSampler:
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append([str(sm), str(mx), hex(r)] +
                                  ["Active" if r & b else "Not Active" for _, b in bits])
+                self._ready.set()
                 self._stop.wait(0.002)
             return
         except Exception as e:  # noqa: BLE001
@@ -109,10 +115,12 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
+        self._ready.wait(timeout=30)  # the timed region starts with the sampler running
         return self
 
     def __exit__(self, *a):
@@ -178,18 +186,22 @@ def run_b200(args):
              for k in (HIDDEN, INTER)}
     outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
     ws_buf = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
+    for _, n, k in LAYERS:
+        ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")
     stream = torch.cuda.Stream()
     launches_per_step = 0
+    lib().ody_dev_set_linear_mode(1 if args.fused else 0)
 
     def step(copy_idx, pdl):
         nonlocal launches_per_step
         if world == 1:
             cnt = 0
             for name, w in layers[copy_idx]:
-                a = a_buf[w.k]
-                dev.act_quant(xs[w.k], out=a, pdl=pdl, stream=stream)
-                dev.w4a8_gemm(a, w, out=outs[name], pdl=pdl, stream=stream, workspace=ws_buf)
-                cnt += 2
+                # public device API: act-quant kernel + FastGEMM (PDL-chained), or one
+                # kernel with K1 fused into the GEMM prologue under --fused
+                dev.w4a8_linear(xs[w.k], w, out=outs[name], pdl=pdl, stream=stream,
+                                workspace=ws_buf)
+                cnt += 1 if lib().ody_dev_linear_is_fused(m, w.n, w.k) else 2
             launches_per_step = cnt
         else:
             layers[copy_idx](xs[HIDDEN])
@@ -250,13 +262,14 @@ def run_b200(args):
                    "intermediate": INTER, "parallelism": f"tp{world}" if world > 1 else "single",
                    "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
                    "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
-                   "cuda_graph": use_graph, "pdl": bool(args.pdl)},
+                   "cuda_graph": use_graph, "pdl": bool(args.pdl),
+                   "lowering": "fused act-quant prologue" if args.fused else "act_quant + FastGEMM"},
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps if world == 1 else None,
     }
 
     if rank == 0 and world == 1:
-        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m)
+        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs)
         result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
         result["e2e"] = e2e_c_abi(args, m)
         if not args.no_cpu:
@@ -289,11 +302,15 @@ def _graph_time(fn, stream, reps, warm=3):
     return s.elapsed_time(e) / reps
 
 
-def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m):
+def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs):
     """Dominant kernel = the FastGEMM (HBM-bound at decode).  Its average launch
     duration is timed with CUDA events on its own stream over graph replays that
     rotate all weight copies (each launch streams fresh weights from HBM)."""
     hbm, kind = peaks()
+    fused = bool(args.fused)
+    if not fused:
+        for k in (HIDDEN, INTER):
+            dev.act_quant(xs[k], out=a_buf[k], stream=stream)
     per = {}
     tot_bytes = 0.0
     tot_ms = 0.0
@@ -302,10 +319,13 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m):
 
         def fn(ws=ws, name=name, k=k):
             for w in ws:
-                dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=ws_buf)
+                if not fused:
+                    dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=ws_buf)
+                else:
+                    dev.w4a8_linear(xs[k], w, out=outs[name], stream=stream, workspace=ws_buf)
 
-        ms = _graph_time(fn, stream, reps=max(5, args.steps // 2)) / len(ws)
-        b = gemm_bytes(m, n, k)
+        ms = _graph_time(fn, stream, reps=200) / len(ws)
+        b = gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k)
         per[name] = {"N": n, "K": k, "us": round(ms * 1e3, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1),
                      "frac": round(b / (ms * 1e-3) / 1e9 / hbm, 4)}
         tot_bytes += b
@@ -321,9 +341,13 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m):
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
-            "kernel": "w4a8_gemm_kernel (avg over the 4 layer shapes, bytes-weighted)",
+            "kernel": ("w4a8_gemm_kernel" if not fused else
+                       "w4a8_gemm_kernel<16,FUSE> (K1 fused)") +
+                      " -- avg over the 4 layer shapes, bytes-weighted",
             "per_shape": per,
-            "algorithmic_bytes_per_launch": {nm: gemm_bytes(m, n, k) for nm, n, k in LAYERS}}
+            "algorithmic_bytes_per_launch": {
+                nm: (gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k))
+                for nm, n, k in LAYERS}}
 
 
 def decode_sweep(args, dev, layers, stream):
@@ -333,20 +357,20 @@ def decode_sweep(args, dev, layers, stream):
     hbm, _ = peaks()
     res = {}
     for m in (1, 2, 4, 8, 16, 32, 64):
-        ws_buf = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
+        for _, n, k in LAYERS:
+            ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")
         row = {}
         for li, (name, n, k) in enumerate(LAYERS):
             x = (torch.randn((m, k), device="cuda")).to(torch.float16)
-            a = dev.act_quant(x)
             out = torch.empty((m, n), dtype=torch.float16, device="cuda")
             ws = [layers[c][li][1] for c in range(len(layers))]
 
             def fn(ws=ws):
                 for w in ws:
-                    dev.w4a8_gemm(a, w, out=out, stream=stream, workspace=ws_buf)
+                    dev.w4a8_linear(x, w, out=out, stream=stream, workspace=ws_buf)
 
             ms = _graph_time(fn, stream, reps=10) / len(ws)
-            gbs = gemm_bytes(m, n, k) / (ms * 1e-3) / 1e9
+            gbs = linear_bytes(m, n, k) / (ms * 1e-3) / 1e9
             row[name] = {"us": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3)}
         res[f"M{m}"] = row
     _ = lib
@@ -490,7 +514,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--m", type=int, default=16, help="decode batch (tokens) per step")
@@ -499,6 +523,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="lower each linear to ONE kernel (act quant fused into the GEMM prologue)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

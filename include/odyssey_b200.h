@@ -150,6 +150,23 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
                              void* out, int32_t* acc_out, void* workspace,
                              size_t workspace_bytes, int max_ctas, int pdl, void* stream);
 ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream);
+
+/* K1+K3+K4: the whole W4A8 linear y = x W^T from unquantized activations x (m x k,
+ * dtype x_dtype, row stride ldx).  For decode widths (m <= 16) the per-token INT8
+ * quantization runs inside the GEMM kernel (codes never leave shared memory; a tile
+ * split over a thread-block cluster combines the per-token maxima through DSMEM), one
+ * launch per linear; otherwise act quant + GEMM.  Results are identical to
+ * ody_dev_act_quant + ody_dev_w4a8_gemm.  s_a_out (optional, m floats) receives the
+ * per-token scales.  workspace: ody_dev_linear_workspace_bytes(m,n,k), zeroed once. */
+ody_status ody_dev_w4a8_linear(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed,
+                               const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                               void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
+                               int max_ctas, int pdl, void* stream);
+size_t ody_dev_linear_workspace_bytes(size_t m, size_t n, size_t k);
+int ody_dev_linear_is_fused(size_t m, size_t n, size_t k); /* 1: single fused kernel */
+/* Linear lowering: 0 (default) = act-quant kernel + FastGEMM (PDL-chained);
+ * 1 = act quant fused into the GEMM prologue where eligible (M <= 16, 16-bit x). */
+void ody_dev_set_linear_mode(int mode);
 /* Diagnostics: when buf (device, >= 8 * #CTAs u64) is non-NULL, subsequent
  * ody_dev_w4a8_gemm launches record a per-CTA %globaltimer timeline into it:
  * [entry, setup done, first data at MMA, last MMA commit, epilogue done, exit,

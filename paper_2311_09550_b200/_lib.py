@@ -66,6 +66,12 @@ SIGNATURES = {
                                   c_size_t, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_int,
                                   c_int, c_void_p]),
     "ody_dev_workspace_init": (c_int, [c_void_p, c_size_t, c_void_p]),
+    "ody_dev_w4a8_linear": (c_int, [c_void_p, c_int, c_size_t, c_void_p, c_void_p, c_size_t, c_size_t,
+                                    c_size_t, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_int,
+                                    c_int, c_void_p]),
+    "ody_dev_linear_workspace_bytes": (c_size_t, [c_size_t, c_size_t, c_size_t]),
+    "ody_dev_linear_is_fused": (c_int, [c_size_t, c_size_t, c_size_t]),
+    "ody_dev_set_linear_mode": (None, [c_int]),
     "ody_dev_set_trace": (None, [c_void_p]),
     "ody_dev_set_act_trace": (None, [c_void_p]),
     "ody_dev_a8_unpack": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p,

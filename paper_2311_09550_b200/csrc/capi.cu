@@ -567,6 +567,52 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
 void ody_dev_set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 void ody_dev_set_act_trace(void* buf) { set_act_trace(static_cast<unsigned long long*>(buf)); }
 
+size_t ody_dev_linear_workspace_bytes(size_t m, size_t n, size_t k) {
+    return linear_scratch_bytes(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0);
+}
+
+void ody_dev_set_linear_mode(int mode) { set_linear_mode(mode); }
+
+int ody_dev_linear_is_fused(size_t m, size_t n, size_t k) {
+    return linear_is_fused(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0) ? 1 : 0;
+}
+
+ody_status ody_dev_w4a8_linear(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed,
+                               const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                               void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
+                               int max_ctas, int pdl, void* stream) {
+    if (!x || !w_packed || !s_w || !out || !workspace)
+        return einval("ody_dev_w4a8_linear: null argument");
+    if (m == 0 || n == 0 || k == 0) return einval("ody_dev_w4a8_linear: empty operand");
+    if (ldx < k) return einval("ody_dev_w4a8_linear: ldx < k");
+    if (k > kMaxK) return einval("GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
+    if (x_dtype < ODY_DTYPE_F32 || x_dtype > ODY_DTYPE_BF16 || out_dtype < ODY_DTYPE_F32 ||
+        out_dtype > ODY_DTYPE_BF16)
+        return einval("bad dtype");
+    return guarded([&] {
+        LinearArgs a = {};
+        a.x = x;
+        a.x_dtype = static_cast<int>(x_dtype);
+        a.ldx = ldx;
+        a.wp = static_cast<const uint8_t*>(w_packed);
+        a.sw = s_w;
+        a.out = out;
+        a.out_dtype = static_cast<int>(out_dtype);
+        a.sa_out = s_a_out;
+        a.workspace = workspace;
+        a.workspace_bytes = workspace_bytes;
+        a.M = static_cast<int>(m);
+        a.N = static_cast<int>(n);
+        a.K = static_cast<int>(k);
+        a.max_ctas = max_ctas;
+        a.pdl = pdl != 0;
+        a.trace = g_trace;
+        if (workspace_bytes < linear_scratch_bytes(a.M, a.N, a.K, max_ctas))
+            fail(ODY_EINVAL, "ody_dev_w4a8_linear: workspace too small");
+        cuda_check(launch_w4a8_linear(a, static_cast<cudaStream_t>(stream)), "w4a8_linear launch");
+    });
+}
+
 ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream) {
     if (!workspace) return einval("ody_dev_workspace_init: null argument");
     return guarded([&] {

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -36,6 +37,7 @@
 #include "kernels.h"
 #include "layout.h"
 #include "ptx.cuh"
+#include "quant_common.cuh"
 
 namespace odyb200 {
 
@@ -64,18 +66,24 @@ constexpr int kTraceMma = kTraceEpi + 148 * 16;      // (epi: 3 segs x 4 + fixup
 constexpr int kTraceDbg = kTraceMma + 64 * 4;        // per CTA: epilogue clock64 checkpoints
 static_assert(kAColBase + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
 
-template <int BN>
+template <int BN, bool FUSE = false>
 struct Cfg {
     static constexpr int kBBytes = BN * 128;                          // one activation k-block
-    static constexpr int kStageBytes = kUnitBlocks * (kBBytes + kWBlockBytes);
-    static constexpr int kWOff = kUnitBlocks * kBBytes;               // weights after B tiles
+    // FUSE: activations are quantized inside the kernel into a resident smem B (all of
+    // this CTA's k-range), so pipeline stages carry weights only.
+    static constexpr int kStageBytes = FUSE ? kUnitBlocks * kWBlockBytes
+                                            : kUnitBlocks * (kBBytes + kWBlockBytes);
+    static constexpr int kWOff = FUSE ? 0 : kUnitBlocks * kBBytes;   // weights after B tiles
+    static constexpr int kResBBytes = FUSE ? 96 * 1024 : 0;
+    static constexpr int kTokBytes = FUSE ? (2 + 8) * BN * 4 : 0;  // max, scale, peers' maxima
     // Owned stream-K tile: the fixup warp bulk-copies the other contributors' partial
     // sums (kSlotBytes each, kStageSlots at a time) into smem and adds them into
     // fix_buf.  For BN=128 (prefill remainder tiles) the owner reads them directly.
     static constexpr int kSlotBytes = BN * kTileN * 4;
     static constexpr bool kBulkFix = BN <= 64;
     static constexpr int kStageSlots = BN == 16 ? 4 : (BN == 32 ? 2 : 1);
-    static constexpr int kFixBytes = kBulkFix ? kSlotBytes * (1 + kStageSlots) : 0;
+    static constexpr int kFixBytes =
+        FUSE ? kSlotBytes * 2 : (kBulkFix ? kSlotBytes * (1 + kStageSlots) : 0);
     // Epilogue scales of the first kSegPre segments, prefetched at kernel start: loads
     // issued during the weight stream queue behind it for microseconds.
     static constexpr int kSegPre = 4;
@@ -83,21 +91,23 @@ struct Cfg {
     // Output tile staged in smem and written with bulk async stores (one per token row)
     // instead of 2-byte scattered stores.
     static constexpr int kOutBytes = BN <= 64 ? BN * kTileN * 4 : 0;
-    static constexpr int kStages =
-        std::min(12, (kSmemBudget - kFixBytes - kScaleBytes - kOutBytes) / kStageBytes);
+    static constexpr int kBudget = FUSE ? 220 * 1024 : kSmemBudget;
+    static constexpr int kStages = std::min(
+        12, (kBudget - kResBBytes - kFixBytes - kScaleBytes - kOutBytes - kTokBytes) / kStageBytes);
     // Accumulator chains (chunk c -> chain c % kChains, summed in the epilogue).  The
     // tensor pipe pipelines dependent kind::i8 accumulations (measured: 10 cycles per
     // 128x16x32 MMA with 1 or 4 chains, tools/mma_bench.cu), so one chain suffices.
     static constexpr int kChains = 1;
     static constexpr int kBarrierBytes = 1024;
-    static constexpr int kSmemBytes =
-        kStages * kStageBytes + kFixBytes + kScaleBytes + kOutBytes + kBarrierBytes + 1024;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kResBBytes + kFixBytes + kScaleBytes +
+                                      kOutBytes + kTokBytes + kBarrierBytes + 1024;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                        (static_cast<uint32_t>(BN >> 3) << 17) |
                                        (static_cast<uint32_t>(128 >> 4) << 24);
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 128, "BN");
     static_assert(kBBytes % 1024 == 0 && kStageBytes % 1024 == 0, "swizzle atom alignment");
+    static_assert(!FUSE || BN == 16, "in-kernel activation quantization is a decode (M<=16) path");
 };
 
 struct Params {
@@ -114,9 +124,16 @@ struct Params {
     int M, N, K, Mp;
     int kblocks, m_tiles, tiles, dp_tiles, sk_units;
     int bulk_out;        // outputs may be staged in smem and bulk-stored (16 B aligned rows)
+    // FUSE: quantize x (M x K, dtype x_dtype, row stride ldx) in-kernel; sa_out optional
+    const void* x;
+    int x_dtype;
+    size_t ldx;
+    float* sa_out;
     int split;           // 0: stream-K; >= 1: DP waves + remainder tiles split over
                          // clusters of `split` CTAs, reduced through DSMEM
+    int cluster;         // cluster size (>= split; FUSE: activation share groups)
     int pdl;
+    int dbg;             // diagnostics (ODY_DBG_FUSE): 1 hold weights until B quantized, 2 skip quant math
     unsigned long long* trace;  // optional timeline, see ody_dev_set_trace
 };
 
@@ -216,18 +233,225 @@ __device__ __forceinline__ void store_out(const Params& p, int t, int n, int32_t
     }
 }
 
+// FUSE quantization geometry.  The CTAs of a cluster that consume the same activation
+// k-range (a "share class": the whole cluster when every CTA owns a data-parallel
+// tile, the CTAs with the same split rank when the tiles are cluster-split) quantize
+// disjoint sub-slices of it and push their codes into each other's resident B, so each
+// activation byte is loaded and quantized once per class rather than once per CTA.
+struct FuseGeom {
+    int klo, khi;  // class k-block range (this CTA's resident B)
+    int slo, shi;  // this CTA's sub-slice, quantized here
+    int crank;     // rank in the cluster
+    int seff;      // class stride in cluster ranks (1, or the split S)
+    int D, j;      // class size, this CTA's index in it
+};
+__device__ __forceinline__ FuseGeom fuse_geom(const Params& p) {
+    FuseGeom g;
+    const int G = p.cluster;
+    g.crank = static_cast<int>(blockIdx.x) % G;
+    g.seff = (p.dp_tiles == 0 && p.split > 1) ? p.split : 1;
+    const int s = g.crank % g.seff;
+    g.D = G / g.seff;
+    g.j = g.crank / g.seff;
+    g.klo = s * p.kblocks / g.seff;  // == SegIter's split slice of rank s
+    g.khi = (s + 1) * p.kblocks / g.seff;
+    const int nb = g.khi - g.klo;
+    g.slo = g.klo + g.j * nb / g.D;
+    g.shi = g.klo + (g.j + 1) * nb / g.D;
+    return g;
+}
+
+// FUSE prologue, run by the 384 threads of warps 4..15 before their pipeline roles:
+// the per-token max|x| over this CTA's k-range (combined across the cluster's ranks
+// through DSMEM when the tile is split, so every rank sees the max over ALL of K --
+// ref quantize.cpp:113-132), then the INT8 codes of that k-range straight into the
+// resident smem B operand in the swizzled K-major layout.  tok[0..BN) = scales.
+// 16-bit activations are held packed (16 values = 2 x uint4) in registers between the
+// max pass and the quantize pass: every x load of the CTA is issued at once, so the
+// prologue costs one memory round trip even while the weight stream is in flight.
+constexpr int kFuseThreads = 448;  // warps 2..15
+constexpr int kFuseChunks = 6;     // 16-element chunks per thread (M * sub-slice <= 43008)
+
+template <typename T>
+__device__ __forceinline__ void load_chunk_raw(const T* row, int k0, int K, uint4 (&r)[2]) {
+    if (k0 + 16 <= K) {
+        r[0] = __ldg(reinterpret_cast<const uint4*>(row + k0));
+        r[1] = __ldg(reinterpret_cast<const uint4*>(row + k0 + 8));
+    } else {
+        unsigned short h[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            h[i] = k0 + i < K ? reinterpret_cast<const unsigned short*>(row)[k0 + i] : 0;
+        r[0] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
+                          h[6] | (h[7] << 16));
+        r[1] = make_uint4(h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16),
+                          h[14] | (h[15] << 16));
+    }
+}
+
+__device__ __forceinline__ float unpack16(uint32_t w, int hi, bool bf16) {
+    const unsigned short h = hi ? static_cast<unsigned short>(w >> 16) : static_cast<unsigned short>(w);
+    return bf16 ? __uint_as_float(static_cast<uint32_t>(h) << 16) : __half2float(__ushort_as_half(h));
+}
+
+// 16 packed 16-bit values -> 16 INT8 codes through the IEEE-division path (the rare
+// chunks holding a near-half-integer quotient, or a non-finite reciprocal).
+__device__ __noinline__ uint4 quant16_exact(uint4 r0, uint4 r1, float scale, float rcp, bool bf16) {
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t out[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int32_t code = quant_code_i8(unpack16(w[e >> 1], e & 1, bf16), scale, rcp, true);
+        out[e >> 2] |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * (e & 3));
+    }
+    return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// Fast path (quant_byte_fast): ~7 instructions per element, no branches.
+__device__ __forceinline__ uint4 quant16_packed(uint4 r0, uint4 r1, float scale, float rcp, bool exact,
+                                                bool bf16) {
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t t[16];
+    bool redo = exact;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) t[e] = quant_byte_fast(unpack16(w[e >> 1], e & 1, bf16), rcp, redo);
+    if (redo) return quant16_exact(r0, r1, scale, rcp, bf16);
+    return make_uint4(pack4_low_bytes(t[0], t[1], t[2], t[3]), pack4_low_bytes(t[4], t[5], t[6], t[7]),
+                      pack4_low_bytes(t[8], t[9], t[10], t[11]),
+                      pack4_low_bytes(t[12], t[13], t[14], t[15]));
+}
+
+__device__ __forceinline__ float absmax16_packed(uint4 r0, uint4 r1, bool bf16) {
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    float m = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) m = fmaxf(m, fabsf(unpack16(w[e >> 1], e & 1, bf16)));
+    return m;
+}
+
+// FUSE prologue, run by the 448 threads of warps 2..15 before their pipeline roles:
+// per-token max|x| over this CTA's sub-slice, combined over the whole cluster through
+// DSMEM (the cluster's sub-slices tile all of K, so every CTA sees the max over ALL of
+// K -- ref quantize.cpp:113-132), then the INT8 codes of the sub-slice into the resident
+// smem B (swizzled K-major), pushed to the share class with DSMEM bulk copies that
+// complete on the peers' b_ready.  The 16-bit activations stay packed in registers
+// between the max pass and the quantize pass: every load is issued at once.
 template <int BN>
+__device__ __forceinline__ void fused_act_quant(const Params& p, const FuseGeom& g, uint32_t resb,
+                                                float* tok, uint64_t* max_ready, uint64_t* b_ready,
+                                                int qt, bool kBf16) {
+    constexpr int kQ = kFuseThreads;
+    constexpr uint32_t kBlk = BN * 128;  // one resident B k-block
+    const __half* x = static_cast<const __half*>(p.x);  // raw 16-bit payload (f16 or bf16)
+    const int nch = (g.shi - g.slo) * (kBlockK / 16);  // 16-element chunks per token row
+    const int total = p.M * nch;
+    const int G = p.cluster;
+    uint32_t* tmax = reinterpret_cast<uint32_t*>(tok + BN);  // [BN] as float bits (>= 0)
+    float* peer = tok + 2 * BN;                               // [8][BN] cluster ranks' maxima
+    if (qt < BN) tmax[qt] = 0u;
+    uint4 raw[kFuseChunks][2];
+#pragma unroll
+    for (int i = 0; i < kFuseChunks; ++i) {  // all loads in flight together
+        const int c = qt + i * kQ;
+        if (c < total) {
+            const int t = c / nch, kc = c - t * nch;
+            load_chunk_raw(x + static_cast<size_t>(t) * p.ldx, g.slo * kBlockK + kc * 16, p.K, raw[i]);
+        }
+    }
+    named_bar_sync(2, kQ);  // tmax zeroed
+    unsigned long long* dbg = p.trace ? p.trace + kTraceDbg + blockIdx.x * 8 : nullptr;
+    if (dbg && qt == 0) dbg[0] = globaltimer();
+#pragma unroll
+    for (int i = 0; i < kFuseChunks; ++i) {
+        const int c = qt + i * kQ;
+        if (c < total) {
+            const float m = absmax16_packed(raw[i][0], raw[i][1], kBf16);
+            atom_max_shared_u32(smem_u32(tmax + c / nch), __float_as_uint(m));  // floats >= 0
+        }
+    }
+    named_bar_sync(2, kQ);
+    if (dbg && qt == 0) dbg[1] = globaltimer();
+    if (G > 1) {  // all-to-all of the partial maxima over the cluster (DSMEM)
+        // Thread (d, token) stores one token's maximum into rank d and arrives there with
+        // release semantics (orders its own store; no fence), all pairs in parallel.
+        if (qt < G * BN) {
+            const int d = qt / BN, tk = qt % BN;
+            if (d != g.crank) {
+                st_dsmem_u32(mapa_shared(smem_u32(peer + g.crank * BN + tk), d), tmax[tk]);
+                mbar_arrive_remote(mapa_shared(smem_u32(max_ready), d));
+            }
+        }
+        if (dbg && qt == 0) dbg[4] = globaltimer();
+        mbar_wait_cluster(max_ready, 0);
+        if (dbg && qt == 0) dbg[5] = globaltimer();
+        if (qt < BN) {
+            uint32_t m = tmax[qt];
+            for (int d = 0; d < G; ++d)
+                if (d != g.crank) m = max(m, __float_as_uint(peer[d * BN + qt]));
+            tmax[qt] = m;
+        }
+        named_bar_sync(2, kQ);
+    }
+    float* trcp = peer;  // reuse: per-token reciprocal (thread qt only overwrites column qt)
+    if (qt < BN) {
+        float sc = __uint_as_float(tmax[qt]) / 127.0f;  // ref quantize.cpp:22-35
+        if (!(sc > 0.0f)) sc = kMinScale;
+        tok[qt] = sc;
+        trcp[qt] = 1.0f / sc;
+        if (p.sa_out && blockIdx.x == 0 && qt < p.M) p.sa_out[qt] = sc;
+    }
+    named_bar_sync(2, kQ);
+    if (dbg && qt == 0) dbg[2] = globaltimer();
+    const uint32_t mine = resb + (g.slo - g.klo) * kBlk;
+#pragma unroll
+    for (int i = 0; i < kFuseChunks; ++i) {
+        const int c = qt + i * kQ;
+        if (c < total) {
+            const int t = c / nch, kc = c - t * nch;
+            const float scale = __uint_as_float(lds32(smem_u32(tok + t)));
+            const float rcp = __uint_as_float(lds32(smem_u32(trcp + t)));
+            const bool exact = !(rcp < INFINITY);
+            const uint4 q = p.dbg == 2 ? raw[i][0] : quant16_packed(raw[i][0], raw[i][1], scale, rcp, exact, kBf16);
+            const int kb = kc / 8, chunk = kc % 8;  // block (relative to slo), 16-byte chunk
+            sts128(mine + kb * kBlk + t * 128 + (((chunk ^ (t & 7)) & 7) * 16), q);
+        }
+    }
+    for (int c = total + qt; c < BN * nch; c += kQ) {  // padding tokens M..BN-1: zero codes
+        const int t = c / nch, kc = c - t * nch;
+        const int kb = kc / 8, chunk = kc % 8;
+        sts128(mine + kb * kBlk + t * 128 + (((chunk ^ (t & 7)) & 7) * 16), make_uint4(0, 0, 0, 0));
+    }
+    if (dbg && qt == 0) dbg[6] = globaltimer();
+    fence_proxy_async_shared();  // generic smem writes -> async proxy (tcgen05, bulk copies)
+    named_bar_sync(2, kQ);
+    if (qt == 0) {
+        const uint32_t bytes = (g.shi - g.slo) * kBlk;
+        if (bytes > 0)
+            for (int jj = 0; jj < g.D; ++jj) {
+                if (jj == g.j) continue;
+                const uint32_t rk = g.crank % g.seff + jj * g.seff;
+                bulk_s2peer(mapa_shared(mine, rk), mine, bytes, mapa_shared(smem_u32(b_ready), rk));
+            }
+        // own arrival + the bytes the class peers push into this CTA
+        mbar_expect_tx(b_ready, (g.khi - g.klo - (g.shi - g.slo)) * kBlk);
+    }
+    if (dbg && qt == 0) dbg[3] = globaltimer();
+}
+
+template <int BN, bool FUSE>
 __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, FUSE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* stages = smem;
-    int32_t* fix_buf = reinterpret_cast<int32_t*>(smem + C::kStages * C::kStageBytes);
-    float* scl = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes + C::kFixBytes);
-    uint8_t* out_stage = smem + C::kStages * C::kStageBytes + C::kFixBytes + C::kScaleBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kFixBytes +
-                                                 C::kScaleBytes + C::kOutBytes);
+    uint8_t* resb_ptr = smem + C::kStages * C::kStageBytes;  // FUSE: resident B (1 KiB aligned)
+    uint8_t* after_b = resb_ptr + C::kResBBytes;
+    int32_t* fix_buf = reinterpret_cast<int32_t*>(after_b);
+    float* scl = reinterpret_cast<float*>(after_b + C::kFixBytes);
+    uint8_t* out_stage = after_b + C::kFixBytes + C::kScaleBytes;
+    float* tok = reinterpret_cast<float*>(out_stage + C::kOutBytes);  // FUSE: token scales
+    uint64_t* bars = reinterpret_cast<uint64_t*>(out_stage + C::kOutBytes + C::kTokBytes);
     uint64_t* w_full = bars;
     uint64_t* w_empty = w_full + C::kStages;
     uint64_t* a_full = w_empty + C::kStages;
@@ -237,7 +461,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     uint64_t* fix_full = d_empty + 2;
     uint64_t* fix_tx = fix_full + 1;
     uint64_t* recv_full = fix_tx + 1;  // cluster split-K: partials of ranks 1..S-1 landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 1);
+    uint64_t* b_ready = recv_full + 1;  // FUSE: resident B quantized
+    uint64_t* max_ready = b_ready + 1;  // FUSE + cluster: the other ranks' token maxima landed
+    uint64_t* push_done = max_ready + 1;  // FUSE: class peers received this CTA's codes
+    uint64_t* b_full = push_done + 1;  // !FUSE: [kStages] activation tile of the stage landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + C::kStages);
     const uint32_t stage_base = smem_u32(stages);
 
     const int warp = threadIdx.x >> 5;
@@ -252,6 +480,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::kStages; ++i) {
             mbar_init(&w_full[i], 1);
+            mbar_init(&b_full[i], 1);
             mbar_init(&w_empty[i], 1);  // MMA commit (converters finished reading before MMA)
         }
         for (int i = 0; i < kAStages; ++i) {
@@ -265,6 +494,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         mbar_init(fix_full, 1);
         mbar_init(fix_tx, 1);
         mbar_init(recv_full, p.split > 1 ? 4 * (p.split - 1) : 1);
+        mbar_init(b_ready, 1);
+        mbar_init(max_ready, p.cluster > 1 ? (p.cluster - 1) * BN : 1);
+        mbar_init(push_done, p.cluster > 1 ? p.cluster - 1 : 1);
         fence_mbar_init();
     }
     if (warp == kWarpAlloc) {
@@ -273,13 +505,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     }
     tc_fence_before();
     __syncthreads();
-    if (p.split > 1) cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
+    if (p.cluster > 1) cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
     tc_fence_after();
     const uint32_t tmem = lds32(smem_u32(tmem_slot));
     if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 1] = globaltimer();
 
     SegIter it;
     it.init(p);
+
+    if (FUSE && warp >= kWarpAlloc) {
+        if (p.pdl) pdl_wait();  // x is produced by the previous kernel
+        const int qt = threadIdx.x - kWarpAlloc * 32;
+        fused_act_quant<BN>(p, fuse_geom(p), smem_u32(resb_ptr), tok, max_ready, b_ready, qt,
+                            p.x_dtype == kDtypeBF16);
+    }
 
     if (warp == kWarpProducer) {
         if (lane == 0) {
@@ -289,6 +528,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             // ring's worth of weight blocks while the producer of the activations is
             // still finishing, then wait for it and fetch the activation tiles.
             int pre = 0;
+            if (FUSE && p.dbg == 1) mbar_wait(b_ready, 0);
             if (p.pdl) {
                 SegIter ip = it;
                 bool more = true;
@@ -300,14 +540,14 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                             break;
                         }
                         const int nb = min(kUnitBlocks, ip.kb1 - kb);
-                        mbar_expect_tx(&w_full[pre], nb * (C::kBBytes + kWBlockBytes));
+                        mbar_expect_tx(&w_full[pre], nb * kWBlockBytes);
                         bulk_g2s(stages + pre * C::kStageBytes + C::kWOff,
                                  p.wp + (static_cast<size_t>(nt) * p.kblocks + kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[pre], pol_w);
                         ++pre;
                     }
                 }
-                pdl_wait();
+                if (!FUSE) pdl_wait();
             }
             int u = 0;
             while (it.next(p)) {
@@ -320,13 +560,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                     uint8_t* st = stages + s * C::kStageBytes;
                     if (u >= pre) {
                         mbar_wait(&w_empty[s], ((u / C::kStages) & 1) ^ 1);
-                        mbar_expect_tx(&w_full[s], nb * (C::kBBytes + kWBlockBytes));
+                        mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
                         bulk_g2s(st + C::kWOff, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol_w);
                     }
-                    for (int b = 0; b < nb; ++b)
-                        bulk_g2s(st + b * C::kBBytes, asrc + static_cast<size_t>(kb + b) * p.Mp * 128,
-                                 C::kBBytes, &w_full[s], pol_a);
+                    if (!FUSE) {  // own barrier: converters widen weights before B lands
+                        mbar_expect_tx(&b_full[s], nb * C::kBBytes);
+                        for (int b = 0; b < nb; ++b)
+                            bulk_g2s(st + b * C::kBBytes,
+                                     asrc + static_cast<size_t>(kb + b) * p.Mp * 128, C::kBBytes,
+                                     &b_full[s], pol_a);
+                    }
                 }
             }
             if (trc) trc[blockIdx.x * kTraceCta + 6] = globaltimer();
@@ -334,6 +578,22 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     } else if (warp == kWarpMma) {
         // Whole warp runs the (warp-uniform) loop; one elected lane issues tcgen05.
         int u = 0, j = 0;
+        int klo = 0, khi = 0;
+        if (FUSE) {
+            const FuseGeom g = fuse_geom(p);
+            klo = g.klo;
+            khi = g.khi;
+            mbar_wait(b_ready, 0);
+            tc_fence_after();
+            if (trc && lane == 0) trc[kTraceDbg + blockIdx.x * 8 + 7] = globaltimer();
+            // every class peer's codes have landed here: tell them their pushes are done
+            if (p.cluster > 1 && elect_one()) {
+                for (int d = 0; d < p.cluster; ++d)
+                    if (d != g.crank) mbar_arrive_remote(mapa_shared(smem_u32(push_done), d));
+            }
+            __syncwarp();
+        }
+        const uint32_t resb = smem_u32(resb_ptr);
         while (it.next(p)) {
             const int db = j & 1;
             mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
@@ -345,14 +605,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                 const int as = u % kAStages;
                 const bool mtr = trc && blockIdx.x == 0 && u < 64 && lane == 0;
                 if (mtr) trc[kTraceMma + u * 4 + 0] = clock64();
-                // a_full(u) is arrived by converters that already observed w_full(u)
-                // (the B tile shares that stage barrier), so one wait covers both.
+                // a_full(u): the converters observed w_full(u) and widened it into TMEM;
+                // the stage's activation tile has its own barrier.
                 mbar_wait(&a_full[as], (u / kAStages) & 1);
+                if (!FUSE) mbar_wait(&b_full[s], (u / C::kStages) & 1);
                 if (mtr) trc[kTraceMma + u * 4 + 1] = clock64();
                 if (u == 0 && trc && lane == 0) trc[blockIdx.x * kTraceCta + 2] = globaltimer();
                 if (mtr) trc[kTraceUnits + u * 4 + 3] = clock64();
                 tc_fence_after();
-                const uint32_t b_addr = stage_base + s * C::kStageBytes;
+                const uint32_t b_addr =
+                    FUSE ? resb + (kb - klo) * C::kBBytes : stage_base + s * C::kStageBytes;
                 const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
                 if (elect_one()) {
 #pragma unroll
@@ -499,7 +761,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                 const int n = nt * kTileN + r;
                 float* sc = scl + jj * (kTileN + BN);
                 sc[r] = n < p.N ? __ldg(p.sw + n) : 0.0f;
-                if (r < BN) sc[kTileN + r] = mt * BN + r < p.M ? __ldg(p.sa + mt * BN + r) : 0.0f;
+                if (r < BN)
+                    sc[kTileN + r] = FUSE ? tok[r]
+                                          : (mt * BN + r < p.M ? __ldg(p.sa + mt * BN + r) : 0.0f);
             }
             named_bar_sync(1, 128);
         }
@@ -511,6 +775,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             const int t0 = mt * BN;
             const bool csplit = it.is_split;
             const int crank = csplit ? static_cast<int>(blockIdx.x % p.split) : 0;
+            // cluster rank of this split group's rank 0 (clusters may hold several groups)
+            const uint32_t sbase = csplit ? static_cast<uint32_t>(blockIdx.x % p.cluster - crank) : 0u;
             const bool full = csplit ? crank == 0 : (it.kb0 == 0 && it.kb1 == p.kblocks);
             const bool owner = !csplit && !full && it.kb1 == p.kblocks;
             const int skt = it.tile - p.dp_tiles;
@@ -528,6 +794,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
             for (int i = 0; i < kPre; ++i)
                 sa_pre[i] = !(full || owner) ? 0.0f
                             : pref           ? sc[kTileN + i]
+                            : FUSE           ? tok[i]
                             : (t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f);
             const bool stage_out = C::kOutBytes > 0 && p.bulk_out && (full || owner) &&
                                    (nt + 1) * kTileN <= p.N;
@@ -572,7 +839,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                     for (int i = 0; i < 16; ++i) v[i] += w[i];  // exact int32 (mod 2^32)
                 }
                 tmem_wait_ld();
-                if (etr && tc == 0) trc[kTraceDbg + blockIdx.x * 4 + 0] = clock64();
                 if (full || owner) {
                     if (csplit) {
                         for (int c = 0; c < p.split - 1; ++c) {
@@ -595,7 +861,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                             for (int i = 0; i < 16; ++i) v[i] += static_cast<uint32_t>(w[i]);
                         }
                     }
-                    if (etr && tc == 0) trc[kTraceDbg + blockIdx.x * 4 + 1] = clock64();
                     if (stage_out) {
                         // value of (token tc+i, row r) into the smem tile [token][128 rows]
                         float val[16];
@@ -634,7 +899,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                     }
                 } else if (csplit) {  // rank > 0: partials into rank 0's smem (DSMEM)
                     const uint32_t dst0 =
-                        mapa_shared(fix_base + (((crank - 1) * BN + tc) * kTileN + r) * 4, 0);
+                        mapa_shared(fix_base + (((crank - 1) * BN + tc) * kTileN + r) * 4, sbase);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) st_dsmem_u32(dst0 + i * kTileN * 4, v[i]);
                 } else {
@@ -643,7 +908,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                         __stcg(slot + (tc + i) * kTileN + r, static_cast<int32_t>(v[i]));
                 }
             }
-            if (etr) trc[kTraceDbg + blockIdx.x * 4 + 2] = clock64();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[db]);
@@ -661,12 +925,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
                 }
                 named_bar_sync(1, 128);  // staging reusable by the next segment
             }
-            if (etr) trc[kTraceDbg + blockIdx.x * 4 + 3] = clock64();
             if (etr) et[1] = globaltimer();
             if (csplit && crank > 0) {
                 fence_acq_rel_cluster();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(recv_full), 0));
+                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(recv_full), sbase));
             } else if (!full && !owner) {
                 __threadfence();  // this thread's partials are visible before the count
                 named_bar_sync(1, 128);
@@ -686,19 +949,29 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
     __syncthreads();
     tc_fence_after();
     if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
+    // FUSE: this CTA's smem is the source of DSMEM bulk pushes; stay resident until every
+    // cluster peer has received them.
+    if (FUSE && p.cluster > 1 && threadIdx.x == 0) mbar_wait_cluster(push_done, 0);
     if (trc && threadIdx.x == 0) trc[blockIdx.x * kTraceCta + 5] = globaltimer();
 }
 
-template <int BN>
-cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
-    static_assert(Cfg<BN>::kFixBytes == 0 || Cfg<BN>::kFixBytes >= Cfg<BN>::kSlotBytes, "fix region");
-    using C = Cfg<BN>;
+template <int BN, bool FUSE = false>
+cudaError_t ensure_attr() {
+    using C = Cfg<BN, FUSE>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(w4a8_gemm_kernel<BN>,
+        attr_err = cudaFuncSetAttribute(w4a8_gemm_kernel<BN, FUSE>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
+    return attr_err;
+}
+
+template <int BN, bool FUSE = false>
+cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
+    using C = Cfg<BN, FUSE>;
+    static_assert(C::kFixBytes == 0 || C::kFixBytes >= C::kSlotBytes, "fix region");
+    const cudaError_t attr_err = ensure_attr<BN, FUSE>();
     if (attr_err != cudaSuccess) return attr_err;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -707,9 +980,9 @@ cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (p.split > 1) {
+    if (p.cluster > 1) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = p.split;
+        attr[na].val.clusterDim.x = p.cluster;
         attr[na].val.clusterDim.y = 1;
         attr[na].val.clusterDim.z = 1;
         ++na;
@@ -721,7 +994,7 @@ cudaError_t launch_bn(const Params& p, int grid, bool pdl, cudaStream_t st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, w4a8_gemm_kernel<BN>, p);
+    return cudaLaunchKernelEx(&cfg, w4a8_gemm_kernel<BN, FUSE>, p);
 }
 
 int pick_bn(int M) {
@@ -753,7 +1026,8 @@ struct SkPlan {
 };
 
 // Largest cluster split S with (S-1) partial tiles fitting the receive region.
-static int max_split_for_bn(int bn) {
+static int max_split_for_bn(int bn, bool fused = false) {
+    if (fused) return bn == 16 ? Cfg<16, true>::kFixBytes / Cfg<16, true>::kSlotBytes + 1 : 1;
     switch (bn) {
         case 16: return Cfg<16>::kFixBytes / Cfg<16>::kSlotBytes + 1;
         case 32: return Cfg<32>::kFixBytes / Cfg<32>::kSlotBytes + 1;
@@ -762,7 +1036,7 @@ static int max_split_for_bn(int bn) {
     }
 }
 
-static SkPlan plan_for(int M, int N, int K, int sms) {
+static SkPlan plan_for(int M, int N, int K, int sms, bool fused = false) {
     SkPlan s = {};
     s.bn = pick_bn(M);
     s.kblocks = static_cast<int>(pad_k(K) / kBlockK);
@@ -773,7 +1047,8 @@ static SkPlan plan_for(int M, int N, int K, int sms) {
     s.split = 0;
     static const char* mode_env = std::getenv("ODY_GEMM_SCHED");  // "sk" forces stream-K
     const bool force_sk = mode_env && std::string(mode_env) == "sk";
-    const int max_split = std::min({max_split_for_bn(s.bn), 8, std::max(1, s.kblocks / 2)});
+    const int max_split =
+        std::min({max_split_for_bn(s.bn, fused), 8, std::max(1, s.kblocks / 2)});
     if (!force_sk && max_split >= 1 && s.bn <= 64) {
         // DP waves over P' = floor(P/S)*S CTAs, then the R remaining tiles each split over
         // a cluster of S = min(P'/R, max) CTAs.  Choose S to minimise the busiest CTA's
@@ -854,6 +1129,7 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     p.sk_units = s.sk_units;
     p.max_contrib = s.max_contrib;
     p.split = s.split;
+    p.cluster = s.split > 1 ? s.split : 1;
     {
         const size_t esz = a.out_dtype == kDtypeF32 ? 4 : 2;
         p.bulk_out = (a.out && !a.acc_out && (static_cast<size_t>(a.N) * esz) % 16 == 0 &&
@@ -873,6 +1149,146 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
         case 64: return launch_bn<64>(p, s.P, a.pdl, st);
         default: return launch_bn<128>(p, s.P, a.pdl, st);
     }
+}
+
+// How many clusters of G fused-kernel CTAs (one per SM) can be resident at once.
+static int max_active_clusters_fused(int G) {
+    static int cache[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    if (G < 1 || G > 8) return 0;
+    if (cache[G] >= 0) return cache[G];
+    int n = 0;
+    if (ensure_attr<16, true>() == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G * 64);
+        cfg.blockDim = dim3(kNumThreads);
+        cfg.dynamicSmemBytes = Cfg<16, true>::kSmemBytes;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = G;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, w4a8_gemm_kernel<16, true>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+    }
+    cache[G] = n;
+    return n;
+}
+
+// Cluster size of the fused launch: the largest G <= 8 that is a multiple of the split S,
+// divides the grid and keeps every cluster co-resident (one CTA per SM); the share
+// classes then load and quantize 1/(G/S_eff) of the activations each.
+static int fused_cluster(const SkPlan& s) {
+    const int S = std::max(1, s.split);
+    static const char* env = std::getenv("ODY_FUSE_CLUSTER");  // diagnostics override
+    const int forced = env ? std::atoi(env) : 0;
+    for (int G = 8; G >= 2; --G) {
+        if (forced > 0 && G != forced) continue;
+        if (G % S != 0 || s.P % G != 0) continue;
+        if (max_active_clusters_fused(G) < s.P / G) continue;
+        return G;
+    }
+    return S;
+}
+
+// K1 fused into K3+K4 for decode widths (M <= 16): one kernel per linear.  Falls back to
+// act_quant + GEMM (two kernels, codes in the caller's a8 scratch) when not eligible.
+size_t linear_scratch_bytes(int M, int N, int K, int num_sms) {
+    return gemm_workspace_bytes(M, N, K, num_sms) + round_up(a8_bytes(M, K), 256) +
+           round_up(pad_m(M) * sizeof(float), 256);
+}
+
+static int g_linear_mode = 0;  // 0: act_quant + GEMM; 1: fused when eligible
+void set_linear_mode(int mode) { g_linear_mode = mode; }
+
+bool linear_is_fused(int M, int N, int K, int num_sms) {
+    if (g_linear_mode != 1) return false;
+    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+    const SkPlan s = plan_for(M, N, K, sms, true);
+    if (s.bn != 16 || s.split < 1) return false;
+    const int G = fused_cluster(s);
+    const int seff = (s.dp_tiles == 0 && s.split > 1) ? s.split : 1;
+    const int D = G / seff;
+    const int span = (s.kblocks + seff - 1) / seff;  // class range (resident B)
+    const int sub = (span + D - 1) / D;               // per-CTA quantized sub-slice
+    return static_cast<long long>(span) * 16 * 128 <= Cfg<16, true>::kResBBytes &&
+           static_cast<long long>(M) * sub * (kBlockK / 16) <= kFuseThreads * kFuseChunks;
+}
+
+cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
+    const int sms = a.max_ctas > 0 ? a.max_ctas : device_sm_count();
+    if (a.workspace_bytes < linear_scratch_bytes(a.M, a.N, a.K, sms)) return cudaErrorInvalidValue;
+    const size_t esz_x = a.x_dtype == kDtypeF32 ? 4 : 2;
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * esz_x) % 16 == 0;
+    uint8_t* ws = static_cast<uint8_t*>(a.workspace);
+    const size_t gws = gemm_workspace_bytes(a.M, a.N, a.K, sms);
+    if (!(aligned && a.x_dtype != kDtypeF32 && linear_is_fused(a.M, a.N, a.K, sms))) {
+        int8_t* q = reinterpret_cast<int8_t*>(ws + gws);
+        float* sa = a.sa_out ? a.sa_out
+                             : reinterpret_cast<float*>(ws + gws + round_up(a8_bytes(a.M, a.K), 256));
+        cudaError_t e = launch_act_quant(a.x, a.x_dtype, a.ldx, a.M, a.K, q, sa, nullptr, nullptr,
+                                         a.pdl, st);
+        if (e != cudaSuccess) return e;
+        GemmArgs g = {};
+        g.qa = q;
+        g.sa = sa;
+        g.wp = a.wp;
+        g.sw = a.sw;
+        g.out = a.out;
+        g.out_dtype = a.out_dtype;
+        g.workspace = ws;
+        g.workspace_bytes = gws;
+        g.M = a.M;
+        g.N = a.N;
+        g.K = a.K;
+        g.max_ctas = a.max_ctas;
+        g.pdl = a.pdl;
+        g.trace = a.trace;
+        return launch_w4a8_gemm(g, st);
+    }
+    const SkPlan s = plan_for(a.M, a.N, a.K, sms, true);
+    Params p = {};
+    p.wp = a.wp;
+    p.sw = a.sw;
+    p.out = a.out;
+    p.out_dtype = a.out_dtype;
+    p.M = a.M;
+    p.N = a.N;
+    p.K = a.K;
+    p.Mp = static_cast<int>(pad_m(a.M));
+    p.kblocks = s.kblocks;
+    p.m_tiles = s.m_tiles;
+    p.tiles = s.tiles;
+    p.dp_tiles = s.dp_tiles;
+    p.sk_units = 0;
+    p.max_contrib = 1;
+    p.split = s.split;
+    p.cluster = fused_cluster(s);
+    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    if (plan_log)
+        std::fprintf(stderr, "[ody] fused %dx%dx%d: grid %d split %d dp_tiles %d cluster %d (max active %d)\n",
+                     a.M, a.N, a.K, s.P, s.split, s.dp_tiles, p.cluster,
+                     max_active_clusters_fused(p.cluster));
+    const size_t esz = a.out_dtype == kDtypeF32 ? 4 : 2;
+    p.bulk_out = ((static_cast<size_t>(a.N) * esz) % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
+                     ? 1
+                     : 0;
+    p.x = a.x;
+    p.x_dtype = a.x_dtype;
+    p.ldx = a.ldx;
+    p.sa_out = a.sa_out;
+    p.ws_cnt = static_cast<uint32_t*>(a.workspace);
+    p.ws_slots = reinterpret_cast<int32_t*>(ws + kCounterBytes);
+    p.pdl = a.pdl ? 1 : 0;
+    static const char* dbg_env = std::getenv("ODY_DBG_FUSE");
+    p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
+    p.trace = a.trace;
+    return launch_bn<16, true>(p, s.P, a.pdl, st);
 }
 
 }  // namespace odyb200

@@ -55,6 +55,29 @@ struct GemmArgs {
 size_t gemm_workspace_bytes(int M, int N, int K, int num_sms);
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st);
 
+// The W4A8 linear y = x W^T end to end from unquantized activations: K1 fused into the
+// GEMM (decode widths, one kernel) or act_quant + GEMM.  workspace: linear_scratch_bytes.
+struct LinearArgs {
+    const void* x;        // M x K, row stride ldx elements, dtype x_dtype
+    int x_dtype;
+    size_t ldx;
+    const uint8_t* wp;    // w4 tile layout
+    const float* sw;
+    void* out;            // M x N row-major, out_dtype
+    int out_dtype;
+    float* sa_out;        // optional: the M per-token scales
+    void* workspace;
+    size_t workspace_bytes;
+    int M, N, K;
+    int max_ctas;
+    bool pdl;
+    unsigned long long* trace;
+};
+size_t linear_scratch_bytes(int M, int N, int K, int num_sms);
+bool linear_is_fused(int M, int N, int K, int num_sms);
+void set_linear_mode(int mode);  // 0: act_quant + GEMM (default); 1: K1 fused when eligible
+cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st);
+
 int device_sm_count();
 
 }  // namespace odyb200

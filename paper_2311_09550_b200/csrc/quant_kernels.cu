@@ -14,70 +14,13 @@
 #include "kernels.h"
 #include "layout.h"
 #include "ptx.cuh"
+#include "quant_common.cuh"
 
 namespace odyb200 {
 
 namespace {
 
-template <typename T>
-__device__ __forceinline__ float to_f32(T v);
-template <>
-__device__ __forceinline__ float to_f32<float>(float v) { return v; }
-template <>
-__device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
-template <>
-__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
-
-// ref quantize.cpp:12-18
-__device__ __forceinline__ int32_t clamp_code(float x, int32_t lo, int32_t hi) {
-    float r = roundf(x);
-    if (r < static_cast<float>(lo)) return lo;
-    if (r > static_cast<float>(hi)) return hi;
-    return static_cast<int32_t>(r);
-}
-
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ __forceinline__ float warp_min(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
 constexpr int kActThreads = 128;
-
-// Load 16 consecutive row elements starting at k0 (zero beyond K).
-template <typename T>
-__device__ __forceinline__ void load16(const T* __restrict__ row, int k0, int K, float (&v)[16]) {
-    if (k0 + 16 <= K && (reinterpret_cast<uintptr_t>(row + k0) & 15) == 0) {
-        constexpr int kPer = 16 / sizeof(T);
-#pragma unroll
-        for (int i = 0; i < 16; i += kPer) {
-            uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + k0 + i));
-            const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) v[i + j] = to_f32(e[j]);
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = (k0 + i < K) ? to_f32(row[k0 + i]) : 0.0f;
-    }
-}
-
-// Exact fast path for clamp(roundf(fl(x / S))): with r = RN(1/S), q' = RN(x * r) is
-// within |x/S| * 1.8e-7 <= 2.3e-5 of fl(x/S) (|x/S| <= 127.0001 since S = max|x|/127).
-// roundf(q') can only differ from roundf(fl(x/S)) when a half-integer lies within that
-// distance, so those rare elements (and a non-finite r) take the IEEE division.
-__device__ __forceinline__ int32_t quant_code_i8(float x, float scale, float rcp, bool exact) {
-    const float qa = __fmul_rn(x, rcp);
-    const float a = fabsf(qa);
-    const float f = a - truncf(a);
-    if (exact || fabsf(f - 0.5f) < 6.0e-5f) return clamp_code(x / scale, -128, 127);
-    return clamp_code(qa, -128, 127);
-}
 
 // K1: per-token INT8 quantization, one CTA of NT threads per token row; every thread
 // keeps its MC 16-element chunks in registers across both passes.  Pass 1: row
@@ -138,16 +81,25 @@ act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int 
     for (int i = 0; i < MC; ++i) {
         const int c = threadIdx.x + i * NT;
         if (c < nchunks) {
+            uint32_t tb[16];
+            bool redo = exact;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) tb[e] = quant_byte_fast(v[i][e], rcp, redo);
             uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t acc = 0;
+            for (int j = 0; j < 4; ++j)
+                w[j] = pack4_low_bytes(tb[4 * j], tb[4 * j + 1], tb[4 * j + 2], tb[4 * j + 3]);
+            if (redo) {  // rare: a near-half-integer quotient or non-finite 1/S
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int32_t code = quant_code_i8(v[i][j * 4 + b], scale, rcp, exact);
-                    acc |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * b);
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int32_t code = quant_code_i8(v[i][j * 4 + b], scale, rcp, true);
+                        acc |= (static_cast<uint32_t>(code) & 0xFFu) << (8 * b);
+                    }
+                    w[j] = acc;
                 }
-                w[j] = acc;
             }
             const size_t off = a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, Mp);
             *reinterpret_cast<uint4*>(q + off) = make_uint4(w[0], w[1], w[2], w[3]);

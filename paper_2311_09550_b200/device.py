@@ -155,6 +155,20 @@ class Workspace:
         return ws
 
     @classmethod
+    def get_linear(cls, m: int, n: int, k: int, device) -> torch.Tensor:
+        """Workspace for w4a8_linear (stream-K state + fallback a8 scratch)."""
+        return cls._sized(lib().ody_dev_linear_workspace_bytes(m, n, k), device)
+
+    @classmethod
+    def _sized(cls, need: int, device) -> torch.Tensor:
+        dev = torch.device(device)
+        ws = cls._per_device.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+            cls._per_device[dev] = ws
+        return ws
+
+    @classmethod
     def get(cls, m: int, n: int, k: int, device) -> torch.Tensor:
         dev = torch.device(device)
         need = lib().ody_dev_workspace_bytes(m, n, k)
@@ -205,6 +219,32 @@ def dequant_epilogue(acc: torch.Tensor, sa: torch.Tensor, sw: torch.Tensor, out_
     return out
 
 
+def w4a8_linear(x: torch.Tensor, w: W4Weight, out_dtype=torch.float16,
+                out: torch.Tensor | None = None, sa_out: torch.Tensor | None = None,
+                max_ctas: int = 0, pdl: bool = False, stream=None,
+                workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """The whole W4A8 linear y = x W^T from unquantized x (K1 + K3 + K4).
+
+    Decode widths (m <= 16) run as ONE kernel: the per-token INT8 quantization happens
+    inside the GEMM (codes stay in shared memory).  Bit-identical to
+    ``w4a8_gemm(act_quant(x), w)``."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.shape[1] != w.k:
+        raise OdyError(1, "gemm_w4a8_fast: inner dims disagree")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    m, k = x.shape
+    if out is None:
+        out = torch.empty((m, w.n), dtype=out_dtype, device=x.device)
+    if workspace is None:
+        workspace = Workspace.get_linear(m, w.n, k, x.device)
+    check(lib().ody_dev_w4a8_linear(
+        x.data_ptr(), _DT[x.dtype], x.stride(0), w.packed.data_ptr(), w.s.data_ptr(), m, w.n, k,
+        _DT[out.dtype], out.data_ptr(), sa_out.data_ptr() if sa_out is not None else None,
+        workspace.data_ptr(), workspace.numel(), max_ctas, int(pdl), _stream(stream)))
+    return out
+
+
 class W4A8Linear:
     """A linear layer on the FastGEMM path: y = x @ W^T with W4 per-channel weights
     and dynamic per-token A8 activations (the paper's W4A8 linear)."""
@@ -226,5 +266,4 @@ class W4A8Linear:
         return self.weight.n
 
     def __call__(self, x: torch.Tensor, pdl: bool = False) -> torch.Tensor:
-        a = act_quant(x, pdl=pdl)
-        return w4a8_gemm(a, self.weight, self.out_dtype, pdl=pdl)
+        return w4a8_linear(x, self.weight, self.out_dtype, pdl=pdl)

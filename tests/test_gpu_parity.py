@@ -295,3 +295,51 @@ def test_error_paths_match_reference():
     with pytest.raises(OdyError) as e:
         api.run_engine(1, None, aq, wq)
     assert e.value.status == ODY_EINVAL
+
+
+@pytest.fixture(params=[0, 1], ids=["two_kernel", "fused"])
+def linear_mode(request, dev):
+    """Both lowerings of w4a8_linear: act-quant kernel + GEMM, and K1 fused into the GEMM."""
+    dev.lib().ody_dev_set_linear_mode(request.param)
+    yield request.param
+    dev.lib().ody_dev_set_linear_mode(0)
+
+
+@pytest.mark.parametrize("m", [1, 3, 16, 17, 64])
+@pytest.mark.parametrize("layer", ["qkv", "o", "gate_up", "down"])
+def test_fused_linear_matches_oracle(m, layer, linear_mode, oracle, torch_cuda, dev):
+    """w4a8_linear (either lowering) == oracle act quant + FastGEMM, bit for bit,
+    including the per-token scales it exports."""
+    torch = torch_cuda
+    n, k = LLAMA13B[layer]
+    r = oracle.rng(77 + m)
+    a16 = oracle.gaussian_fill(r, (m, k), 1.5).astype(np.float16)  # fp16 x: the fused path
+    a = a16.astype(np.float32)
+    codes, sa = oracle.quantize_activations(a)
+    rs = np.random.default_rng(m + n)
+    wt = torch.from_numpy((rs.standard_normal((n, k), dtype=np.float32) * 0.1)).cuda()
+    wq = dev.W4Weight.quantize(wt)
+    flat = wq.to_flat().cpu().numpy()
+    sw = wq.s.cpu().numpy()
+    want = oracle.fast_gemm(codes, sa, flat, sw, m, n, k, threads=THREADS)
+    sa_out = torch.empty(m, dtype=torch.float32, device="cuda")
+    got = dev.w4a8_linear(torch.from_numpy(a16).cuda(), wq, torch.float32, sa_out=sa_out)
+    assert np.array_equal(bits_of(sa_out.cpu().numpy()), bits_of(sa))
+    got_np = got.cpu().numpy()
+    if not np.array_equal(bits_of(got_np), bits_of(want)):
+        bad = np.argwhere(got_np != want)
+        pytest.fail(f"{len(bad)} mismatches, first {bad[:4].tolist()}")
+    assert dev.lib().ody_dev_linear_is_fused(m, n, k) == (1 if (linear_mode and m <= 16) else 0)
+
+
+def test_fused_linear_input_dtypes(linear_mode, oracle, torch_cuda, dev):
+    torch = torch_cuda
+    m, n, k = 16, 5120, 5120
+    wq = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.05)
+    flat, sw = wq.to_flat().cpu().numpy(), wq.s.cpu().numpy()
+    for dt in (torch.float16, torch.bfloat16, torch.float32):
+        x = (torch.randn((m, k), device="cuda") * 3).to(dt)
+        codes, sa = oracle.quantize_activations(x.float().cpu().numpy())
+        want = oracle.fast_gemm(codes, sa, flat, sw, m, n, k, threads=THREADS)
+        got = dev.w4a8_linear(x, wq, torch.float16)
+        assert torch.equal(got.cpu(), torch.from_numpy(want).to(torch.float16))

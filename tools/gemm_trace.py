@@ -49,16 +49,52 @@ def trace_one(name, m, n, k, pdl, reps=3):
           f"weights {n * k / 2 / 1e6:.1f} MB -> {n * k / 2 / (span * 1e-6) / 1e9:.0f} GB/s")
 
 
+def fused_trace(m=16, n=15360, k=5120):
+    x = (torch.randn((m, k), device="cuda") * 2).half()
+    wq = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1)
+    out = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    dbg0 = 148 * 8 + 64 * 4 + 148 * 16 + 256
+    buf = torch.zeros(dbg0 + 148 * 8, dtype=torch.int64, device="cuda")
+    dev.w4a8_linear(x, wq, out=out)
+    torch.cuda.synchronize()
+    lib().ody_dev_set_trace(buf.data_ptr())
+    dev.w4a8_linear(x, wq, out=out)
+    torch.cuda.synchronize()
+    lib().ody_dev_set_trace(None)
+    cta = buf[:148 * 8].view(148, 8).cpu().numpy()
+    live = cta[:, 0] > 0
+    base = cta[live, 0].min()
+    d = buf[dbg0:].view(148, 8).cpu().numpy()[live]
+    rel = lambda v: (v - base) / 1000.0
+    print(f"fused {m}x{n}x{k}: CTAs {live.sum()}")
+    for i, nm in [(0, "loads issued"), (1, "local max"), (4, "max sent"), (5, "max recv"),
+                  (2, "scales done"), (6, "codes stored"), (3, "pushes issued"), (7, "b_ready")]:
+        col = d[:, i]
+        if (col == 0).all():
+            continue
+        col = rel(col)
+        print(f"   {nm:>14}: min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
+    for i, nm in [(1, "setup"), (2, "first_data"), (3, "last_mma"), (5, "exit")]:
+        col = rel(cta[live, i])
+        print(f"   {nm:>14}: min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--pdl", type=int, default=0)
     ap.add_argument("--units", action="store_true")
     ap.add_argument("--epi", action="store_true")
+    ap.add_argument("--fused", action="store_true")
     ap.add_argument("--layer", default="o")
     args = ap.parse_args()
     if args.units:
         unit_trace(args.m)
+        return
+    if args.fused:
+        shapes = {"qkv": (15360, 5120), "o": (5120, 5120), "gate_up": (27648, 5120), "down": (5120, 13824)}
+        for nm in (shapes if args.layer == "all" else [args.layer if args.layer in shapes else "qkv"]):
+            fused_trace(args.m, *shapes[nm])
         return
     if args.epi:
         n, k = {"qkv": (15360, 5120), "o": (5120, 5120), "gate_up": (27648, 5120),

@@ -20,13 +20,17 @@ def main():
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--graph", type=int, default=1)
+    ap.add_argument("--fused", action="store_true")
     args = ap.parse_args()
     m = args.m
+    lib().ody_dev_set_linear_mode(1 if args.fused else 0)
     ws = [dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1) for _, n, k in LAYERS]
     xs = {k: (torch.randn((m, k), device="cuda") * 2).half() for k in (HIDDEN, INTER)}
     a_buf = {k: dev.act_quant(xs[k]) for k in (HIDDEN, INTER)}
     outs = [torch.empty((m, n), dtype=torch.float16, device="cuda") for _, n, _ in LAYERS]
     wsb = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
+    for _, n, k in LAYERS:
+        wsb = dev.Workspace.get_linear(m, n, k, "cuda")
     st = torch.cuda.Stream()
     gtr = [torch.zeros(148 * 8 + 4096, dtype=torch.int64, device="cuda") for _ in LAYERS]
     atr = [torch.zeros(8 * 1024, dtype=torch.int64, device="cuda") for _ in LAYERS]
@@ -34,9 +38,12 @@ def main():
     def step(trace):
         for i, (w, (_, n, k)) in enumerate(zip(ws, LAYERS)):
             lib().ody_dev_set_act_trace(atr[i].data_ptr() if trace else None)
-            dev.act_quant(xs[k], out=a_buf[k], pdl=bool(args.pdl), stream=st)
             lib().ody_dev_set_trace(gtr[i].data_ptr() if trace else None)
-            dev.w4a8_gemm(a_buf[k], w, out=outs[i], pdl=bool(args.pdl), stream=st, workspace=wsb)
+            if not args.fused:
+                dev.act_quant(xs[k], out=a_buf[k], pdl=bool(args.pdl), stream=st)
+                dev.w4a8_gemm(a_buf[k], w, out=outs[i], pdl=bool(args.pdl), stream=st, workspace=wsb)
+            else:
+                dev.w4a8_linear(xs[k], w, out=outs[i], pdl=bool(args.pdl), stream=st, workspace=wsb)
         lib().ody_dev_set_act_trace(None)
         lib().ody_dev_set_trace(None)
 
@@ -65,15 +72,19 @@ def main():
     for i, (name, n, k) in enumerate(LAYERS):
         a8 = atr[i][: 8 * 1024].view(1024, 8).cpu().numpy()
         a8 = a8[a8[:, 0] > 0]
+        if len(a8) == 0:
+            a8 = np.zeros((1, 8), np.int64)
         a = a8[:, :2]
         act_detail.append((name, a8))
         t = gtr[i][: 148 * 8].view(148, 8).cpu().numpy()
         ev.append((f"act_quant[{name}]", a[:, 0], a[:, 1], None))
         ev.append((f"gemm[{name}] {n}x{k}", t[:, 0], t[:, 5], t))
-    base = min(e[1][e[1] > 0].min() for e in ev)
+    base = min(e[1][e[1] > 0].min() for e in ev if (e[1] > 0).any())
     print(f"M={m} pdl={args.pdl} graph={args.graph}  (us from first kernel entry)")
     print(f"{'kernel':32s} {'entry0':>8s} {'entry_max':>9s} {'exit_min':>8s} {'exit_max':>8s}  extra")
     for name, ent, ex, t in ev:
+        if not (ent > 0).any():
+            continue
         ent = (ent[ent > 0] - base) / 1e3
         ex = (ex[ex > 0] - base) / 1e3
         extra = ""
