@@ -41,6 +41,7 @@ HIDDEN, INTER = 5120, 13824
 LAYERS = [("qkv", 3 * HIDDEN, HIDDEN), ("o", HIDDEN, HIDDEN), ("gate_up", 2 * INTER, HIDDEN),
           ("down", HIDDEN, INTER)]
 METRIC = "W4A8 GEMM HBM GB/s (LLaMA-13B decoder-layer linears, decode)"
+LOWERINGS = {"two_kernel": 0, "fused_prologue": 1, "decode": 2, "program": 2}
 
 
 def gemm_bytes(m, n, k):
@@ -190,17 +191,31 @@ def run_b200(args):
         ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")
     stream = torch.cuda.Stream()
     launches_per_step = 0
-    lib().ody_dev_set_linear_mode(1 if args.fused else 0)
+    lib().ody_dev_set_linear_mode(LOWERINGS[args.lowering])
+
+    programs = None
+    if world == 1 and args.lowering == "program":
+        # one persistent launch per step: the layer's 4 linears as a linear program; the
+        # next step's first weights are passed as the L2 prefetch hint
+        programs = [dev.Program([dev.LinearCall(xs[w.k], w, outs[name]) for name, w in layers[c]],
+                                prefetch_next=layers[(c + 1) % copies][0][1] if args.prefetch else None)
+                    for c in range(copies)]
 
     def step(copy_idx, pdl):
         nonlocal launches_per_step
+        if programs is not None:
+            programs[copy_idx].run(pdl=pdl, stream=stream)
+            launches_per_step = 1 if programs[copy_idx].fused else 2 * len(LAYERS)
+            return
         if world == 1:
             cnt = 0
-            for name, w in layers[copy_idx]:
-                # public device API: act-quant kernel + FastGEMM (PDL-chained), or one
-                # kernel with K1 fused into the GEMM prologue under --fused
+            seq = layers[copy_idx]
+            for li, (name, w) in enumerate(seq):
+                # public device API, one call per linear (see --lowering); the weights of
+                # the linear launched next are passed as an L2 prefetch hint
+                nxt = seq[li + 1][1] if li + 1 < len(seq) else layers[(copy_idx + 1) % copies][0][1]
                 dev.w4a8_linear(xs[w.k], w, out=outs[name], pdl=pdl, stream=stream,
-                                workspace=ws_buf)
+                                workspace=ws_buf, prefetch_next=nxt if args.prefetch else None)
                 cnt += 1 if lib().ody_dev_linear_is_fused(m, w.n, w.k) else 2
             launches_per_step = cnt
         else:
@@ -263,13 +278,14 @@ def run_b200(args):
                    "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
                    "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
                    "cuda_graph": use_graph, "pdl": bool(args.pdl),
-                   "lowering": "fused act-quant prologue" if args.fused else "act_quant + FastGEMM"},
+                   "l2_prefetch_next_weights": bool(args.prefetch),
+                   "lowering": args.lowering},
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps if world == 1 else None,
     }
 
     if rank == 0 and world == 1:
-        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs)
+        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs)
         result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
         result["e2e"] = e2e_c_abi(args, m)
         if not args.no_cpu:
@@ -302,12 +318,12 @@ def _graph_time(fn, stream, reps, warm=3):
     return s.elapsed_time(e) / reps
 
 
-def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs):
+def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs=None):
     """Dominant kernel = the FastGEMM (HBM-bound at decode).  Its average launch
     duration is timed with CUDA events on its own stream over graph replays that
     rotate all weight copies (each launch streams fresh weights from HBM)."""
     hbm, kind = peaks()
-    fused = bool(args.fused)
+    fused = args.lowering != "two_kernel"
     if not fused:
         for k in (HIDDEN, INTER):
             dev.act_quant(xs[k], out=a_buf[k], stream=stream)
@@ -331,6 +347,19 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs):
         tot_bytes += b
         tot_ms += ms
     achieved = tot_bytes / (tot_ms * 1e-3) / 1e9
+    launch = None
+    if programs is not None:
+        # the dominant kernel of the program lowering is the ONE program launch per step:
+        # algorithmic bytes of the layer / its average launch duration (graph of the copies,
+        # back to back, no PDL), each launch streaming fresh weights
+        def fn():
+            for pr in programs:
+                pr.run(stream=stream)
+
+        ms = _graph_time(fn, stream, reps=50) / len(programs)
+        launch = {"kernel": "w4a8_decode_kernel (linear program: the layer's 4 linears)",
+                  "us": round(ms * 1e3, 3), "bytes": step_bytes(m)}
+        achieved = step_bytes(m) / (ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(prof):
@@ -341,10 +370,13 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs):
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
-            "kernel": ("w4a8_gemm_kernel" if not fused else
-                       "w4a8_gemm_kernel<16,FUSE> (K1 fused)") +
+            "kernel": {"two_kernel": "w4a8_gemm_kernel (act_quant launched separately)",
+                       "fused_prologue": "w4a8_gemm_kernel<16,FUSE> (K1 fused)",
+                       "decode": "w4a8_decode_kernel (K1+K3+K4 in one launch)",
+                       "program": "w4a8_decode_kernel (K1+K3+K4 in one launch)"}[args.lowering] +
                       " -- avg over the 4 layer shapes, bytes-weighted",
             "per_shape": per,
+            "program_launch": launch,
             "algorithmic_bytes_per_launch": {
                 nm: (gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k))
                 for nm, n, k in LAYERS}}
@@ -522,9 +554,14 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="also report the M=1..64 GEMM sweep")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--prefetch", type=int, default=1,
+                    help="pass the next linear's weights as an L2 prefetch hint")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--fused", action="store_true",
-                    help="lower each linear to ONE kernel (act quant fused into the GEMM prologue)")
+    ap.add_argument("--lowering", default="program", choices=list(LOWERINGS),
+                    help="program: the layer's linears in ONE persistent launch; "
+                         "decode: one cluster split-K kernel per linear (K1 fused per k-slice); "
+                         "fused_prologue: K1 fused via a cluster code all-gather; "
+                         "two_kernel: act_quant kernel + FastGEMM")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -153,19 +153,59 @@ ody_status ody_dev_workspace_init(void* workspace, size_t bytes, void* stream);
 
 /* K1+K3+K4: the whole W4A8 linear y = x W^T from unquantized activations x (m x k,
  * dtype x_dtype, row stride ldx).  For decode widths (m <= 16) the per-token INT8
- * quantization runs inside the GEMM kernel (codes never leave shared memory; a tile
- * split over a thread-block cluster combines the per-token maxima through DSMEM), one
- * launch per linear; otherwise act quant + GEMM.  Results are identical to
+ * quantization runs inside the GEMM kernel: each CTA of a thread-block cluster
+ * quantizes its own k-slice, the cluster combines the per-token maxima through DSMEM
+ * and reduce-scatters the int32 partial tiles through DSMEM -- one launch per linear;
+ * otherwise act quant + GEMM.  Results are identical to
  * ody_dev_act_quant + ody_dev_w4a8_gemm.  s_a_out (optional, m floats) receives the
  * per-token scales.  workspace: ody_dev_linear_workspace_bytes(m,n,k), zeroed once. */
 ody_status ody_dev_w4a8_linear(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed,
                                const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
                                void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
                                int max_ctas, int pdl, void* stream);
+/* Same, plus a cross-kernel L2 prefetch hint: once this linear's own weight loads are
+ * issued, its CTAs prefetch next_w[0, next_w_bytes) (the packed weights of the linear
+ * the caller launches next) into L2, so HBM keeps streaming through the kernel boundary
+ * and the next linear's activation prologue.  A pure hint: results never depend on it;
+ * next_w may be NULL. */
+ody_status ody_dev_w4a8_linear_pf(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed,
+                                  const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                                  void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
+                                  int max_ctas, int pdl, const void* next_w, size_t next_w_bytes,
+                                  void* stream);
 size_t ody_dev_linear_workspace_bytes(size_t m, size_t n, size_t k);
+
+/* A "linear program": up to 8 W4A8 linears run by ONE persistent kernel launch when every
+ * linear is decode-width (m <= 16, 16-bit x): the weight stream never drains between
+ * the linears, and a linear whose x is the output of an earlier linear of the program
+ * (dep = that index; -1 = x is an external input) waits for it through grid-wide
+ * completion counters in the workspace.  Otherwise the linears run one after another
+ * (ody_dev_w4a8_linear each; stream order honours the deps).  Results are identical
+ * to running ody_dev_w4a8_linear on each linear in order.  workspace:
+ * ody_dev_program_workspace_bytes(lin, count) bytes, zeroed once (left zeroed). */
+typedef struct ody_linear_desc {
+    const void* x;           /* m x k, row stride ldx elements */
+    ody_dtype x_dtype;
+    size_t ldx;
+    const void* w_packed;    /* ody_dev_w4_quantize / ody_dev_w4_prepack output */
+    const float* s_w;
+    size_t m, n, k;
+    void* out;               /* m x n row-major */
+    ody_dtype out_dtype;
+    float* s_a_out;          /* optional: the m per-token scales */
+    int dep;                 /* -1, or index < this one whose out is this x */
+} ody_linear_desc;
+size_t ody_dev_program_workspace_bytes(const ody_linear_desc* lin, int count);
+ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, void* workspace,
+                                       size_t workspace_bytes, int max_ctas, int pdl,
+                                       const void* next_w, size_t next_w_bytes, void* stream);
+/* 1 if ody_dev_w4a8_linear_program runs these linears as one kernel launch. */
+int ody_dev_program_is_fused(const ody_linear_desc* lin, int count);
 int ody_dev_linear_is_fused(size_t m, size_t n, size_t k); /* 1: single fused kernel */
-/* Linear lowering: 0 (default) = act-quant kernel + FastGEMM (PDL-chained);
- * 1 = act quant fused into the GEMM prologue where eligible (M <= 16, 16-bit x). */
+/* Linear lowering: 0 = act-quant kernel + FastGEMM (PDL-chained); 1 = act quant fused
+ * into the GEMM prologue (cluster code all-gather) where eligible; 2 (default) = the
+ * cluster split-K decode kernel (K1 per k-slice + K3 + K4 in one launch) where eligible
+ * (m <= 16, 16-bit x), else 0. */
 void ody_dev_set_linear_mode(int mode);
 /* Diagnostics: when buf (device, >= 8 * #CTAs u64) is non-NULL, subsequent
  * ody_dev_w4a8_gemm launches record a per-CTA %globaltimer timeline into it:

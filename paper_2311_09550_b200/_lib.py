@@ -31,6 +31,13 @@ class ody_gemm_counters(ctypes.Structure):
                 ("zero_point_sub_ops", ctypes.c_uint64), ("final_scale_ops", ctypes.c_uint64)]
 
 
+class ody_linear_desc(ctypes.Structure):
+    """include/odyssey_b200.h ody_linear_desc (one linear of a linear program)."""
+    _fields_ = [("x", c_void_p), ("x_dtype", c_int), ("ldx", c_size_t), ("w_packed", c_void_p),
+                ("s_w", c_void_p), ("m", c_size_t), ("n", c_size_t), ("k", c_size_t), ("out", c_void_p),
+                ("out_dtype", c_int), ("s_a_out", c_void_p), ("dep", c_int)]
+
+
 # name -> (restype, argtypes); the complete exported surface of odyssey_b200.h
 SIGNATURES = {
     "ody_last_error": (c_char_p, []),
@@ -69,7 +76,14 @@ SIGNATURES = {
     "ody_dev_w4a8_linear": (c_int, [c_void_p, c_int, c_size_t, c_void_p, c_void_p, c_size_t, c_size_t,
                                     c_size_t, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_int,
                                     c_int, c_void_p]),
+    "ody_dev_w4a8_linear_pf": (c_int, [c_void_p, c_int, c_size_t, c_void_p, c_void_p, c_size_t, c_size_t,
+                                       c_size_t, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_int,
+                                       c_int, c_void_p, c_size_t, c_void_p]),
     "ody_dev_linear_workspace_bytes": (c_size_t, [c_size_t, c_size_t, c_size_t]),
+    "ody_dev_program_workspace_bytes": (c_size_t, [c_void_p, c_int]),
+    "ody_dev_w4a8_linear_program": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p,
+                                            c_size_t, c_void_p]),
+    "ody_dev_program_is_fused": (c_int, [c_void_p, c_int]),
     "ody_dev_linear_is_fused": (c_int, [c_size_t, c_size_t, c_size_t]),
     "ody_dev_set_linear_mode": (None, [c_int]),
     "ody_dev_set_trace": (None, [c_void_p]),

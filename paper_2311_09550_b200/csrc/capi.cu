@@ -567,6 +567,95 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
 void ody_dev_set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 void ody_dev_set_act_trace(void* buf) { set_act_trace(static_cast<unsigned long long*>(buf)); }
 
+namespace {
+constexpr size_t kProgramCtrRegion = kProgramCounterRegion;  // counters, then the scratch
+
+bool program_args(const ody_linear_desc* lin, int count, int max_ctas, std::vector<LinearArgs>* a,
+                  std::vector<int>* deps) {
+    a->assign(count, LinearArgs{});
+    deps->assign(count, -1);
+    for (int l = 0; l < count; ++l) {
+        const ody_linear_desc& d = lin[l];
+        LinearArgs& x = (*a)[l];
+        x.x = d.x;
+        x.x_dtype = static_cast<int>(d.x_dtype);
+        x.ldx = d.ldx;
+        x.wp = static_cast<const uint8_t*>(d.w_packed);
+        x.sw = d.s_w;
+        x.out = d.out;
+        x.out_dtype = static_cast<int>(d.out_dtype);
+        x.sa_out = d.s_a_out;
+        x.M = static_cast<int>(d.m);
+        x.N = static_cast<int>(d.n);
+        x.K = static_cast<int>(d.k);
+        x.max_ctas = max_ctas;
+        x.trace = g_trace;
+        (*deps)[l] = d.dep;
+    }
+    return true;
+}
+}  // namespace
+
+size_t ody_dev_program_workspace_bytes(const ody_linear_desc* lin, int count) {
+    if (!lin || count < 1 || count > kProgramMaxLinears) return 0;
+    size_t need = 0;
+    for (int l = 0; l < count; ++l)
+        need = std::max(need, linear_scratch_bytes(static_cast<int>(lin[l].m), static_cast<int>(lin[l].n),
+                                                   static_cast<int>(lin[l].k), 0));
+    std::vector<LinearArgs> a;
+    std::vector<int> deps;
+    program_args(lin, count, 0, &a, &deps);
+    return std::max(kProgramCtrRegion + need, program_scratch_bytes(a.data(), deps.data(), count));
+}
+
+int ody_dev_program_is_fused(const ody_linear_desc* lin, int count) {
+    if (!lin || count < 1 || count > kProgramMaxLinears) return 0;
+    std::vector<LinearArgs> a;
+    std::vector<int> deps;
+    program_args(lin, count, 0, &a, &deps);
+    return linear_mode() == 2 && program_eligible(a.data(), deps.data(), count, 0) ? 1 : 0;
+}
+
+ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, void* workspace,
+                                       size_t workspace_bytes, int max_ctas, int pdl,
+                                       const void* next_w, size_t next_w_bytes, void* stream) {
+    if (!lin || !workspace) return einval("ody_dev_w4a8_linear_program: null argument");
+    if (count < 1 || count > kProgramMaxLinears)
+        return einval("ody_dev_w4a8_linear_program: 1..8 linears per program");
+    for (int l = 0; l < count; ++l) {
+        const ody_linear_desc& d = lin[l];
+        if (!d.x || !d.w_packed || !d.s_w || !d.out) return einval("ody_dev_w4a8_linear_program: null argument");
+        if (d.m == 0 || d.n == 0 || d.k == 0) return einval("ody_dev_w4a8_linear_program: empty operand");
+        if (d.ldx < d.k) return einval("ody_dev_w4a8_linear_program: ldx < k");
+        if (d.k > kMaxK) return einval("GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
+        if (d.dep < -1 || d.dep >= l) return einval("ody_dev_w4a8_linear_program: dep must name an earlier linear");
+        if (d.x_dtype < ODY_DTYPE_F32 || d.x_dtype > ODY_DTYPE_BF16 || d.out_dtype < ODY_DTYPE_F32 ||
+            d.out_dtype > ODY_DTYPE_BF16)
+            return einval("bad dtype");
+    }
+    if (workspace_bytes < ody_dev_program_workspace_bytes(lin, count))
+        return einval("ody_dev_w4a8_linear_program: workspace too small");
+    return guarded([&] {
+        std::vector<LinearArgs> a;
+        std::vector<int> deps;
+        program_args(lin, count, max_ctas, &a, &deps);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (linear_mode() == 2 && program_eligible(a.data(), deps.data(), count, max_ctas)) {
+            cuda_check(launch_w4a8_program(a.data(), deps.data(), count, workspace, workspace_bytes, pdl != 0,
+                                           static_cast<const uint8_t*>(next_w), next_w ? next_w_bytes : 0, st),
+                       "w4a8 linear program launch");
+            return;
+        }
+        uint8_t* scratch = static_cast<uint8_t*>(workspace) + kProgramCtrRegion;
+        for (int l = 0; l < count; ++l) {
+            a[l].workspace = scratch;
+            a[l].workspace_bytes = workspace_bytes - kProgramCtrRegion;
+            a[l].pdl = pdl != 0;
+            cuda_check(launch_w4a8_linear(a[l], st), "w4a8_linear launch");
+        }
+    });
+}
+
 size_t ody_dev_linear_workspace_bytes(size_t m, size_t n, size_t k) {
     return linear_scratch_bytes(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0);
 }
@@ -581,6 +670,15 @@ ody_status ody_dev_w4a8_linear(const void* x, ody_dtype x_dtype, size_t ldx, con
                                const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
                                void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
                                int max_ctas, int pdl, void* stream) {
+    return ody_dev_w4a8_linear_pf(x, x_dtype, ldx, w_packed, s_w, m, n, k, out_dtype, out, s_a_out,
+                                  workspace, workspace_bytes, max_ctas, pdl, nullptr, 0, stream);
+}
+
+ody_status ody_dev_w4a8_linear_pf(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed,
+                                  const float* s_w, size_t m, size_t n, size_t k, ody_dtype out_dtype,
+                                  void* out, float* s_a_out, void* workspace, size_t workspace_bytes,
+                                  int max_ctas, int pdl, const void* next_w, size_t next_w_bytes,
+                                  void* stream) {
     if (!x || !w_packed || !s_w || !out || !workspace)
         return einval("ody_dev_w4a8_linear: null argument");
     if (m == 0 || n == 0 || k == 0) return einval("ody_dev_w4a8_linear: empty operand");
@@ -606,6 +704,8 @@ ody_status ody_dev_w4a8_linear(const void* x, ody_dtype x_dtype, size_t ldx, con
         a.K = static_cast<int>(k);
         a.max_ctas = max_ctas;
         a.pdl = pdl != 0;
+        a.next_wp = static_cast<const uint8_t*>(next_w);
+        a.next_bytes = next_w ? next_w_bytes : 0;
         a.trace = g_trace;
         if (workspace_bytes < linear_scratch_bytes(a.M, a.N, a.K, max_ctas))
             fail(ODY_EINVAL, "ody_dev_w4a8_linear: workspace too small");

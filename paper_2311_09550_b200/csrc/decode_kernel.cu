@@ -1,0 +1,1146 @@
+// decode_kernel.cu -- decode-width (M <= 16) W4A8 linears as ONE persistent kernel: a
+// "linear program" of up to kMaxLin linears y_l = x_l W_l^T, each with per-token INT8
+// activation quantization (K1), the FastGEMM mainloop (K3) and the dequantizing
+// epilogue (K4), from unquantized fp16/bf16 activations.  A single linear is a program
+// of length 1 (ody_dev_w4a8_linear).
+//
+// Reference semantics (bit-exact):
+//   S_t   = max_k |x[t,k]| / 127   (0 -> 2^-24)          ref quantize.cpp:22-35, 113-132
+//   q     = clamp(roundf(x / S_t), -128, 127)             ref quantize.cpp:12-18, 44
+//   acc16 = sum_k q[t,k] * (16 * w[n,k])                  ref gemm.cpp:229-249 (high-nibble lanes)
+//   y     = float(acc16 >> 4) * (S_t * S_w[n])            ref gemm.cpp:251-279
+//
+// Partition ("cluster split-K"): the grid is C clusters of S CTAs (S uniform over the
+// program).  For linear l, cluster c owns the 128-row weight tiles v, v+C, v+2C, ...
+// (v = (c + rot_l) mod C: independent linears rotate, so the program's tiles spread
+// evenly over the clusters); rank r owns k-blocks [r*kb/S, (r+1)*kb/S) of every tile.
+//   * a CTA needs only its own k-slice of x_l: it loads x[:, slice], takes the per-token
+//     partial max|x|, exchanges the S partial maxima over DSMEM (st.async -> the peers'
+//     mbarrier) and quantizes its slice straight into a resident, MMA-ready smem B;
+//   * the S int32 partial tiles are reduced by a DSMEM reduce-scatter: rank j owns rows
+//     [j*R, (j+1)*R) of each tile, the other ranks st.async those rows to it, and it adds
+//     them (integer addition: exact in any order) and runs the epilogue on its rows.
+// The weight stream never waits for activations: the producer walks the WHOLE program's
+// weight units from the first instruction (no griddepcontrol.wait on that path), with an
+// L2 prefetch window ahead of the smem ring, so HBM keeps streaming through every
+// linear's activation prologue and epilogue tail.  A linear whose x is the output of an
+// earlier linear of the program (dep >= 0) waits for that linear's grid-wide completion
+// counter before loading x; the counters reset themselves at the end of the launch.
+//
+// Warp roles (12 warps, one CTA per SM; 168 registers per thread):
+//   0      producer: 1-D bulk copies (UBLKCP) of 16 KiB packed-INT4 weight units and of
+//          the per-tile channel scales
+//   1      MMA: tcgen05.mma.cta_group::1.kind::i8, A (widened weights) from TMEM,
+//          B (resident activation codes) from smem, int32 D in TMEM (double-buffered)
+//   2      TMEM allocator; warps 2..11: the activation-quantization prologue of each linear
+//   4..7   converters (one warp per TMEM sub-partition): smem packed INT4 ->
+//          (w<<4)&0xF0F0F0F0 / w&0xF0F0F0F0 int8 lanes (the paper's SINT4->S8 trick) ->
+//          tcgen05.st
+//   8..11  epilogue: tcgen05.ld D -> DSMEM reduce-scatter -> >>4, scale, store
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.h"
+#include "layout.h"
+#include "ptx.cuh"
+#include "quant_common.cuh"
+
+namespace odyb200 {
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kWarpProducer = 0;
+constexpr int kWarpMma = 1;
+constexpr int kWarpAlloc = 2;
+constexpr int kWarpConv0 = 4;
+constexpr int kConvGroups = 1;
+constexpr int kWarpEpi0 = 8;
+constexpr int kBN = 16;                 // tokens per tile (MMA N); decode widths M <= 16
+constexpr int kUnitBlocks = 2;          // k-blocks per pipeline unit (16 KiB of weights)
+constexpr int kUnitBytes = kUnitBlocks * kWBlockBytes;
+constexpr int kBN_ = 16;
+constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBN_ * 128;  // weights + pre-quantized B tiles
+constexpr int kAStages = 4;             // TMEM A stages (64 columns each)
+constexpr int kAStageCols = kUnitBlocks * kBlockK / 4;
+constexpr int kAColBase = 256;
+constexpr int kDBufs = 4;               // TMEM accumulator buffers (tiles in flight to the epilogue)
+constexpr int kTmemCols = 512;
+constexpr int kMaxSplit = 8;            // portable cluster size
+constexpr int kMaxKbPerCta = 28;        // resident B: 28 k-blocks x 16 tokens x 128 B = 56 KiB
+constexpr int kBBlockBytes = kBN * 128;
+constexpr int kResBBytes = kMaxKbPerCta * kBBlockBytes;
+constexpr int kQThreads = 320;          // warps 2..11 quantize the activations
+constexpr int kQHold = 3;              // 16-element activation chunks held per thread per batch
+constexpr int kStages = 7;
+constexpr int kMaxLin = 8;
+constexpr int kSmemBytes = kStages * kStageBytes + kResBBytes + 16 /*finalise flag*/ +
+                           kMaxSplit * kBN * 4 /*peer maxima*/ + 3 * kBN * 4 /*max, scale, rcp*/ +
+                           1024 /*barriers*/ + 1024 /*alignment*/;
+static_assert(kSmemBytes <= 227 * 1024, "smem budget");
+static_assert(kAColBase + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
+static_assert(4 * 16 <= 256, "D buffers below the A stages");
+// kind::i8, D=s32, A=B=s8 signed, K-major both, N=16, M=128
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                            (static_cast<uint32_t>(kBN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+constexpr int kTraceCta = 32;  // [entry, setup, -, -, -, exit, producer done, meta, per linear 4 x 6]
+
+struct LinDesc {
+    const void* x;        // M x K, row stride ldx elements, f16 or bf16
+    size_t ldx;
+    const uint8_t* wp;    // w4 tile layout
+    const float* sw;
+    void* out;            // M x N row-major
+    float* sa_out;        // optional per-token scales
+    int x_bf16, out_dtype;
+    int M, N, K, kblocks, n_tiles;
+    const int8_t* qa;     // pre-quantized activations (a8 k-block layout, Mp rows) or NULL:
+    const float* sa;      //   then B tiles ride in the ring stages and no prologue runs
+    int Mp;
+    int dep;              // x is the output of linear `dep` of this program (-1: external)
+    int signal;           // a later linear depends on this one: publish its completion
+    int rot;              // tile rotation (independent linears spread over the clusters)
+};
+
+struct PParams {
+    LinDesc lin[kMaxLin];
+    int L;
+    int S, C;             // cluster size (split-K factor), clusters
+    uint32_t* ctr;        // [kMaxLin] completion counters + [kMaxLin] exit counter (zeroed)
+    int32_t* acc;         // [program tiles][BN][128] split-K accumulators in L2 (zeroed)
+    uint32_t* tile_cnt;   // [program tiles] split arrivals (zeroed)
+    int pdl;
+    int pf_units;         // L2 prefetch window past the smem ring (units)
+    const uint8_t* next_wp;  // cross-kernel hint: L2-prefetch this slice of the next weights
+    size_t next_bytes;
+    int dbg;              // diagnostics (ODY_DBG_DECODE): 1 store raw x (no quant math), 2 no IEEE redo
+    unsigned long long* trace;
+};
+
+__device__ __forceinline__ uint64_t b_desc(uint32_t smem_addr) {
+    // K-major SWIZZLE_128B: start>>4, SBO = 1024 B (8 rows x 128 B), version 1, swizzle 128B.
+    return static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(64) << 32) |
+           (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+
+// ---- DSMEM helpers local to this kernel ----
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];"
+                 ::"r"(remote_addr), "r"(v), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint32_t a, uint32_t b, uint32_t c,
+                                            uint32_t d, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];"
+                 ::"r"(remote_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ float half_bits_to_f32(uint32_t w, int hi, bool bf16) {
+    const unsigned short h = hi ? static_cast<unsigned short>(w >> 16) : static_cast<unsigned short>(w);
+    return bf16 ? __uint_as_float(static_cast<uint32_t>(h) << 16) : __half2float(__ushort_as_half(h));
+}
+
+// Elements whose fast quotient lies within 6e-5 of a half-integer (flag bit e) are
+// recomputed with the reference's IEEE division and roundf (ref quantize.cpp:44).
+// Rare (~1e-4 of elements): kept out of line, and only the flagged bytes are redone.
+// Out-of-line slow path of quant16 (a lane of the chunk is within 7e-5 of a half-integer,
+// ~1e-4 of elements, or 1/S overflowed): find those lanes and redo them with the
+// reference's IEEE division and roundf (ref quantize.cpp:12-18, 44).
+__device__ __noinline__ uint4 fix16(uint4 q, uint4 r0, uint4 r1, float scale, float rcp, bool bf16) {
+    uint32_t o[4] = {q.x, q.y, q.z, q.w};
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const bool all = !(rcp < INFINITY);
+    for (int e = 0; e < 16; ++e) {
+        const float x = half_bits_to_f32(w[e >> 1], e & 1, bf16);
+        const uint32_t byte = (o[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+        const float r = static_cast<float>(static_cast<int8_t>(byte));
+        if (!all && fabsf(__fmaf_rn(x, rcp, -r)) < 0.49993f) continue;
+        const int32_t code = clamp_code(x / scale, -128, 127);
+        const int sh = 8 * (e & 3);
+        o[e >> 2] = (o[e >> 2] & ~(0xFFu << sh)) | ((static_cast<uint32_t>(code) & 0xFFu) << sh);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+struct uint4x2 {
+    uint4 a, b;
+};
+
+// ---- packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100) ----
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long v, uint32_t& a, uint32_t& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+template <bool BF16>
+__device__ __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
+    if (BF16) {
+        lo = __uint_as_float(w << 16);
+        hi = __uint_as_float(w & 0xFFFF0000u);
+    } else {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
+        lo = f.x;
+        hi = f.y;
+    }
+}
+
+// 16 packed 16-bit values -> 16 INT8 codes, bit-exact with clamp(roundf(fl(x / S))):
+//   t = RN(x*rcp + 1.5*2^23)   rounds the EXACT product x*rcp to an integer r (low byte of
+//                              t = r, two's complement; |x*rcp| <= 127.0001 needs no clamp)
+//   d = RN(x*rcp - r)          its distance to r, accurate to 2^-25
+// |x*rcp - x/S| <= |x/S| * 2^-24 < 7.6e-6 and |fl(x/S) - x/S| < 7.6e-6, so whenever
+// |d| < 0.49993 both the exact and the reference's rounded quotient round to r.  The
+// check d*d - 0.49993^2 < 0 is folded over all 16 lanes with sign-bit ANDs; a chunk with
+// any lane at or past the threshold (~1e-4 of elements) is redone element by element
+// through the IEEE division (fix16).  Two lanes per instruction: ~4.3 ops per element.
+template <bool BF16>
+__device__ __forceinline__ uint4 quant16(uint4 r0, uint4 r1, float scale, float rcp, int dbg) {
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const unsigned long long RCP = pk2(rcp, rcp);
+    const unsigned long long MAGIC = pk2(12582912.0f, 12582912.0f);
+    const unsigned long long THR = pk2(-0.2499300049f, -0.2499300049f);  // -(0.49993^2)
+    uint32_t t[16];
+    uint32_t sign_and = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float lo, hi;
+        unpack2<BF16>(w[i], lo, hi);
+        const unsigned long long X = pk2(lo, hi);
+        const unsigned long long T = ffma2(X, RCP, MAGIC);
+        const unsigned long long NR = fsub2(MAGIC, T);     // -r
+        const unsigned long long D = ffma2(X, RCP, NR);    // x*rcp - r
+        const unsigned long long U = ffma2(D, D, THR);     // d^2 - 0.49993^2 (< 0: safe)
+        upk2(T, t[2 * i], t[2 * i + 1]);
+        uint32_t u0, u1;
+        upk2(U, u0, u1);
+        sign_and &= u0 & u1;
+    }
+    const uint4 q = make_uint4(pack4_low_bytes(t[0], t[1], t[2], t[3]), pack4_low_bytes(t[4], t[5], t[6], t[7]),
+                               pack4_low_bytes(t[8], t[9], t[10], t[11]),
+                               pack4_low_bytes(t[12], t[13], t[14], t[15]));
+    if (dbg != 2 && (!(sign_and >> 31) || !(rcp < INFINITY))) return fix16(q, r0, r1, scale, rcp, BF16);
+    return q;
+}
+
+// Largest |x| bit pattern of 16 packed 16-bit floats as f32 bits (non-negative floats
+// order like their bits; NaN stays NaN): sign-masked 16-bit magnitudes, packed max.
+template <bool BF16>
+__device__ __forceinline__ uint32_t absmax16_bits(uint4 r0, uint4 r1) {
+    uint32_t m2 = __vmaxu2(__vmaxu2(r0.x & 0x7FFF7FFFu, r0.y & 0x7FFF7FFFu),
+                           __vmaxu2(r0.z & 0x7FFF7FFFu, r0.w & 0x7FFF7FFFu));
+    m2 = __vmaxu2(m2, __vmaxu2(__vmaxu2(r1.x & 0x7FFF7FFFu, r1.y & 0x7FFF7FFFu),
+                               __vmaxu2(r1.z & 0x7FFF7FFFu, r1.w & 0x7FFF7FFFu)));
+    const uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+    return BF16 ? (m << 16) : __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(m))));
+}
+
+// Row tail (k0 + 16 > K): element loads, zero past K.  Out of line: it runs for at most
+// one chunk per token row and would otherwise be inlined into every unrolled chunk.
+__device__ __noinline__ uint4x2 load16_tail(const unsigned short* row, int k0, int K) {
+    uint32_t h[8];
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t lo = k0 + 2 * i < K ? row[k0 + 2 * i] : 0u;
+        const uint32_t hi = k0 + 2 * i + 1 < K ? row[k0 + 2 * i + 1] : 0u;
+        h[i] = lo | (hi << 16);
+    }
+    return {make_uint4(h[0], h[1], h[2], h[3]), make_uint4(h[4], h[5], h[6], h[7])};
+}
+
+__device__ __forceinline__ void load16_raw(const unsigned short* row, int k0, int K, bool cg, uint4& r0,
+                                           uint4& r1) {
+    if (k0 + 16 <= K) {
+        const uint4* src = reinterpret_cast<const uint4*>(row + k0);
+        if (cg) {  // x written earlier in this launch by other CTAs: coherent L2 loads
+            r0 = __ldcg(src);
+            r1 = __ldcg(src + 1);
+        } else {
+            r0 = __ldg(src);
+            r1 = __ldg(src + 1);
+        }
+    } else {
+        const uint4x2 v = load16_tail(row, k0, K);
+        r0 = v.a;
+        r1 = v.b;
+    }
+}
+
+// Shared-memory carve-up of one CTA.
+struct Smem {
+    uint8_t* ring;
+    uint8_t* resb;
+    float* swr;          // [4]: the epilogue's "this CTA finalises the tile" broadcast
+    uint32_t* peer_max;  // [kMaxSplit][BN] partial maxima pushed by the cluster peers
+    uint32_t* tmax;      // [BN] this CTA's partial maxima
+    float* tscale;       // [BN]
+    float* trcp;         // [BN]
+    uint64_t *w_full, *w_empty, *b_full, *a_full, *a_empty, *d_full, *d_empty, *b_ready, *max_full;
+    uint32_t* tmem_slot;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* smem) {
+    Smem m;
+    m.ring = smem;
+    m.resb = m.ring + kStages * kStageBytes;
+    m.swr = reinterpret_cast<float*>(m.resb + kResBBytes);
+    m.peer_max = reinterpret_cast<uint32_t*>(m.swr + 4);
+    m.tmax = m.peer_max + kMaxSplit * kBN;
+    m.tscale = reinterpret_cast<float*>(m.tmax + kBN);
+    m.trcp = m.tscale + kBN;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(m.trcp + kBN);
+    m.w_full = bars;
+    m.w_empty = m.w_full + kStages;
+    m.b_full = m.w_empty + kStages;
+    m.a_full = m.b_full + kStages;
+    m.a_empty = m.a_full + kAStages;
+    m.d_full = m.a_empty + kAStages;
+    m.d_empty = m.d_full + kDBufs;
+    m.b_ready = m.d_empty + kDBufs;
+    m.max_full = m.b_ready + 1;
+    m.tmem_slot = reinterpret_cast<uint32_t*>(m.max_full + 1);
+    return m;
+}
+
+// Geometry of linear l for this CTA: k-slice, tiles, pipeline units.
+struct LGeo {
+    int kb_lo, kb_hi, nkb, upt, ntiles, units, vcl, C;
+    __device__ __forceinline__ int tile(int i) const { return vcl + i * C; }
+    __device__ __forceinline__ int unit_kb(int k) const { return kb_lo + kUnitBlocks * (k % upt); }
+    __device__ __forceinline__ int unit_nb(int k) const { return min(kUnitBlocks, kb_hi - unit_kb(k)); }
+};
+__device__ __forceinline__ LGeo lgeo(const PParams& p, int l, int crank, int cl) {
+    const LinDesc& d = p.lin[l];
+    LGeo g;
+    g.kb_lo = crank * d.kblocks / p.S;
+    g.kb_hi = (crank + 1) * d.kblocks / p.S;
+    g.nkb = g.kb_hi - g.kb_lo;
+    g.upt = (g.nkb + kUnitBlocks - 1) / kUnitBlocks;
+    g.C = p.C;
+    g.vcl = (cl + d.rot) % p.C;
+    g.ntiles = g.vcl < d.n_tiles ? (d.n_tiles - 1 - g.vcl) / p.C + 1 : 0;
+    g.units = g.ntiles * g.upt;
+    return g;
+}
+
+// Converter warp q of one group widens global unit u (nb k-blocks): smem packed INT4 ->
+// int8 lanes (value*16) -> TMEM A stage.  The ring stage is handed back once read.
+__device__ __forceinline__ void convert_unit(const Smem& m, uint32_t tmem, int q, int lane, int u, int nb,
+                                             unsigned long long* utr) {
+    const int r = 32 * q + lane;
+    const int s = u % kStages;
+    const int as = u % kAStages;
+    mbar_wait(&m.w_full[s], (u / kStages) & 1);
+    if (utr && u < 64 && r == 0) utr[8 * u] = clock64();
+    const uint32_t src = smem_u32(m.ring) + s * kStageBytes + r * 16;
+    uint32_t lanes8[kUnitBlocks][32];
+#pragma unroll
+    for (int b = 0; b < kUnitBlocks; ++b) {
+        if (b < nb) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 v = lds128(src + b * kWBlockBytes + c * 2048);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    lanes8[b][c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k 8jj+0..3
+                    lanes8[b][c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k 8jj+4..7
+                }
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&m.w_empty[s]);
+    mbar_wait(&m.a_empty[as], ((u / kAStages) & 1) ^ 1);
+    tc_fence_after();
+    const uint32_t dst = tmem + (static_cast<uint32_t>(32 * q) << 16) + kAColBase + as * kAStageCols;
+    tmem_st_32x32b_x32(dst, lanes8[0]);
+    if (nb > 1) tmem_st_32x32b_x32(dst + 32, lanes8[1]);
+    tmem_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&m.a_full[as]);
+    if (utr && u < 64 && r == 0) utr[8 * u + 1] = clock64();
+}
+
+// K1 of linear l over this CTA's k-slice, by the kQThreads threads of warps 2..11:
+// (wait for the producing linear if any) load x[:, slice] (all loads in flight at once,
+// held packed in registers), per-token partial max|x| (warp-reduced per token, one
+// shared atomic per token and warp), all-to-all of the partial maxima over the cluster
+// (DSMEM st.async completing on the peers' max_full), S = max/127 (ref
+// quantize.cpp:22-35), codes into the resident, MMA-ready B (SWIZZLE_128B K-major), then
+// b_ready.  The MMAs of linear l-1 are complete when it writes B: the epilogue warps,
+// which join the first barrier, have drained all of its accumulators.
+template <bool BF16>
+__device__ __forceinline__ void quantize_slice(const PParams& p, const Smem& m, int l, int qi, const LGeo& g,
+                                               int crank, int qt, unsigned long long* trc) {
+    const LinDesc& d = p.lin[l];
+    const int lane = qt & 31;
+    if (d.dep >= 0) {  // x_l is linear dep's output: wait for its grid-wide completion
+        if (qt == 0) {
+            while (ld_acquire_u32(p.ctr + d.dep) < gridDim.x) __nanosleep(64);
+        }
+        named_bar_sync(2, kQThreads);
+    }
+    if (trc && qt == 0 && l < 6) trc[8 + 4 * l] = globaltimer();
+    const bool cg = d.dep >= 0;
+    const unsigned short* x = static_cast<const unsigned short*>(d.x);
+    const int nch = g.nkb * (kBlockK / 16);  // 16-element chunks per token row
+    if (qt < kBN) m.tmax[qt] = 0u;
+    // Chunk j of this thread is c = qt + j * kQThreads -> (token t = c / nch, 16-element
+    // chunk k = c % nch); t >= M: none.  Chunks are processed in batches of kQHold held
+    // packed in registers: the max pass walks every batch, the quantize pass keeps the
+    // last batch and reloads the others (large k-slices only; L2 hits).
+    const int nbatch = max(1, (d.M * nch - qt + kQThreads * kQHold - 1) / (kQThreads * kQHold));
+    const int dt = nch > 0 ? kQThreads / nch : 0, dk = kQThreads - dt * nch;
+    const unsigned short* xs = x + g.kb_lo * kBlockK;
+    const int kx = d.K - g.kb_lo * kBlockK;
+    uint4 raw[kQHold][2];
+    auto batch_start = [&](int b, int& t, int& k) {
+        const int c = qt + b * kQHold * kQThreads;
+        t = nch > 0 ? c / nch : d.M;
+        k = nch > 0 ? c - t * nch : 0;
+    };
+    auto load_batch = [&](int b) {
+        int t, k;
+        batch_start(b, t, k);
+#pragma unroll
+        for (int i = 0; i < kQHold; ++i) {
+            if (t < d.M) load16_raw(xs + static_cast<size_t>(t) * d.ldx, k * 16, kx, cg, raw[i][0], raw[i][1]);
+            t += dt;
+            k += dk;
+            if (k >= nch) {
+                k -= nch;
+                ++t;
+            }
+        }
+    };
+    const uint32_t tmax_s = smem_u32(m.tmax);
+    for (int b = 0; b < nbatch; ++b) {
+        load_batch(b);
+        if (b == 0) named_bar_sync(2, kQThreads);  // tmax zeroed; linear l-1's MMAs all complete
+        int t, k;
+        batch_start(b, t, k);
+#pragma unroll
+        for (int i = 0; i < kQHold; ++i) {
+            const bool live = t < d.M;
+            const int tt = live ? t : -1;
+            const uint32_t v = live ? absmax16_bits<BF16>(raw[i][0], raw[i][1]) : 0u;
+            const uint32_t grp = __match_any_sync(0xffffffffu, tt);
+            const uint32_t mx = __reduce_max_sync(grp, v);
+            if (live && lane == __ffs(grp) - 1) atom_max_shared_u32(tmax_s + t * 4, mx);
+            t += dt;
+            k += dk;
+            if (k >= nch) {
+                k -= nch;
+                ++t;
+            }
+        }
+    }
+    named_bar_sync(2, kQThreads);
+    if (p.S > 1) {  // all-to-all of the partial maxima over the cluster (DSMEM)
+        if (qt < p.S * kBN) {
+            const int dst = qt / kBN, t = qt % kBN;
+            if (dst != crank)
+                st_async_u32(mapa_shared(smem_u32(m.peer_max + crank * kBN + t), dst), lds32(tmax_s + t * 4),
+                             mapa_shared(smem_u32(m.max_full), dst));
+        }
+        mbar_wait_cluster(m.max_full, qi & 1);
+    }
+    if (qt < kBN) {
+        uint32_t mx = lds32(tmax_s + qt * 4);
+        for (int s = 0; s < p.S; ++s)
+            if (s != crank) mx = max(mx, lds32(smem_u32(m.peer_max) + (s * kBN + qt) * 4));
+        float sc = __uint_as_float(mx) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
+        if (!(sc > 0.0f)) sc = kMinScale;
+        m.tscale[qt] = sc;
+        m.trcp[qt] = 1.0f / sc;
+        if (d.sa_out && blockIdx.x == 0 && qt < d.M) d.sa_out[qt] = sc;
+    }
+    // every thread has passed the max_full wait: re-arm it for the next linear's maxima
+    if (p.S > 1 && qt == 0) mbar_expect_tx(m.max_full, (p.S - 1) * kBN * 4);  // next in-kernel linear
+    named_bar_sync(2, kQThreads);
+    const uint32_t rb = smem_u32(m.resb);
+    const uint32_t sc_s = smem_u32(m.tscale), rc_s = smem_u32(m.trcp);
+    for (int b = nbatch - 1; b >= 0; --b) {
+        if (b != nbatch - 1) load_batch(b);  // earlier batches were not kept
+        int t, k;
+        batch_start(b, t, k);
+#pragma unroll
+        for (int i = 0; i < kQHold; ++i) {
+            if (t < d.M) {
+                const float scale = __uint_as_float(lds32(sc_s + t * 4));
+                const float rcp = __uint_as_float(lds32(rc_s + t * 4));
+                const uint4 qv = p.dbg == 1 ? raw[i][0] : quant16<BF16>(raw[i][0], raw[i][1], scale, rcp, p.dbg);
+                sts128(rb + (k >> 3) * kBBlockBytes + t * 128 + ((((k & 7) ^ (t & 7)) & 7) * 16), qv);
+            }
+            t += dt;
+            k += dk;
+            if (k >= nch) {
+                k -= nch;
+                ++t;
+            }
+        }
+    }
+    for (int c = d.M * nch + qt; c < kBN * nch; c += kQThreads) {  // padding tokens: zero codes
+        const int t = c / nch, k = c - t * nch;
+        sts128(rb + (k >> 3) * kBBlockBytes + t * 128 + ((((k & 7) ^ (t & 7)) & 7) * 16), make_uint4(0, 0, 0, 0));
+    }
+    fence_proxy_async_shared();  // generic smem writes -> visible to tcgen05.mma
+    named_bar_sync(2, kQThreads);
+    if (qt == 0) mbar_arrive(m.b_ready);
+    if (trc && qt == 0 && l < 6) trc[9 + 4 * l] = globaltimer();
+}
+
+// Runs linear l's prologue unless its activations arrive pre-quantized; qi counts the
+// in-kernel-quantized linears (their b_ready / max_full phases).
+__device__ __forceinline__ void quantize_slice_any(const PParams& p, const Smem& m, int l, int& qi, const LGeo& g,
+                                                   int crank, int qt, unsigned long long* trc) {
+    if (p.lin[l].qa) return;
+    if (p.lin[l].x_bf16)
+        quantize_slice<true>(p, m, l, qi, g, crank, qt, trc);
+    else
+        quantize_slice<false>(p, m, l, qi, g, crank, qt, trc);
+    ++qi;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_constant__ PParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const Smem m = carve(reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                    ~static_cast<uintptr_t>(1023)));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int S = p.S;
+    const int crank = S > 1 ? static_cast<int>(cluster_rank()) : 0;
+    const int cl = blockIdx.x / S;
+    int total_tiles = 0;  // this cluster's tiles over the whole program (same on every rank)
+    bool any_signal = false;
+    for (int l = 0; l < p.L; ++l) {
+        total_tiles += lgeo(p, l, crank, cl).ntiles;
+        any_signal |= p.lin[l].signal != 0;
+    }
+    unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
+    // CTA 0 only: per-unit clock64 [converter start, converter done, MMA ready, MMA issued]
+    unsigned long long* utr = p.trace && blockIdx.x == 0 ? p.trace + 148 * kTraceCta : nullptr;
+    if (trc && threadIdx.x == 0) trc[0] = globaltimer();
+    if (p.pdl) pdl_launch_dependents();
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&m.w_full[i], 1);
+            mbar_init(&m.w_empty[i], 5);  // the 4 converter warps + the MMA commit (B tiles)
+            mbar_init(&m.b_full[i], 1);
+        }
+        for (int i = 0; i < kAStages; ++i) {
+            mbar_init(&m.a_full[i], 4);
+            mbar_init(&m.a_empty[i], 1);
+        }
+        for (int i = 0; i < kDBufs; ++i) {
+            mbar_init(&m.d_full[i], 1);
+            mbar_init(&m.d_empty[i], 4);
+        }
+        mbar_init(m.b_ready, 1);
+        mbar_init(m.max_full, 1);
+        fence_mbar_init();
+        if (S > 1) mbar_expect_tx(m.max_full, (S - 1) * kBN * 4);  // peers' partial maxima
+    }
+    if (warp == kWarpAlloc) {
+        tmem_alloc(m.tmem_slot, kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (S > 1) cluster_sync();  // every peer's barriers are armed before any DSMEM traffic
+    tc_fence_after();
+    const uint32_t tmem = lds32(smem_u32(m.tmem_slot));
+    if (trc && threadIdx.x == 0) trc[1] = globaltimer();
+
+    if (warp == kWarpProducer) {
+        // Weights and channel scales are constant: the only griddepcontrol.wait on this
+        // path guards the pre-quantized B tiles.
+        if (lane < 2) {
+            const uint64_t pol = l2_policy_evict_first();
+            // L2 prefetch window: units [kStages, U + kStages + pf_units) ahead of the load
+            // position U, walking across the program's linears.
+            int pl = 0, pk = 0, PU = 0;
+            LGeo pg = lgeo(p, 0, crank, cl);
+            auto pf_step = [&](bool issue) -> bool {
+                while (pl < p.L && pk >= pg.units) {
+                    if (++pl < p.L) pg = lgeo(p, pl, crank, cl);
+                    pk = 0;
+                }
+                if (pl >= p.L) return false;
+                if (issue) {
+                    const LinDesc& d = p.lin[pl];
+                    const int nt = pg.tile(pk / pg.upt);
+                    bulk_prefetch_l2(d.wp + (static_cast<size_t>(nt) * d.kblocks + pg.unit_kb(pk)) * kWBlockBytes,
+                                     pg.unit_nb(pk) * kWBlockBytes);
+                }
+                ++pk;
+                ++PU;
+                return true;
+            };
+            // Pre-quantized B tiles come from the previous kernel (the act quant): the
+            // first ring of weight units is issued before griddepcontrol.wait, their B
+            // tiles after it.
+            const uint64_t pol_b = l2_policy_evict_last();
+            auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
+                mbar_expect_tx(&m.b_full[s], nb * kBBlockBytes);
+                for (int b = 0; b < nb; ++b)
+                    bulk_g2s(m.ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
+                             d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &m.b_full[s], pol_b);
+            };
+            bool waited = p.pdl == 0;
+            auto flush_deferred = [&](int upto) {  // B tiles of units [0, upto)
+                int u = 0;
+                for (int l = 0; l < p.L && u < upto; ++l) {
+                    const LinDesc& d = p.lin[l];
+                    const LGeo g = lgeo(p, l, crank, cl);
+                    for (int k = 0; k < g.units && u < upto; ++k, ++u)
+                        if (d.qa) issue_b(d, u % kStages, g.unit_kb(k), g.unit_nb(k));
+                }
+            };
+            // Two lanes issue alternate units of each tile in SIMT lockstep, halving the
+            // producer's per-unit overhead (waits, barrier arrivals, copy issue).
+            int U = 0, J = 0;
+            for (int l = 0; l < p.L; ++l) {
+                const LinDesc& d = p.lin[l];
+                const LGeo g = lgeo(p, l, crank, cl);
+                const uint8_t* wp = d.wp;
+                const size_t kbl = static_cast<size_t>(d.kblocks);
+                const bool pre = d.qa != nullptr;
+                for (int i = 0; i < g.ntiles; ++i, ++J) {
+                    const int nt = g.tile(i);
+                    const uint8_t* wtile = wp + static_cast<size_t>(nt) * kbl * kWBlockBytes;
+                    for (int k0 = 0; k0 < g.upt; k0 += 2) {
+                        if (!waited && U + k0 + 1 >= kStages) {
+                            // the ring's first units are in flight: wait for the act quant,
+                            // then send the B tiles of every unit issued so far
+                            pdl_wait();
+                            waited = true;
+                            if (lane == 0) flush_deferred(U + k0);
+                        }
+                        const int k = k0 + lane;
+                        if (k < g.upt) {
+                            const int Uk = U + k;
+                            const int s = Uk % kStages;
+                            const int kb = g.kb_lo + kUnitBlocks * k;
+                            const int nb = min(kUnitBlocks, g.kb_hi - kb);
+                            if (lane == 0 && p.pf_units > 0)
+                                while (PU < Uk + kStages + p.pf_units && pf_step(PU >= kStages)) {
+                                }
+                            if (utr && Uk < 64) utr[8 * Uk + 4] = clock64();
+                            if (Uk >= kStages) mbar_wait(&m.w_empty[s], ((Uk / kStages) & 1) ^ 1);
+                            if (utr && Uk < 64) utr[8 * Uk + 5] = clock64();
+                            mbar_expect_tx(&m.w_full[s], nb * kWBlockBytes);
+                            bulk_g2s(m.ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
+                                     nb * kWBlockBytes, &m.w_full[s], pol);
+                            if (utr && Uk < 64) utr[8 * Uk + 6] = clock64();
+                            if (pre && waited) issue_b(d, s, kb, nb);
+                            if (utr && Uk < 64) utr[8 * Uk + 7] = clock64();
+                        }
+                        __syncwarp(0x3u);
+                    }
+                    U += g.upt;
+                }
+            }
+            if (!waited) {  // the whole program fit in one ring
+                pdl_wait();
+                if (lane == 0) flush_deferred(U);
+            }
+            if (p.next_bytes > 0 && lane == 0) {
+                // every own load is issued: stream this CTA's share of the next launch's
+                // weights into L2 (evict-normal; that kernel reads them evict-first)
+                const size_t share = (p.next_bytes / gridDim.x + 16383) & ~static_cast<size_t>(16383);
+                const size_t lo = share * blockIdx.x;
+                const size_t hi = min(p.next_bytes, lo + share);
+                for (size_t off = lo; off < hi; off += 16384)
+                    bulk_prefetch_l2(p.next_wp + off, static_cast<uint32_t>(min(static_cast<size_t>(16384), hi - off)));
+            }
+            if (trc && lane == 0) trc[6] = globaltimer();
+        }
+    } else if (warp == kWarpMma) {
+        const uint32_t rb = smem_u32(m.resb);
+        int U = 0, JD = 0, qi = 0;
+        for (int l = 0; l < p.L; ++l) {
+            const LGeo g = lgeo(p, l, crank, cl);
+            const bool pre = p.lin[l].qa != nullptr;  // B tiles ride in the ring stages
+            if (!pre) {
+                mbar_wait(m.b_ready, qi & 1);
+                tc_fence_after();
+                ++qi;
+            }
+            for (int i = 0; i < g.ntiles && g.upt > 0; ++i, ++JD) {
+                const int db = JD % kDBufs;
+                const uint32_t d_tmem = tmem + db * kBN;
+                mbar_wait(&m.d_empty[db], ((JD / kDBufs) & 1) ^ 1);
+                tc_fence_after();
+                for (int k = i * g.upt; k < (i + 1) * g.upt; ++k, ++U) {
+                    const int kb = g.unit_kb(k), nb = g.unit_nb(k);
+                    const int as = U % kAStages;
+                    const int s = U % kStages;
+                    mbar_wait(&m.a_full[as], (U / kAStages) & 1);
+                    if (pre) mbar_wait(&m.b_full[s], (U / kStages) & 1);
+                    tc_fence_after();
+                    if (utr && U < 64 && lane == 0) utr[8 * U + 2] = clock64();
+                    if (trc && lane == 0 && l < 6 && k == 0) trc[10 + 4 * l] = globaltimer();
+                    const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
+                    const uint32_t b0 = pre ? smem_u32(m.ring) + s * kStageBytes + kUnitBytes
+                                            : rb + (kb - g.kb_lo) * kBBlockBytes;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int c = 0; c < 4 * kUnitBlocks; ++c)
+                            if (c < 4 * nb)
+                                mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b0 + (c / 4) * kBBlockBytes + 32 * (c % 4)),
+                                          kIdesc, (kb > g.kb_lo || c > 0) ? 1u : 0u);
+                        mma_commit(&m.a_empty[as]);
+                        mma_commit(&m.w_empty[s]);  // the stage's B tiles are consumed
+                        if (utr && U < 64) utr[8 * U + 3] = clock64();
+                        if (kb + nb == g.kb_hi) mma_commit(&m.d_full[db]);  // tile complete
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // Warps 2..11: every linear starts with its activation prologue (all 10 warps);
+        // then the converters widen the linear's units and warps 8..11 run its epilogue.
+        const bool conv = warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kConvGroups;
+        const bool epi = warp >= kWarpEpi0;
+        const int qt = threadIdx.x - kWarpAlloc * 32;
+        if (p.pdl) pdl_wait();  // the activations may come from the previous kernel
+        if (conv) {
+            const int grp = (warp - kWarpConv0) / 4;
+            const int q = warp & 3;  // TMEM sub-partition: lanes 32q..32q+31
+            int U = 0, qi = 0;
+            for (int l = 0; l < p.L; ++l) {
+                const LGeo g = lgeo(p, l, crank, cl);
+                quantize_slice_any(p, m, l, qi, g, crank, qt, trc);
+                for (int k = 0; k < g.units; ++k, ++U)
+                    if (U % kConvGroups == grp) convert_unit(m, tmem, q, lane, U, g.unit_nb(k), utr);
+            }
+        } else if (!epi) {
+            int qi = 0;
+            for (int l = 0; l < p.L; ++l) quantize_slice_any(p, m, l, qi, lgeo(p, l, crank, cl), crank, qt, trc);
+        } else {
+            const int q = warp & 3;
+            const int r = 32 * q + lane;  // tile row (TMEM lane) of this thread
+            const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
+            uint32_t* flag = reinterpret_cast<uint32_t*>(m.swr);  // "this CTA finalises" broadcast
+            int JD = 0, qi = 0, tbase = 0;
+            for (int l = 0; l < p.L; ++l) {
+                const LinDesc& d = p.lin[l];
+                const LGeo g = lgeo(p, l, crank, cl);
+                quantize_slice_any(p, m, l, qi, g, crank, qt, trc);
+                // ---------------- epilogue.  With S > 1 the S partial tiles meet in L2:
+                // every rank red.adds its int32 partial into the tile's accumulator and
+                // bumps the tile's arrival counter; the LAST rank to arrive finalises the
+                // whole tile (integer addition: exact in any order) and re-zeroes it.  No
+                // rank ever waits for another.
+                float sa[kBN];
+#pragma unroll
+                for (int t = 0; t < kBN; ++t)
+                    sa[t] = !d.qa ? m.tscale[t] : (t < d.M ? __ldg(d.sa + t) : 0.0f);
+                for (int i = 0; i < g.ntiles; ++i) {
+                    const int nt = g.tile(i);
+                    const int n = nt * kTileN + r;
+                    const float sw_n = n < d.N ? __ldg(d.sw + n) : 0.0f;  // in flight during the wait
+                    uint32_t v[kBN];
+                    if (g.upt > 0) {
+                        const int db = JD % kDBufs;
+                        mbar_wait(&m.d_full[db], (JD / kDBufs) & 1);
+                        tc_fence_after();
+                        tmem_ld_32x32b_x16(t_lane + db * kBN, v);
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&m.d_empty[db]);
+                        ++JD;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < kBN; ++t) v[t] = 0u;  // empty k-slice: zero partial
+                    }
+                    bool fin = true;
+                    int32_t* acc = p.acc + (static_cast<size_t>(tbase + nt) * kBN) * kTileN;  // [t][row]
+                    if (S > 1) {
+                        if (g.upt > 0)
+#pragma unroll
+                            for (int t = 0; t < kBN; ++t)
+                                if (t < d.M) red_add_s32(acc + t * kTileN + r, static_cast<int32_t>(v[t]));
+                        named_bar_sync(3, 128);  // this CTA's partial is issued
+                        if (r == 0) {
+                            __threadfence();
+                            const uint32_t prev = atomicAdd(p.tile_cnt + tbase + nt, 1u);
+                            *flag = prev == static_cast<uint32_t>(S - 1) ? 1u : 0u;
+                        }
+                        named_bar_sync(3, 128);
+                        fin = *flag != 0u;
+                        if (fin) {
+                            __threadfence();  // every rank's partial is visible (acquire side)
+#pragma unroll
+                            for (int t = 0; t < kBN; ++t)
+                                if (t < d.M) {
+                                    v[t] = static_cast<uint32_t>(__ldcg(acc + t * kTileN + r));
+                                    __stcg(acc + t * kTileN + r, 0);  // re-zero for the next launch
+                                }
+                            if (r == 0) p.tile_cnt[tbase + nt] = 0u;
+                        }
+                    }
+                    if (fin && n < d.N) {
+#pragma unroll
+                        for (int t = 0; t < kBN; ++t) {
+                            if (t < d.M) {
+                                const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                                const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa[t], sw_n));
+                                const size_t idx = static_cast<size_t>(t) * d.N + n;
+                                if (d.out_dtype == kDtypeF32)
+                                    static_cast<float*>(d.out)[idx] = y;
+                                else if (d.out_dtype == kDtypeF16)
+                                    static_cast<__half*>(d.out)[idx] = __float2half_rn(y);
+                                else
+                                    static_cast<__nv_bfloat16*>(d.out)[idx] = __float2bfloat16_rn(y);
+                            }
+                        }
+                    }
+                }
+                tbase += d.n_tiles;
+                if (d.signal) {
+                    // every output of linear l stored by this CTA -> publish (release, gpu scope)
+                    named_bar_sync(3, 128);
+                    if (r == 0) {
+                        __threadfence();
+                        red_release_add_u32(p.ctr + l, 1u);
+                    }
+                }
+                if (trc && r == 0 && l < 6) trc[11 + 4 * l] = globaltimer();
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
+    if (threadIdx.x == 0) {
+        if (any_signal) {
+            // the last CTA out resets the completion counters for the next launch
+            __threadfence();
+            if (atomicAdd(p.ctr + kMaxLin, 1u) == gridDim.x - 1) {
+                for (int l = 0; l < p.L; ++l) p.ctr[l] = 0u;
+                p.ctr[kMaxLin] = 0u;
+                __threadfence();
+            }
+        }
+        if (trc) {
+            trc[5] = globaltimer();
+            trc[7] = static_cast<unsigned long long>(S) | (static_cast<unsigned long long>(p.C) << 16) |
+                     (static_cast<unsigned long long>(p.L) << 32);
+        }
+    }
+}
+
+cudaError_t ensure_decode_attr() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        err = cudaFuncSetAttribute(w4a8_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    });
+    return err;
+}
+
+// How many clusters of S decode CTAs (one per SM) can be co-resident: clusters must fit
+// inside one GPC, so e.g. S = 7 leaves SMs of every GPC idle.  Cached per S.
+int max_active_clusters(int S) {
+    static int cache[kMaxSplit + 1] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    if (S < 1 || S > kMaxSplit) return 0;
+    if (cache[S] >= 0) return cache[S];
+    int n = 0;
+    if (ensure_decode_attr() == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(S * 64);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = S;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, w4a8_decode_kernel, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+    }
+    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    if (plan_log) std::fprintf(stderr, "[ody] decode: max active clusters of %d = %d\n", S, n);
+    cache[S] = n;
+    return n;
+}
+
+bool lin_ok(const LinearArgs& a) {
+    return a.M >= 1 && a.M <= kBN && a.N >= 1 && a.K >= 1 &&
+           (a.x_dtype == kDtypeF16 || a.x_dtype == kDtypeBF16) &&
+           (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0 &&
+           (reinterpret_cast<uintptr_t>(a.sw) & 15) == 0;
+}
+
+}  // namespace
+
+static size_t program_tiles(const LinearArgs* a, int L) {
+    size_t t = 0;
+    for (int l = 0; l < L; ++l) t += pad_n(a[l].N) / kTileN;
+    return t;
+}
+constexpr size_t kAccOffset = kProgramCounterRegion + kProgramMaxTiles * 4;
+constexpr size_t kZeroRegion = kAccOffset + kProgramMaxTiles * kBN * kTileN * 4;
+// Cluster split S (uniform over the program) and cluster count C: minimise the busiest
+// CTA's k-blocks -- per linear for a dependency chain, over the whole program (tiles
+// rotated across clusters) for independent linears -- plus a small activation-prologue
+// term per linear; subject to the resident-B bound ceil(kb / S) <= kMaxKbPerCta.
+DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms) {
+    DecodePlan best = {};
+    if (L < 1 || L > kMaxLin) return best;
+    bool chain = false;
+    int max_tiles = 0;
+    if (program_tiles(a, L) > kProgramMaxTiles) return best;
+    for (int l = 0; l < L; ++l) {
+        if (!lin_ok(a[l])) return best;
+        chain |= deps && deps[l] >= 0;
+        max_tiles = std::max(max_tiles, static_cast<int>(pad_n(a[l].N) / kTileN));
+    }
+    double best_cost = 0;
+    for (int S = 1; S <= kMaxSplit; ++S) {
+        bool ok = true;
+        for (int l = 0; l < L; ++l)
+            ok &= (static_cast<int>(pad_k(a[l].K) / kBlockK) + S - 1) / S <= kMaxKbPerCta;
+        if (!ok) continue;
+        int C = sms / S;
+        if (C < 1) break;
+        if (sms >= device_sm_count()) C = std::min(C, max_active_clusters(S));  // one wave
+        C = std::min(C, max_tiles);
+        if (C < 1) continue;
+        double cost = 0, total = 0;
+        for (int l = 0; l < L; ++l) {
+            const int kb = static_cast<int>(pad_k(a[l].K) / kBlockK);
+            const int nt = static_cast<int>(pad_n(a[l].N) / kTileN);
+            const int kbpc = (kb + S - 1) / S;
+            const double pro = 0.25 * a[l].M / 16.0 * kbpc;  // activation prologue, per linear
+            if (chain)
+                cost += static_cast<double>((nt + C - 1) / C) * kbpc + pro;
+            else {
+                total += static_cast<double>(nt) * kbpc;
+                cost += pro;
+            }
+        }
+        if (!chain) cost += std::ceil(total / C);
+        if (best.S == 0 || cost < best_cost - 1e-9) {
+            best = {S, C, S * C};
+            best_cost = cost;
+        }
+    }
+    return best;
+}
+
+DecodePlan plan_decode(int M, int N, int K, int sms) {
+    LinearArgs a = {};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.x_dtype = kDtypeF16;
+    static const float dummy_sw[4] = {0, 0, 0, 0};
+    a.sw = dummy_sw;
+    static const uint4 dummy_x = {};
+    a.x = &dummy_x;
+    a.ldx = 8;
+    return plan_program(&a, nullptr, 1, sms);
+}
+
+bool decode_eligible(int M, int N, int K, int x_dtype, int num_sms) {
+    if (x_dtype != kDtypeF16 && x_dtype != kDtypeBF16) return false;
+    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+    return plan_decode(M, N, K, sms).S > 0;
+}
+
+bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms) {
+    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+    return plan_program(a, deps, L, sms).S > 0;
+}
+
+// Scratch: [dependency counters][split-K arrival counters][split-K accumulators] -- a
+// FIXED-size zero region (zeroed once; every launch leaves it zeroed), so scratch
+// shared by programs of different shapes never lands transient data in it --
+// [a8 codes + scales of the external x].
+size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L) {
+    size_t b = kZeroRegion;
+    for (int l = 0; l < L; ++l)
+        if (!deps || deps[l] < 0) b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
+    return b;
+}
+
+cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, void* scratch, size_t scratch_bytes,
+                                bool pdl, const uint8_t* next_wp, size_t next_bytes, cudaStream_t st) {
+    const int sms = a[0].max_ctas > 0 ? a[0].max_ctas : device_sm_count();
+    const DecodePlan pl = plan_program(a, deps, L, sms);
+    if (pl.S == 0) return cudaErrorInvalidValue;
+    if (!scratch || scratch_bytes < program_scratch_bytes(a, deps, L)) return cudaErrorInvalidValue;
+    const cudaError_t e = ensure_decode_attr();
+    if (e != cudaSuccess) return e;
+    PParams p = {};
+    p.L = L;
+    p.S = pl.S;
+    p.C = pl.C;
+    bool chain = false;
+    for (int l = 0; l < L; ++l) chain |= deps && deps[l] >= 0;
+    // External activations are quantized up front by ONE batched K1 launch into the
+    // scratch (a8 layout); the program kernel then streams their B tiles with the weights.
+    if (program_tiles(a, L) > kProgramMaxTiles) return cudaErrorInvalidValue;
+    p.tile_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kProgramCounterRegion);
+    p.acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kAccOffset);
+    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion;
+    int nb = 0;
+    const void* bx[kMaxLin];
+    int bdt[kMaxLin], bm[kMaxLin], bk[kMaxLin];
+    size_t bld[kMaxLin];
+    int8_t* bq[kMaxLin];
+    float* bs[kMaxLin];
+    bool batch_ok = true;
+    int rot = 0;
+    for (int l = 0; l < L; ++l) {
+        LinDesc& d = p.lin[l];
+        d.x = a[l].x;
+        d.ldx = a[l].ldx;
+        d.x_bf16 = a[l].x_dtype == kDtypeBF16 ? 1 : 0;
+        d.wp = a[l].wp;
+        d.sw = a[l].sw;
+        d.out = a[l].out;
+        d.out_dtype = a[l].out_dtype;
+        d.sa_out = a[l].sa_out;
+        d.M = a[l].M;
+        d.N = a[l].N;
+        d.K = a[l].K;
+        d.kblocks = static_cast<int>(pad_k(a[l].K) / kBlockK);
+        d.n_tiles = static_cast<int>(pad_n(a[l].N) / kTileN);
+        d.dep = deps ? deps[l] : -1;
+        if (d.dep >= l) return cudaErrorInvalidValue;  // only earlier linears
+        d.rot = chain ? 0 : rot % pl.C;
+        rot += d.n_tiles;
+        static const char* pq_env = std::getenv("ODY_PROGRAM_PREQUANT");  // diagnostics: 0 = in-kernel K1
+        const bool prequant = !(pq_env && pq_env[0] == '0');
+        if (d.dep < 0 && prequant) {
+            int8_t* q = reinterpret_cast<int8_t*>(cursor);
+            cursor += round_up(a8_bytes(d.M, d.K), 256);
+            float* sa = a[l].sa_out ? a[l].sa_out : reinterpret_cast<float*>(cursor);
+            cursor += round_up(pad_m(d.M) * 4, 256);
+            d.qa = q;
+            d.sa = sa;
+            d.Mp = static_cast<int>(pad_m(d.M));
+            bx[nb] = a[l].x;
+            bdt[nb] = a[l].x_dtype;
+            bld[nb] = a[l].ldx;
+            bm[nb] = d.M;
+            bk[nb] = d.K;
+            bq[nb] = q;
+            bs[nb] = sa;
+            batch_ok &= d.K <= 16384;
+            ++nb;
+        }
+    }
+    uint32_t* counters = static_cast<uint32_t*>(scratch);
+    for (int l = 0; l < L; ++l)
+        if (p.lin[l].dep >= 0) p.lin[p.lin[l].dep].signal = 1;
+    bool prog_pdl = pdl;
+    if (nb > 0) {
+        cudaError_t ea = cudaSuccess;
+        if (batch_ok) {
+            ea = launch_act_quant_batch(nb, bx, bdt, bld, bm, bk, bq, bs, pdl, st);
+        } else {
+            for (int i = 0; i < nb && ea == cudaSuccess; ++i)
+                ea = launch_act_quant(bx[i], bdt[i], bld[i], bm[i], bk[i], bq[i], bs[i], nullptr, nullptr,
+                                      pdl || i > 0, st);
+        }
+        if (ea != cudaSuccess) return ea;
+        prog_pdl = true;  // stream the weights while the act quant runs
+    }
+    p.ctr = counters;
+    p.pdl = prog_pdl ? 1 : 0;
+    p.next_wp = next_wp;
+    p.next_bytes = next_wp ? (next_bytes & ~static_cast<size_t>(15)) : 0;
+    p.trace = a[0].trace;
+    static const char* pf_env = std::getenv("ODY_DECODE_PF");
+    p.pf_units = pf_env ? std::atoi(pf_env) : 0;
+    static const char* dbg_env = std::getenv("ODY_DBG_DECODE");
+    p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
+    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    if (plan_log) {
+        std::fprintf(stderr, "[ody] decode program L=%d: S %d C %d grid %d%s:", L, pl.S, pl.C, pl.grid,
+                     chain ? " (chain)" : "");
+        for (int l = 0; l < L; ++l) std::fprintf(stderr, " %dx%dx%d", a[l].M, a[l].N, a[l].K);
+        std::fprintf(stderr, "\n");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = pl.S;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (prog_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, w4a8_decode_kernel, p);
+}
+
+cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st) {
+    return launch_w4a8_program(&a, nullptr, 1, a.workspace, a.workspace_bytes, a.pdl, a.next_wp, a.next_bytes,
+                               st);
+}
+
+}  // namespace odyb200

@@ -1197,14 +1197,21 @@ static int fused_cluster(const SkPlan& s) {
 // K1 fused into K3+K4 for decode widths (M <= 16): one kernel per linear.  Falls back to
 // act_quant + GEMM (two kernels, codes in the caller's a8 scratch) when not eligible.
 size_t linear_scratch_bytes(int M, int N, int K, int num_sms) {
-    return gemm_workspace_bytes(M, N, K, num_sms) + round_up(a8_bytes(M, K), 256) +
-           round_up(pad_m(M) * sizeof(float), 256);
+    // [GEMM workspace (stream-K counters + slots)][decode-program scratch: counters,
+    // split-K accumulators, a8 codes, scales]; the two-kernel path reuses the a8 part
+    LinearArgs a = {};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    return gemm_workspace_bytes(M, N, K, num_sms) + program_scratch_bytes(&a, nullptr, 1);
 }
 
-static int g_linear_mode = 0;  // 0: act_quant + GEMM; 1: fused when eligible
+static int g_linear_mode = 2;  // see kernels.h
 void set_linear_mode(int mode) { g_linear_mode = mode; }
+int linear_mode() { return g_linear_mode; }
 
 bool linear_is_fused(int M, int N, int K, int num_sms) {
+    if (g_linear_mode == 2) return decode_eligible(M, N, K, kDtypeF16, num_sms);
     if (g_linear_mode != 1) return false;
     const int sms = num_sms > 0 ? num_sms : device_sm_count();
     const SkPlan s = plan_for(M, N, K, sms, true);
@@ -1226,10 +1233,17 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     const bool aligned = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * esz_x) % 16 == 0;
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     const size_t gws = gemm_workspace_bytes(a.M, a.N, a.K, sms);
+    if (g_linear_mode == 2 && aligned && decode_eligible(a.M, a.N, a.K, a.x_dtype, sms)) {
+        LinearArgs d = a;  // the decode kernel's scratch lives past the GEMM workspace
+        d.workspace = ws + gws;
+        d.workspace_bytes = a.workspace_bytes - gws;
+        return launch_w4a8_decode(d, st);
+    }
     if (!(aligned && a.x_dtype != kDtypeF32 && linear_is_fused(a.M, a.N, a.K, sms))) {
-        int8_t* q = reinterpret_cast<int8_t*>(ws + gws);
-        float* sa = a.sa_out ? a.sa_out
-                             : reinterpret_cast<float*>(ws + gws + round_up(a8_bytes(a.M, a.K), 256));
+        const size_t a8_off = linear_scratch_bytes(a.M, a.N, a.K, sms) - round_up(a8_bytes(a.M, a.K), 256) -
+                              round_up(pad_m(a.M) * sizeof(float), 256);
+        int8_t* q = reinterpret_cast<int8_t*>(ws + a8_off);
+        float* sa = a.sa_out ? a.sa_out : reinterpret_cast<float*>(ws + a8_off + round_up(a8_bytes(a.M, a.K), 256));
         cudaError_t e = launch_act_quant(a.x, a.x_dtype, a.ldx, a.M, a.K, q, sa, nullptr, nullptr,
                                          a.pdl, st);
         if (e != cudaSuccess) return e;

@@ -14,7 +14,11 @@ enum : int { kDtypeF32 = 0, kDtypeF16 = 1, kDtypeBF16 = 2 };
 cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K, int8_t* q,
                              float* s, const float* absmax_in, float* absmax_out, bool pdl,
                              cudaStream_t st);
-void set_act_trace(unsigned long long* buf);  // diagnostics: per-CTA entry/exit globaltimer
+void set_act_trace(unsigned long long* buf);
+// K1 over up to 8 activation matrices in one launch (CTA per token row; K <= 16384).
+cudaError_t launch_act_quant_batch(int n, const void* const* x, const int* dtype, const size_t* ldx,
+                                   const int* M, const int* K, int8_t* const* q, float* const* s, bool pdl,
+                                   cudaStream_t st);  // diagnostics: per-CTA entry/exit globaltimer
 cudaError_t launch_row_absmax(const void* x, int dtype, size_t ldx, int M, int K, float* out,
                               cudaStream_t st);
 
@@ -71,12 +75,40 @@ struct LinearArgs {
     int M, N, K;
     int max_ctas;
     bool pdl;
+    const uint8_t* next_wp;  // optional L2 prefetch hint: the next linear's packed weights
+    size_t next_bytes;
     unsigned long long* trace;
 };
 size_t linear_scratch_bytes(int M, int N, int K, int num_sms);
 bool linear_is_fused(int M, int N, int K, int num_sms);
-void set_linear_mode(int mode);  // 0: act_quant + GEMM (default); 1: K1 fused when eligible
+// Linear lowering: 0 act_quant + GEMM; 1 K1 fused into the GEMM prologue (cluster code
+// all-gather); 2 (default) the cluster split-K decode kernel when eligible, else 0.
+void set_linear_mode(int mode);
+int linear_mode();
 cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st);
+
+// Decode-width (M <= 16) linear as one kernel: fused K1 over each CTA's k-slice,
+// cluster split-K, DSMEM reduce-scatter epilogue (decode_kernel.cu).
+struct DecodePlan {
+    int S, C, grid;  // cluster size, clusters, CTAs (S == 0: not eligible)
+};
+DecodePlan plan_decode(int M, int N, int K, int sms);
+bool decode_eligible(int M, int N, int K, int x_dtype, int num_sms);
+cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st);
+// A "linear program": up to 8 decode-width linears in ONE persistent launch (the weight
+// stream never drains between them).  deps[l] (or NULL: all -1) = index of an earlier
+// linear whose output is linear l's x (quantized in-kernel after a grid-wide wait);
+// external activations are quantized by one batched act-quant launch first.  scratch:
+// program_scratch_bytes(), its first kProgramCounterRegion bytes zeroed once (the launch
+// leaves them zeroed).  Of a[]'s launch fields only a[0].max_ctas and a[0].trace are used.
+constexpr int kProgramMaxLinears = 8;
+constexpr size_t kProgramCounterRegion = 256;
+constexpr size_t kProgramMaxTiles = 1024;  // 128-row weight tiles per program (4 MiB of split-K sums)
+DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms);
+bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms);
+size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L);
+cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, void* scratch, size_t scratch_bytes,
+                                bool pdl, const uint8_t* next_wp, size_t next_bytes, cudaStream_t st);
 
 int device_sm_count();
 

@@ -26,8 +26,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-// Blocks until the phase with the given parity has completed.
+// Blocks until the phase with the given parity has completed.  ODY_MBAR_HINT_NS (a
+// compile-time knob) passes a suspend-time hint to try_wait, so a waiting warp sleeps in
+// the barrier unit until the phase completes instead of re-polling it.
+#ifndef ODY_MBAR_HINT_NS
+#define ODY_MBAR_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if ODY_MBAR_HINT_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ODY_MBAR_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -35,6 +49,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ------------------------------------------------------------ bulk copies

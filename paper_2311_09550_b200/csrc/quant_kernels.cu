@@ -21,6 +21,7 @@ namespace odyb200 {
 namespace {
 
 constexpr int kActThreads = 128;
+constexpr int kActBatch = 8;
 
 // K1: per-token INT8 quantization, one CTA of NT threads per token row; every thread
 // keeps its MC 16-element chunks in registers across both passes.  Pass 1: row
@@ -30,22 +31,12 @@ constexpr int kActThreads = 128;
 // max of a K-sharded row); absmax_out (optional) exports it.  With PDL the kernel
 // lets its consumer launch immediately and waits for its producer before touching x.
 template <typename T, int NT, int MC>
-__global__ void __launch_bounds__(NT)
-act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int Mp,
-                 int8_t* __restrict__ q, float* __restrict__ s,
-                 const float* __restrict__ absmax_in, float* __restrict__ absmax_out,
-                 int pdl, unsigned long long* __restrict__ trace) {
-    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8] = globaltimer();
-    if (pdl) {
-        pdl_launch_dependents();  // let the consumer GEMM start streaming its weights now
-        pdl_wait();
-    }
-    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8 + 2] = globaltimer();
-    const int t = blockIdx.x;
-    const T* row = x + static_cast<size_t>(t) * ldx;
-    __shared__ float red[NT / 32];
+__device__ __forceinline__ void act_quant_row(const T* __restrict__ row, int t, int K, int Kp, int Mp,
+                                              int8_t* __restrict__ q, float* __restrict__ s,
+                                              const float* __restrict__ absmax_in,
+                                              float* __restrict__ absmax_out, float* red,
+                                              unsigned long long* __restrict__ trace) {
     const int nchunks = Kp / 16;
-
     float v[MC][16];
     float mx = 0.0f;
 #pragma unroll
@@ -105,9 +96,64 @@ act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int 
             *reinterpret_cast<uint4*>(q + off) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
+}
+
+template <typename T, int NT, int MC>
+__global__ void __launch_bounds__(NT)
+act_quant_kernel(const T* __restrict__ x, size_t ldx, int M, int K, int Kp, int Mp,
+                 int8_t* __restrict__ q, float* __restrict__ s,
+                 const float* __restrict__ absmax_in, float* __restrict__ absmax_out,
+                 int pdl, unsigned long long* __restrict__ trace) {
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8] = globaltimer();
+    if (pdl) {
+        pdl_launch_dependents();  // let the consumer GEMM start streaming its weights now
+        pdl_wait();
+    }
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 8 + 2] = globaltimer();
+    __shared__ float red[NT / 32];
+    const int t = blockIdx.x;
+    act_quant_row<T, NT, MC>(x + static_cast<size_t>(t) * ldx, t, K, Kp, Mp, q, s, absmax_in, absmax_out, red,
+                             trace);
     if (trace) {
         __syncthreads();
         if (threadIdx.x == 0) trace[blockIdx.x * 8 + 1] = globaltimer();
+    }
+}
+
+// K1 for a batch of up to kActBatch activation matrices (the external inputs of a
+// linear program) in ONE launch: CTA b quantizes global row b of the concatenation.
+struct ActBatch {
+    const void* x[kActBatch];
+    size_t ldx[kActBatch];
+    int dtype[kActBatch], M[kActBatch], K[kActBatch];
+    int8_t* q[kActBatch];
+    float* s[kActBatch];
+    int n, pdl;
+};
+
+template <int NT, int MC>
+__global__ void __launch_bounds__(NT) act_quant_batch_kernel(const __grid_constant__ ActBatch b) {
+    if (b.pdl) {
+        pdl_launch_dependents();
+        pdl_wait();
+    }
+    __shared__ float red[NT / 32];
+    int i = 0, t = blockIdx.x;
+    while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
+    const int K = b.K[i], Kp = static_cast<int>(pad_k(K)), Mp = static_cast<int>(pad_m(b.M[i]));
+    switch (b.dtype[i]) {
+        case kDtypeF32:
+            act_quant_row<float, NT, MC>(static_cast<const float*>(b.x[i]) + t * b.ldx[i], t, K, Kp, Mp, b.q[i],
+                                         b.s[i], nullptr, nullptr, red, nullptr);
+            break;
+        case kDtypeF16:
+            act_quant_row<__half, NT, MC>(static_cast<const __half*>(b.x[i]) + t * b.ldx[i], t, K, Kp, Mp, b.q[i],
+                                          b.s[i], nullptr, nullptr, red, nullptr);
+            break;
+        default:
+            act_quant_row<__nv_bfloat16, NT, MC>(static_cast<const __nv_bfloat16*>(b.x[i]) + t * b.ldx[i], t, K,
+                                                 Kp, Mp, b.q[i], b.s[i], nullptr, nullptr, red, nullptr);
+            break;
     }
 }
 
@@ -318,6 +364,45 @@ cudaError_t launch_act_quant_cfg(cudaLaunchConfig_t& cfg, const void* x, int dty
                                       s, absmax_in, absmax_out, p, g_act_trace);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_act_quant_batch(int n, const void* const* x, const int* dtype, const size_t* ldx,
+                                   const int* M, const int* K, int8_t* const* q, float* const* s, bool pdl,
+                                   cudaStream_t st) {
+    if (n < 1 || n > kActBatch) return cudaErrorInvalidValue;
+    ActBatch b = {};
+    int rows = 0, kmax = 0;
+    for (int i = 0; i < n; ++i) {
+        b.x[i] = x[i];
+        b.ldx[i] = ldx[i];
+        b.dtype[i] = dtype[i];
+        b.M[i] = M[i];
+        b.K[i] = K[i];
+        b.q[i] = q[i];
+        b.s[i] = s[i];
+        rows += M[i];
+        kmax = std::max(kmax, K[i]);
+    }
+    b.n = n;
+    b.pdl = pdl ? 1 : 0;
+    const int chunks = static_cast<int>(pad_k(kmax) / 16);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rows);
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (chunks <= 512) {
+        cfg.blockDim = dim3(512);
+        return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<512, 1>, b);
+    }
+    if (chunks <= 1024) {
+        cfg.blockDim = dim3(512);
+        return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<512, 2>, b);
+    }
+    return cudaErrorInvalidValue;  // K > 16384: the per-linear act_quant handles it
 }
 
 cudaError_t launch_act_quant(const void* x, int dtype, size_t ldx, int M, int K, int8_t* q,

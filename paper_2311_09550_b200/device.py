@@ -15,7 +15,8 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import (ODY_DTYPE_BF16, ODY_DTYPE_F16, ODY_DTYPE_F32, OdyError, check, lib)
+from ._lib import (ODY_DTYPE_BF16, ODY_DTYPE_F16, ODY_DTYPE_F32, OdyError, check, lib,
+                   ody_linear_desc)
 
 _DT = {torch.float32: ODY_DTYPE_F32, torch.float16: ODY_DTYPE_F16, torch.bfloat16: ODY_DTYPE_BF16}
 K_MAX = 1 << 17  # ref gemm.cpp:14
@@ -222,12 +223,14 @@ def dequant_epilogue(acc: torch.Tensor, sa: torch.Tensor, sw: torch.Tensor, out_
 def w4a8_linear(x: torch.Tensor, w: W4Weight, out_dtype=torch.float16,
                 out: torch.Tensor | None = None, sa_out: torch.Tensor | None = None,
                 max_ctas: int = 0, pdl: bool = False, stream=None,
-                workspace: torch.Tensor | None = None) -> torch.Tensor:
+                workspace: torch.Tensor | None = None,
+                prefetch_next: "W4Weight | None" = None) -> torch.Tensor:
     """The whole W4A8 linear y = x W^T from unquantized x (K1 + K3 + K4).
 
     Decode widths (m <= 16) run as ONE kernel: the per-token INT8 quantization happens
     inside the GEMM (codes stay in shared memory).  Bit-identical to
-    ``w4a8_gemm(act_quant(x), w)``."""
+    ``w4a8_gemm(act_quant(x), w)``.  ``prefetch_next``: the weights of the linear launched
+    next on this stream, L2-prefetched once this kernel's own loads are issued (a hint)."""
     _require_cuda(x, "x")
     if x.dim() != 2 or x.shape[1] != w.k:
         raise OdyError(1, "gemm_w4a8_fast: inner dims disagree")
@@ -238,11 +241,70 @@ def w4a8_linear(x: torch.Tensor, w: W4Weight, out_dtype=torch.float16,
         out = torch.empty((m, w.n), dtype=out_dtype, device=x.device)
     if workspace is None:
         workspace = Workspace.get_linear(m, w.n, k, x.device)
-    check(lib().ody_dev_w4a8_linear(
+    nxt = prefetch_next.packed if prefetch_next is not None else None
+    check(lib().ody_dev_w4a8_linear_pf(
         x.data_ptr(), _DT[x.dtype], x.stride(0), w.packed.data_ptr(), w.s.data_ptr(), m, w.n, k,
         _DT[out.dtype], out.data_ptr(), sa_out.data_ptr() if sa_out is not None else None,
-        workspace.data_ptr(), workspace.numel(), max_ctas, int(pdl), _stream(stream)))
+        workspace.data_ptr(), workspace.numel(), max_ctas, int(pdl),
+        nxt.data_ptr() if nxt is not None else None, nxt.numel() if nxt is not None else 0,
+        _stream(stream)))
     return out
+
+
+@dataclass
+class LinearCall:
+    """One linear of a program: out = x @ w^T.  ``dep``: index of an earlier linear of
+    the same program whose ``out`` is (or contains) this ``x``, or -1."""
+    x: torch.Tensor
+    w: "W4Weight"
+    out: torch.Tensor
+    dep: int = -1
+    sa_out: torch.Tensor | None = None
+
+
+class Program:
+    """A reusable linear program (ody_dev_w4a8_linear_program): up to 8 W4A8 linears in ONE
+    persistent kernel launch when all are decode-width (m <= 16).  The descriptor array
+    is built once; ``run`` launches it (also inside CUDA-graph capture)."""
+
+    def __init__(self, calls: list, workspace: torch.Tensor | None = None,
+                 prefetch_next: "W4Weight | None" = None, max_ctas: int = 0):
+        if not 1 <= len(calls) <= 8:
+            raise OdyError(1, "a linear program holds 1..8 linears")
+        self.calls = list(calls)
+        descs = (ody_linear_desc * len(calls))()
+        for d, c in zip(descs, self.calls):
+            _require_cuda(c.x, "x")
+            if c.x.dim() != 2 or c.x.shape[1] != c.w.k or c.x.stride(1) != 1:
+                raise OdyError(1, "linear program: x must be [m, k] with unit column stride")
+            m = c.x.shape[0]
+            if tuple(c.out.shape) != (m, c.w.n) or not c.out.is_contiguous():
+                raise OdyError(1, "linear program: out must be a contiguous [m, n] tensor")
+            d.x, d.x_dtype, d.ldx = c.x.data_ptr(), _DT[c.x.dtype], c.x.stride(0)
+            d.w_packed, d.s_w = c.w.packed.data_ptr(), c.w.s.data_ptr()
+            d.m, d.n, d.k = m, c.w.n, c.w.k
+            d.out, d.out_dtype = c.out.data_ptr(), _DT[c.out.dtype]
+            d.s_a_out = c.sa_out.data_ptr() if c.sa_out is not None else None
+            d.dep = c.dep
+        self.descs = descs
+        need = lib().ody_dev_program_workspace_bytes(descs, len(calls))
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.zeros(need, dtype=torch.uint8, device=self.calls[0].x.device)
+        self.workspace = workspace
+        self.prefetch_next = prefetch_next
+        self.max_ctas = max_ctas
+
+    @property
+    def fused(self) -> bool:
+        return bool(lib().ody_dev_program_is_fused(self.descs, len(self.calls)))
+
+    def run(self, pdl: bool = False, stream=None):
+        nxt = self.prefetch_next.packed if self.prefetch_next is not None else None
+        check(lib().ody_dev_w4a8_linear_program(
+            self.descs, len(self.calls), self.workspace.data_ptr(), self.workspace.numel(), self.max_ctas,
+            int(pdl), nxt.data_ptr() if nxt is not None else None, nxt.numel() if nxt is not None else 0,
+            _stream(stream)))
+        return [c.out for c in self.calls]
 
 
 class W4A8Linear:

@@ -297,12 +297,13 @@ def test_error_paths_match_reference():
     assert e.value.status == ODY_EINVAL
 
 
-@pytest.fixture(params=[0, 1], ids=["two_kernel", "fused"])
+@pytest.fixture(params=[0, 1, 2], ids=["two_kernel", "fused_prologue", "decode"])
 def linear_mode(request, dev):
-    """Both lowerings of w4a8_linear: act-quant kernel + GEMM, and K1 fused into the GEMM."""
+    """Every lowering of w4a8_linear: act-quant kernel + GEMM, K1 fused into the GEMM
+    prologue (cluster code all-gather), and the cluster split-K decode kernel (default)."""
     dev.lib().ody_dev_set_linear_mode(request.param)
     yield request.param
-    dev.lib().ody_dev_set_linear_mode(0)
+    dev.lib().ody_dev_set_linear_mode(2)
 
 
 @pytest.mark.parametrize("m", [1, 3, 16, 17, 64])
