@@ -186,9 +186,9 @@ def run_b200(args):
                        torch.empty(m, dtype=torch.float32, device="cuda"), m, k)
              for k in (HIDDEN, INTER)}
     outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
-    ws_buf = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")
+    gemm_ws = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")  # w4a8_gemm
     for _, n, k in LAYERS:
-        ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")
+        ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")  # w4a8_linear
     stream = torch.cuda.Stream()
     launches_per_step = 0
     lib().ody_dev_set_linear_mode(LOWERINGS[args.lowering])
@@ -205,7 +205,8 @@ def run_b200(args):
         nonlocal launches_per_step
         if programs is not None:
             programs[copy_idx].run(pdl=pdl, stream=stream)
-            launches_per_step = 1 if programs[copy_idx].fused else 2 * len(LAYERS)
+            # fused: one batched act-quant launch + one program launch
+            launches_per_step = 2 if programs[copy_idx].fused else 2 * len(LAYERS)
             return
         if world == 1:
             cnt = 0
@@ -285,7 +286,8 @@ def run_b200(args):
     }
 
     if rank == 0 and world == 1:
-        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs)
+        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs,
+                                           gemm_ws)
         result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
         result["e2e"] = e2e_c_abi(args, m)
         if not args.no_cpu:
@@ -318,7 +320,7 @@ def _graph_time(fn, stream, reps, warm=3):
     return s.elapsed_time(e) / reps
 
 
-def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs=None):
+def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs=None, gemm_ws=None):
     """Dominant kernel = the FastGEMM (HBM-bound at decode).  Its average launch
     duration is timed with CUDA events on its own stream over graph replays that
     rotate all weight copies (each launch streams fresh weights from HBM)."""
@@ -336,7 +338,7 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
         def fn(ws=ws, name=name, k=k):
             for w in ws:
                 if not fused:
-                    dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=ws_buf)
+                    dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=gemm_ws)
                 else:
                     dev.w4a8_linear(xs[k], w, out=outs[name], stream=stream, workspace=ws_buf)
 

@@ -568,7 +568,6 @@ void ody_dev_set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(b
 void ody_dev_set_act_trace(void* buf) { set_act_trace(static_cast<unsigned long long*>(buf)); }
 
 namespace {
-constexpr size_t kProgramCtrRegion = kProgramCounterRegion;  // counters, then the scratch
 
 bool program_args(const ody_linear_desc* lin, int count, int max_ctas, std::vector<LinearArgs>* a,
                   std::vector<int>* deps) {
@@ -605,7 +604,8 @@ size_t ody_dev_program_workspace_bytes(const ody_linear_desc* lin, int count) {
     std::vector<LinearArgs> a;
     std::vector<int> deps;
     program_args(lin, count, 0, &a, &deps);
-    return std::max(kProgramCtrRegion + need, program_scratch_bytes(a.data(), deps.data(), count));
+    // the fallback runs each linear on the same buffer (same zero-region layout)
+    return std::max(need, program_scratch_bytes(a.data(), deps.data(), count));
 }
 
 int ody_dev_program_is_fused(const ody_linear_desc* lin, int count) {
@@ -646,10 +646,9 @@ ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, vo
                        "w4a8 linear program launch");
             return;
         }
-        uint8_t* scratch = static_cast<uint8_t*>(workspace) + kProgramCtrRegion;
         for (int l = 0; l < count; ++l) {
-            a[l].workspace = scratch;
-            a[l].workspace_bytes = workspace_bytes - kProgramCtrRegion;
+            a[l].workspace = workspace;
+            a[l].workspace_bytes = workspace_bytes;
             a[l].pdl = pdl != 0;
             cuda_check(launch_w4a8_linear(a[l], st), "w4a8_linear launch");
         }

@@ -106,6 +106,10 @@ struct LinDesc {
     int dep;              // x is the output of linear `dep` of this program (-1: external)
     int signal;           // a later linear depends on this one: publish its completion
     int rot;              // tile rotation (independent linears spread over the clusters)
+    // dynamic schedule (w4a8_decode_dyn_kernel): work items = (tile, k-split) pairs
+    int split;            // k-splits per tile
+    int ibase;            // first work item of this linear
+    int tbase;            // first tile of this linear in the program's tile numbering
 };
 
 struct PParams {
@@ -114,6 +118,9 @@ struct PParams {
     int S, C;             // cluster size (split-K factor), clusters
     uint32_t* ctr;        // [kMaxLin] completion counters + [kMaxLin] exit counter (zeroed)
     int32_t* acc;         // [program tiles][BN][128] split-K accumulators in L2 (zeroed)
+    int32_t* part;        // dynamic schedule: [items][BN][128] split partials (scratch)
+    int n_items;          // dynamic schedule: work items of the whole program
+    uint32_t* work;       // dynamic schedule: next-item counter (zeroed; reset by the last CTA)
     uint32_t* tile_cnt;   // [program tiles] split arrivals (zeroed)
     int pdl;
     int pf_units;         // L2 prefetch window past the smem ring (units)
@@ -877,6 +884,354 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
     }
 }
 
+// ===================================================================== dynamic schedule
+// w4a8_decode_dyn_kernel: the same data path for a program whose activations all arrive
+// pre-quantized, but the work -- (linear, 128-row tile, k-split) items, in program order
+// -- is handed out at run time from one global counter: each CTA's producer grabs the
+// next item whenever its ring has room, so SMs that stream faster simply take more items
+// (measured: the static assignment left some CTAs ~2x behind on every linear).  A
+// split tile's partials meet in L2: each item stores its int32 partial, bumps the tile's
+// arrival counter, and the last item to arrive sums the S partials and runs the
+// epilogue.  No clusters, no DSMEM; the grid is one CTA per SM.
+constexpr int kDynStages = 10;
+constexpr int kItemSlots = 8;
+constexpr int kDynSmem = kDynStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
+static_assert(kDynSmem <= 227 * 1024, "smem budget");
+
+struct DynItem {
+    int l, nt, kb_lo, kb_hi, r;
+};
+__device__ __forceinline__ DynItem dyn_item(const PParams& p, int it) {
+    DynItem x;
+    int l = 0;
+    while (l + 1 < p.L && it >= p.lin[l + 1].ibase) ++l;
+    const LinDesc& d = p.lin[l];
+    const int rel = it - d.ibase;
+    x.l = l;
+    x.nt = rel / d.split;
+    x.r = rel - x.nt * d.split;
+    x.kb_lo = x.r * d.kblocks / d.split;
+    x.kb_hi = (x.r + 1) * d.kblocks / d.split;
+    return x;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kDynStages * kStageBytes);
+    uint64_t* w_full = bars;
+    uint64_t* w_empty = w_full + kDynStages;
+    uint64_t* b_full = w_empty + kDynStages;
+    uint64_t* a_full = b_full + kDynStages;
+    uint64_t* a_empty = a_full + kAStages;
+    uint64_t* d_full = a_empty + kAStages;
+    uint64_t* d_empty = d_full + kDBufs;
+    uint64_t* i_full = d_empty + kDBufs;
+    uint64_t* i_empty = i_full + kItemSlots;
+    int* items = reinterpret_cast<int*>(i_empty + kItemSlots);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(items + kItemSlots);
+    uint32_t* tmem_slot = flag + 1;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
+    if (trc && threadIdx.x == 0) trc[0] = globaltimer();
+    if (p.pdl) pdl_launch_dependents();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kDynStages; ++i) {
+            mbar_init(&w_full[i], 1);
+            mbar_init(&w_empty[i], 5);  // 4 converter warps read W, the MMA consumed B
+            mbar_init(&b_full[i], 1);
+        }
+        for (int i = 0; i < kAStages; ++i) {
+            mbar_init(&a_full[i], 4);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < kDBufs; ++i) {
+            mbar_init(&d_full[i], 1);
+            mbar_init(&d_empty[i], 4);
+        }
+        for (int i = 0; i < kItemSlots; ++i) {
+            mbar_init(&i_full[i], 1);
+            mbar_init(&i_empty[i], 9);  // MMA + 4 converter + 4 epilogue warps
+        }
+        fence_mbar_init();
+    }
+    if (warp == kWarpAlloc) {
+        tmem_alloc(tmem_slot, kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = lds32(smem_u32(tmem_slot));
+    if (trc && threadIdx.x == 0) trc[1] = globaltimer();
+
+    if (warp == kWarpProducer) {
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            const uint64_t pol_b = l2_policy_evict_last();
+            // B tiles come from the act-quant kernel: units issued before griddepcontrol.wait
+            // get their B tiles once it returns (recorded by stage)
+            bool waited = p.pdl == 0;
+            int dq[kDynStages], dkb[kDynStages], dnb[kDynStages], ndef = 0;
+            auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
+                mbar_expect_tx(&b_full[s], nb * kBBlockBytes);
+                for (int b = 0; b < nb; ++b)
+                    bulk_g2s(ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
+                             d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
+            };
+            int U = 0;
+            for (int j = 0;; ++j) {
+                const int is = j % kItemSlots;
+                if (j >= kItemSlots) mbar_wait(&i_empty[is], ((j / kItemSlots) & 1) ^ 1);
+                // item 0 of every CTA is static (blockIdx.x), so the weight stream starts at
+                // once; the shared counter is only touched after griddepcontrol.wait, i.e.
+                // once the previous launch (which re-arms it) has completed
+                int it;
+                if (j == 0) {
+                    it = static_cast<int>(blockIdx.x);
+                } else {
+                    if (!waited) {
+                        pdl_wait();
+                        waited = true;
+                        for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
+                    }
+                    it = static_cast<int>(gridDim.x + atomicAdd(p.work, 1u));
+                }
+                if (it >= p.n_items) it = -1;
+                items[is] = it;
+                mbar_arrive(&i_full[is]);  // release: the item id is visible to the consumers
+                if (it < 0) break;
+                const DynItem x = dyn_item(p, it);
+                const LinDesc& d = p.lin[x.l];
+                const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
+                for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
+                    const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                    const int s = U % kDynStages;
+                    if (!waited && U >= kDynStages) {
+                        pdl_wait();
+                        waited = true;
+                        for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
+                    }
+                    if (U >= kDynStages) mbar_wait(&w_empty[s], ((U / kDynStages) & 1) ^ 1);
+                    mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
+                    bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
+                             nb * kWBlockBytes, &w_full[s], pol);
+                    if (waited) {
+                        issue_b(d, s, kb, nb);
+                    } else {
+                        dq[ndef] = x.l;
+                        dkb[ndef] = kb;
+                        dnb[ndef] = nb;
+                        ++ndef;
+                    }
+                }
+            }
+            if (!waited) {
+                pdl_wait();
+                for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
+            }
+            if (trc) trc[6] = globaltimer();
+        }
+    } else if (warp == kWarpMma) {
+        int U = 0, JD = 0;
+        for (int j = 0;; ++j) {
+            const int is = j % kItemSlots;
+            mbar_wait(&i_full[is], (j / kItemSlots) & 1);
+            const int it = items[is];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&i_empty[is]);
+            if (it < 0) break;
+            const DynItem x = dyn_item(p, it);
+            if (x.kb_hi <= x.kb_lo) continue;
+            const int db = JD % kDBufs;
+            const uint32_t d_tmem = tmem + db * kBN;
+            mbar_wait(&d_empty[db], ((JD / kDBufs) & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
+                const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                const int as = U % kAStages;
+                const int s = U % kDynStages;
+                mbar_wait(&a_full[as], (U / kAStages) & 1);
+                mbar_wait(&b_full[s], (U / kDynStages) & 1);
+                tc_fence_after();
+                const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
+                const uint32_t b0 = smem_u32(ring) + s * kStageBytes + kUnitBytes;
+                if (elect_one()) {
+#pragma unroll
+                    for (int c = 0; c < 4 * kUnitBlocks; ++c)
+                        if (c < 4 * nb)
+                            mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b0 + (c / 4) * kBBlockBytes + 32 * (c % 4)),
+                                      kIdesc, (kb > x.kb_lo || c > 0) ? 1u : 0u);
+                    mma_commit(&a_empty[as]);
+                    mma_commit(&w_empty[s]);
+                    if (kb + nb >= x.kb_hi) mma_commit(&d_full[db]);
+                }
+                __syncwarp();
+            }
+            ++JD;
+        }
+    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        int U = 0;
+        for (int j = 0;; ++j) {
+            const int is = j % kItemSlots;
+            mbar_wait(&i_full[is], (j / kItemSlots) & 1);
+            const int it = items[is];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&i_empty[is]);
+            if (it < 0) break;
+            const DynItem x = dyn_item(p, it);
+            for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
+                const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                const int s = U % kDynStages;
+                const int as = U % kAStages;
+                mbar_wait(&w_full[s], (U / kDynStages) & 1);
+                const uint32_t src = smem_u32(ring) + s * kStageBytes + r * 16;
+                uint32_t lanes8[kUnitBlocks][32];
+#pragma unroll
+                for (int b = 0; b < kUnitBlocks; ++b) {
+                    if (b < nb) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 v = lds128(src + b * kWBlockBytes + c * 2048);
+                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) {
+                                lanes8[b][c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k 8jj+0..3
+                                lanes8[b][c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k 8jj+4..7
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&w_empty[s]);
+                mbar_wait(&a_empty[as], ((U / kAStages) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dst = tmem + (static_cast<uint32_t>(32 * q) << 16) + kAColBase + as * kAStageCols;
+                tmem_st_32x32b_x32(dst, lanes8[0]);
+                if (nb > 1) tmem_st_32x32b_x32(dst + 32, lanes8[1]);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[as]);
+            }
+        }
+    } else if (warp >= kWarpEpi0) {
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
+        int JD = 0, cur_l = -1;
+        float sa[kBN];
+        for (int j = 0;; ++j) {
+            const int is = j % kItemSlots;
+            mbar_wait(&i_full[is], (j / kItemSlots) & 1);
+            const int it = items[is];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&i_empty[is]);
+            if (it < 0) break;
+            const DynItem x = dyn_item(p, it);
+            const LinDesc& d = p.lin[x.l];
+            if (x.l != cur_l) {  // per-token scales of this linear (from the act-quant kernel)
+                if (cur_l < 0 && p.pdl) pdl_wait();
+                cur_l = x.l;
+#pragma unroll
+                for (int t = 0; t < kBN; ++t) sa[t] = t < d.M ? __ldcg(d.sa + t) : 0.0f;
+            }
+            const int n = x.nt * kTileN + r;
+            const float sw_n = n < d.N ? __ldg(d.sw + n) : 0.0f;  // in flight during the wait
+            uint32_t v[kBN];
+            if (x.kb_hi > x.kb_lo) {
+                const int db = JD % kDBufs;
+                mbar_wait(&d_full[db], (JD / kDBufs) & 1);
+                tc_fence_after();
+                tmem_ld_32x32b_x16(t_lane + db * kBN, v);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&d_empty[db]);
+                ++JD;
+            } else {
+#pragma unroll
+                for (int t = 0; t < kBN; ++t) v[t] = 0u;
+            }
+            bool fin = true;
+            if (d.split > 1) {
+                // Splits r < S-1 publish their partial and a release-increment (no round
+                // trip); split S-1 -- handed out last of its tile, so its peers are already
+                // in flight -- waits for the count, sums the partials and stores the tile.
+                uint32_t* cnt = p.tile_cnt + d.tbase + x.nt;
+                if (x.r < d.split - 1) {
+                    fin = false;
+                    int32_t* part = p.part + static_cast<size_t>(it) * kBN * kTileN;  // [t][row]
+#pragma unroll
+                    for (int t = 0; t < kBN; ++t)
+                        if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
+                    named_bar_sync(3, 128);  // this item's partial is written
+                    if (r == 0) {
+                        __threadfence();
+                        red_release_add_u32(cnt, 1u);
+                    }
+                } else {
+                    if (r == 0) {
+                        while (ld_acquire_u32(cnt) < static_cast<uint32_t>(d.split - 1)) __nanosleep(32);
+                        *cnt = 0u;  // re-armed for the next launch
+                    }
+                    named_bar_sync(3, 128);
+                    __threadfence();
+                    const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * kBN * kTileN;
+                    for (int s2 = 0; s2 < d.split - 1; ++s2)
+#pragma unroll
+                        for (int t = 0; t < kBN; ++t)
+                            if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * kBN + t) * kTileN + r));
+                }
+            }
+            if (fin && n < d.N) {
+#pragma unroll
+                for (int t = 0; t < kBN; ++t) {
+                    if (t < d.M) {
+                        const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                        const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa[t], sw_n));
+                        const size_t idx = static_cast<size_t>(t) * d.N + n;
+                        if (d.out_dtype == kDtypeF32)
+                            static_cast<float*>(d.out)[idx] = y;
+                        else if (d.out_dtype == kDtypeF16)
+                            static_cast<__half*>(d.out)[idx] = __float2half_rn(y);
+                        else
+                            static_cast<__nv_bfloat16*>(d.out)[idx] = __float2bfloat16_rn(y);
+                    }
+                }
+            }
+        }
+        if (trc && r == 0) trc[4] = globaltimer();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
+    if (threadIdx.x == 0) {
+        // the last CTA out re-arms the item counter for the next launch
+        __threadfence();
+        if (atomicAdd(p.ctr + kMaxLin, 1u) == gridDim.x - 1) {
+            *p.work = 0u;
+            p.ctr[kMaxLin] = 0u;
+            __threadfence();
+        }
+        if (trc) trc[5] = globaltimer();
+    }
+}
+
+cudaError_t ensure_dyn_attr() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    });
+    return err;
+}
+
 cudaError_t ensure_decode_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
@@ -931,7 +1286,11 @@ static size_t program_tiles(const LinearArgs* a, int L) {
     return t;
 }
 constexpr size_t kAccOffset = kProgramCounterRegion + kProgramMaxTiles * 4;
-constexpr size_t kZeroRegion = kAccOffset + kProgramMaxTiles * kBN * kTileN * 4;
+// the last 4 KiB of the zero region are the two-kernel GEMM's stream-K counters when the
+// same scratch serves ody_dev_w4a8_linear's fallback (kLinearGemmCounters)
+constexpr size_t kZeroRegion = kAccOffset + kProgramMaxTiles * kBN * kTileN * 4 + kLinearGemmCounters;
+size_t program_zero_bytes() { return kZeroRegion; }
+
 // Cluster split S (uniform over the program) and cluster count C: minimise the busiest
 // CTA's k-blocks -- per linear for a dependency chain, over the whole program (tiles
 // rotated across clusters) for independent linears -- plus a small activation-prologue
@@ -980,6 +1339,22 @@ DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms) {
     return best;
 }
 
+// Dynamic schedule: k-splits per tile so a work item streams <= 48 k-blocks (384 KiB).
+static int dyn_split(int kblocks) {
+    static const char* env = std::getenv("ODY_DYN_KB");  // diagnostics: target k-blocks per item
+    // measured (tools/program_trace.py, LLaMA-13B layer): whole 40-block tiles for
+    // K = 5120 and 3 splits of 36 blocks for K = 13824 beat finer splits, whose L2 partial
+    // round trips make the epilogue the bottleneck
+    static const int target = env ? std::max(1, std::atoi(env)) : 48;
+    return std::max(1, (kblocks + target - 1) / target);
+}
+static size_t dyn_items(const LinearArgs* a, int L) {
+    size_t n = 0;
+    for (int l = 0; l < L; ++l)
+        n += (pad_n(a[l].N) / kTileN) * dyn_split(static_cast<int>(pad_k(a[l].K) / kBlockK));
+    return n;
+}
+
 DecodePlan plan_decode(int M, int N, int K, int sms) {
     LinearArgs a = {};
     a.M = M;
@@ -1010,7 +1385,7 @@ bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms) 
 // shared by programs of different shapes never lands transient data in it --
 // [a8 codes + scales of the external x].
 size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L) {
-    size_t b = kZeroRegion;
+    size_t b = kZeroRegion + dyn_items(a, L) * kBN * kTileN * 4;  // + split partials
     for (int l = 0; l < L; ++l)
         if (!deps || deps[l] < 0) b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
     return b;
@@ -1035,7 +1410,8 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     if (program_tiles(a, L) > kProgramMaxTiles) return cudaErrorInvalidValue;
     p.tile_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kProgramCounterRegion);
     p.acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kAccOffset);
-    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion;
+    p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
+    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion + dyn_items(a, L) * kBN * kTileN * 4;
     int nb = 0;
     const void* bx[kMaxLin];
     int bdt[kMaxLin], bm[kMaxLin], bk[kMaxLin];
@@ -1115,6 +1491,37 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
                      chain ? " (chain)" : "");
         for (int l = 0; l < L; ++l) std::fprintf(stderr, " %dx%dx%d", a[l].M, a[l].N, a[l].K);
         std::fprintf(stderr, "\n");
+    }
+    static const char* dyn_env = std::getenv("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
+    const bool dyn = !chain && nb == L && !(dyn_env && dyn_env[0] == '0');
+    if (dyn) {
+        const cudaError_t ed = ensure_dyn_attr();
+        if (ed != cudaSuccess) return ed;
+        int ib = 0, tb = 0;
+        for (int l = 0; l < L; ++l) {
+            LinDesc& d = p.lin[l];
+            d.split = dyn_split(d.kblocks);
+            d.ibase = ib;
+            d.tbase = tb;
+            ib += d.n_tiles * d.split;
+            tb += d.n_tiles;
+        }
+        p.n_items = ib;
+        p.work = counters + kMaxLin + 1;
+        p.S = 1;
+        p.C = std::min(sms, ib);
+        if (plan_log) std::fprintf(stderr, "[ody] dynamic schedule: %d items over %d CTAs\n", ib, p.C);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.C);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kDynSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr.val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = prog_pdl ? 1 : 0;
+        return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel, p);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.grid);

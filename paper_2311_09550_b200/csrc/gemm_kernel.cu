@@ -1197,13 +1197,18 @@ static int fused_cluster(const SkPlan& s) {
 // K1 fused into K3+K4 for decode widths (M <= 16): one kernel per linear.  Falls back to
 // act_quant + GEMM (two kernels, codes in the caller's a8 scratch) when not eligible.
 size_t linear_scratch_bytes(int M, int N, int K, int num_sms) {
-    // [GEMM workspace (stream-K counters + slots)][decode-program scratch: counters,
-    // split-K accumulators, a8 codes, scales]; the two-kernel path reuses the a8 part
+    // One buffer serves both lowerings, with every zero-invariant region at a fixed,
+    // shape-independent offset: [decode-program zero region, whose last 4 KiB are the
+    // GEMM's stream-K counters][transient: GEMM slots / program partials + a8 ...]; the
+    // two-kernel path's a8 codes + scales sit at the very end.
+    static_assert(kLinearGemmCounters == kCounterBytes, "GEMM counter region");
     LinearArgs a = {};
     a.M = M;
     a.N = N;
     a.K = K;
-    return gemm_workspace_bytes(M, N, K, num_sms) + program_scratch_bytes(&a, nullptr, 1);
+    const size_t gemm_path = program_zero_bytes() - kCounterBytes + gemm_workspace_bytes(M, N, K, num_sms) +
+                             round_up(a8_bytes(M, K), 256) + round_up(pad_m(M) * sizeof(float), 256);
+    return std::max(gemm_path, program_scratch_bytes(&a, nullptr, 1));
 }
 
 static int g_linear_mode = 2;  // see kernels.h
@@ -1233,12 +1238,9 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     const bool aligned = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * esz_x) % 16 == 0;
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     const size_t gws = gemm_workspace_bytes(a.M, a.N, a.K, sms);
-    if (g_linear_mode == 2 && aligned && decode_eligible(a.M, a.N, a.K, a.x_dtype, sms)) {
-        LinearArgs d = a;  // the decode kernel's scratch lives past the GEMM workspace
-        d.workspace = ws + gws;
-        d.workspace_bytes = a.workspace_bytes - gws;
-        return launch_w4a8_decode(d, st);
-    }
+    if (g_linear_mode == 2 && aligned && decode_eligible(a.M, a.N, a.K, a.x_dtype, sms))
+        return launch_w4a8_decode(a, st);  // the whole buffer is its program scratch
+    uint8_t* gemm_ws = ws + program_zero_bytes() - kCounterBytes;
     if (!(aligned && a.x_dtype != kDtypeF32 && linear_is_fused(a.M, a.N, a.K, sms))) {
         const size_t a8_off = linear_scratch_bytes(a.M, a.N, a.K, sms) - round_up(a8_bytes(a.M, a.K), 256) -
                               round_up(pad_m(a.M) * sizeof(float), 256);
@@ -1254,7 +1256,7 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
         g.sw = a.sw;
         g.out = a.out;
         g.out_dtype = a.out_dtype;
-        g.workspace = ws;
+        g.workspace = gemm_ws;
         g.workspace_bytes = gws;
         g.M = a.M;
         g.N = a.N;
@@ -1296,8 +1298,8 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     p.x_dtype = a.x_dtype;
     p.ldx = a.ldx;
     p.sa_out = a.sa_out;
-    p.ws_cnt = static_cast<uint32_t*>(a.workspace);
-    p.ws_slots = reinterpret_cast<int32_t*>(ws + kCounterBytes);
+    p.ws_cnt = reinterpret_cast<uint32_t*>(gemm_ws);
+    p.ws_slots = reinterpret_cast<int32_t*>(gemm_ws + kCounterBytes);
     p.pdl = a.pdl ? 1 : 0;
     static const char* dbg_env = std::getenv("ODY_DBG_FUSE");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;

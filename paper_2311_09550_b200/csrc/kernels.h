@@ -103,7 +103,11 @@ cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st);
 // leaves them zeroed).  Of a[]'s launch fields only a[0].max_ctas and a[0].trace are used.
 constexpr int kProgramMaxLinears = 8;
 constexpr size_t kProgramCounterRegion = 256;
-constexpr size_t kProgramMaxTiles = 1024;  // 128-row weight tiles per program (4 MiB of split-K sums)
+constexpr size_t kProgramMaxTiles = 1024;  // 128-row weight tiles per program (8 MiB of split-K sums)
+constexpr size_t kLinearGemmCounters = 4096;  // == the GEMM workspace's counter region
+// Bytes at the start of a program scratch that must stay zero (counters, accumulators);
+// shape-independent, so one scratch buffer can serve programs/linears of any shape.
+size_t program_zero_bytes();
 DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms);
 bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms);
 size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L);

@@ -155,18 +155,19 @@ class Workspace:
             ws = cls.get(m, n, k, device)
         return ws
 
-    @classmethod
-    def get_linear(cls, m: int, n: int, k: int, device) -> torch.Tensor:
-        """Workspace for w4a8_linear (stream-K state + fallback a8 scratch)."""
-        return cls._sized(lib().ody_dev_linear_workspace_bytes(m, n, k), device)
+    _per_device_linear: dict = {}
 
     @classmethod
-    def _sized(cls, need: int, device) -> torch.Tensor:
+    def get_linear(cls, m: int, n: int, k: int, device) -> torch.Tensor:
+        """Workspace for w4a8_linear (decode-program counters and split-K sums, GEMM
+        stream-K state, a8 scratch).  A separate buffer from ``get``'s: the two layouts
+        keep different regions zero."""
         dev = torch.device(device)
-        ws = cls._per_device.get(dev)
+        need = lib().ody_dev_linear_workspace_bytes(m, n, k)
+        ws = cls._per_device_linear.get(dev)
         if ws is None or ws.numel() < need:
             ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
-            cls._per_device[dev] = ws
+            cls._per_device_linear[dev] = ws
         return ws
 
     @classmethod

@@ -61,6 +61,12 @@ def main():
         print(f"  {nm:14s} {stat(col)}")
     for i, (name, _, _) in enumerate(sel):
         print(f"  {name:8s} first MMA {stat(10 + 4 * i)}   epilogue done {stat(11 + 4 * i)}")
+    full = buf[:148 * 32].view(148, 32).cpu().numpy()
+    ex = [(b, (full[b, 5] - base) / 1e3) for b in range(148) if full[b, 0] > 0]
+    ex.sort(key=lambda z: -z[1])
+    print("slowest CTAs (block, exit us, per-linear epilogue done):",
+          [(b, round(e, 1), [round((full[b, 11 + 4 * i] - base) / 1e3, 1) for i in range(len(sel))]) for b, e in ex[:12]])
+    print("fastest CTAs:", [(b, round(e, 1)) for b, e in ex[-6:]])
     ub = ut[ut > 0].min() if (ut > 0).any() else 0
     print("CTA 0 units (cycles): conv start, conv done, MMA ready, MMA issued, prod at unit, prod slot free, W issued, B issued")
     for u in range(64):
