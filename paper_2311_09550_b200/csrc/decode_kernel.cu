@@ -968,18 +968,25 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
     if (trc && threadIdx.x == 0) trc[1] = globaltimer();
 
     if (warp == kWarpProducer) {
-        if (lane == 0) {
+        // Lanes 0 and 1 issue alternate units of each item in SIMT lockstep (halves the
+        // per-unit producer overhead); lane 0 fetches the items.
+        if (lane < 2) {
             const uint64_t pol = l2_policy_evict_first();
             const uint64_t pol_b = l2_policy_evict_last();
             // B tiles come from the act-quant kernel: units issued before griddepcontrol.wait
-            // get their B tiles once it returns (recorded by stage)
+            // get their B tiles once it returns (each lane records its own)
             bool waited = p.pdl == 0;
-            int dq[kDynStages], dkb[kDynStages], dnb[kDynStages], ndef = 0;
+            int dq[kDynStages], dst[kDynStages], dkb[kDynStages], dnb[kDynStages], ndef = 0;
             auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
                 mbar_expect_tx(&b_full[s], nb * kBBlockBytes);
                 for (int b = 0; b < nb; ++b)
                     bulk_g2s(ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
                              d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
+            };
+            auto release_deferred = [&]() {
+                pdl_wait();
+                waited = true;
+                for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], dst[i], dkb[i], dnb[i]);
             };
             int U = 0;
             for (int j = 0;; ++j) {
@@ -988,51 +995,50 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
                 // item 0 of every CTA is static (blockIdx.x), so the weight stream starts at
                 // once; the shared counter is only touched after griddepcontrol.wait, i.e.
                 // once the previous launch (which re-arms it) has completed
-                int it;
-                if (j == 0) {
-                    it = static_cast<int>(blockIdx.x);
-                } else {
-                    if (!waited) {
-                        pdl_wait();
-                        waited = true;
-                        for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
-                    }
-                    it = static_cast<int>(gridDim.x + atomicAdd(p.work, 1u));
+                int it = static_cast<int>(blockIdx.x);
+                if (j > 0) {
+                    if (!waited) release_deferred();
+                    if (lane == 0) it = static_cast<int>(gridDim.x + atomicAdd(p.work, 1u));
+                    it = __shfl_sync(0x3u, it, 0);
                 }
                 if (it >= p.n_items) it = -1;
-                items[is] = it;
-                mbar_arrive(&i_full[is]);  // release: the item id is visible to the consumers
+                if (lane == 0) {
+                    items[is] = it;
+                    mbar_arrive(&i_full[is]);  // release: the item id is visible to the consumers
+                }
                 if (it < 0) break;
                 const DynItem x = dyn_item(p, it);
                 const LinDesc& d = p.lin[x.l];
                 const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
-                for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
-                    const int nb = min(kUnitBlocks, x.kb_hi - kb);
-                    const int s = U % kDynStages;
-                    if (!waited && U >= kDynStages) {
-                        pdl_wait();
-                        waited = true;
-                        for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
+                const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
+                for (int k0 = 0; k0 < nunits; k0 += 2) {
+                    if (!waited && U + k0 + 1 >= kDynStages) release_deferred();
+                    const int k = k0 + lane;
+                    if (k < nunits) {
+                        const int Uk = U + k;
+                        const int s = Uk % kDynStages;
+                        const int kb = x.kb_lo + kUnitBlocks * k;
+                        const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                        if (Uk >= kDynStages) mbar_wait(&w_empty[s], ((Uk / kDynStages) & 1) ^ 1);
+                        mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
+                        bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
+                                 nb * kWBlockBytes, &w_full[s], pol);
+                        if (waited) {
+                            issue_b(d, s, kb, nb);
+                        } else {
+                            dq[ndef] = x.l;
+                            dst[ndef] = s;
+                            dkb[ndef] = kb;
+                            dnb[ndef] = nb;
+                            ++ndef;
+                        }
                     }
-                    if (U >= kDynStages) mbar_wait(&w_empty[s], ((U / kDynStages) & 1) ^ 1);
-                    mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
-                    bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
-                             nb * kWBlockBytes, &w_full[s], pol);
-                    if (waited) {
-                        issue_b(d, s, kb, nb);
-                    } else {
-                        dq[ndef] = x.l;
-                        dkb[ndef] = kb;
-                        dnb[ndef] = nb;
-                        ++ndef;
-                    }
+                    __syncwarp(0x3u);
                 }
+                U += nunits;
             }
-            if (!waited) {
-                pdl_wait();
-                for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], i, dkb[i], dnb[i]);
-            }
-            if (trc) trc[6] = globaltimer();
+            if (!waited) release_deferred();
+            if (trc && lane == 0) trc[6] = globaltimer();
         }
     } else if (warp == kWarpMma) {
         int U = 0, JD = 0;
@@ -1349,9 +1355,12 @@ static int dyn_split(int kblocks) {
     return std::max(1, (kblocks + target - 1) / target);
 }
 static size_t dyn_items(const LinearArgs* a, int L) {
+    // upper bound over the tail refinement (any linear may be the tail one, <= 12-block items)
     size_t n = 0;
-    for (int l = 0; l < L; ++l)
-        n += (pad_n(a[l].N) / kTileN) * dyn_split(static_cast<int>(pad_k(a[l].K) / kBlockK));
+    for (int l = 0; l < L; ++l) {
+        const int kb = static_cast<int>(pad_k(a[l].K) / kBlockK);
+        n += (pad_n(a[l].N) / kTileN) * std::max(dyn_split(kb), (kb + 11) / 12);
+    }
     return n;
 }
 
@@ -1497,15 +1506,28 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     if (dyn) {
         const cudaError_t ed = ensure_dyn_attr();
         if (ed != cudaSuccess) return ed;
+        // Independent linears: hand the items out largest first (LPT), and end with the
+        // linear of fewest bytes cut into ~12-block items, so the last items -- whose
+        // duration is the tail -- are small.
+        int order[kMaxLin];
+        for (int l = 0; l < L; ++l) order[l] = l;
+        auto bytes_of = [&](int l) { return static_cast<long long>(p.lin[l].n_tiles) * p.lin[l].kblocks; };
+        std::sort(order, order + L, [&](int x, int y) { return bytes_of(x) > bytes_of(y); });
+        static const char* tail_env = std::getenv("ODY_DYN_TAIL_KB");  // diagnostics: 0 = off
+        const int tail_kb = tail_env ? std::atoi(tail_env) : 0;  // measured: finer tails cost more (L2 partials)
+        LinDesc sorted[kMaxLin];
+        for (int l = 0; l < L; ++l) sorted[l] = p.lin[order[l]];
         int ib = 0, tb = 0;
         for (int l = 0; l < L; ++l) {
-            LinDesc& d = p.lin[l];
+            LinDesc& d = sorted[l];
             d.split = dyn_split(d.kblocks);
+            if (l == L - 1 && L > 1 && tail_kb > 0) d.split = std::max(d.split, (d.kblocks + tail_kb - 1) / tail_kb);
             d.ibase = ib;
             d.tbase = tb;
             ib += d.n_tiles * d.split;
             tb += d.n_tiles;
         }
+        for (int l = 0; l < L; ++l) p.lin[l] = sorted[l];
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
         p.S = 1;
