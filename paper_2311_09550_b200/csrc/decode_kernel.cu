@@ -894,6 +894,9 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 // arrival counter, and the last item to arrive sums the S partials and runs the
 // epilogue.  No clusters, no DSMEM; the grid is one CTA per SM.
 constexpr int kDynStages = 10;
+constexpr int kDynThreads = 512;        // 16 warps: two converter groups (4..7, 8..11), epilogue 12..15
+constexpr int kDynConvGroups = 2;
+constexpr int kDynEpi0 = 12;
 constexpr int kItemSlots = 8;
 constexpr int kDynSmem = kDynStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
 static_assert(kDynSmem <= 227 * 1024, "smem budget");
@@ -915,7 +918,7 @@ __device__ __forceinline__ DynItem dyn_item(const PParams& p, int it) {
     return x;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
+__global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -953,7 +956,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
         }
         for (int i = 0; i < kItemSlots; ++i) {
             mbar_init(&i_full[i], 1);
-            mbar_init(&i_empty[i], 9);  // MMA + 4 converter + 4 epilogue warps
+            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4);  // MMA + converter + epilogue warps
         }
         fence_mbar_init();
     }
@@ -1078,9 +1081,10 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
             }
             ++JD;
         }
-    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
+    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kDynConvGroups) {
         const int q = warp & 3;
         const int r = 32 * q + lane;
+        const int grp = (warp - kWarpConv0) / 4;
         int U = 0;
         for (int j = 0;; ++j) {
             const int is = j % kItemSlots;
@@ -1091,6 +1095,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
             if (it < 0) break;
             const DynItem x = dyn_item(p, it);
             for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
+                if (U % kDynConvGroups != grp) continue;  // the other group widens this unit
                 const int nb = min(kUnitBlocks, x.kb_hi - kb);
                 const int s = U % kDynStages;
                 const int as = U % kAStages;
@@ -1125,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_dyn_kernel(const __gr
                 if (lane == 0) mbar_arrive(&a_full[as]);
             }
         }
-    } else if (warp >= kWarpEpi0) {
+    } else if (warp >= kDynEpi0) {
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
@@ -1535,7 +1540,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         if (plan_log) std::fprintf(stderr, "[ody] dynamic schedule: %d items over %d CTAs\n", ib, p.C);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(p.C);
-        cfg.blockDim = dim3(kThreads);
+        cfg.blockDim = dim3(kDynThreads);
         cfg.dynamicSmemBytes = kDynSmem;
         cfg.stream = st;
         cudaLaunchAttribute attr;
