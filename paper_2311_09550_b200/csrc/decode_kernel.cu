@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 // split tile's partials meet in L2: each item stores its int32 partial, bumps the tile's
 // arrival counter, and the last item to arrive sums the S partials and runs the
 // epilogue.  No clusters, no DSMEM; the grid is one CTA per SM.
-constexpr int kDynStages = 10;
+constexpr int kDynStages = 11;
 constexpr int kDynThreads = 512;        // 16 warps: two converter groups (4..7, 8..11), epilogue 12..15
 constexpr int kDynConvGroups = 2;
 constexpr int kDynEpi0 = 12;
@@ -1356,7 +1356,7 @@ static int dyn_split(int kblocks) {
     // measured (tools/program_trace.py, LLaMA-13B layer): whole 40-block tiles for
     // K = 5120 and 3 splits of 36 blocks for K = 13824 beat finer splits, whose L2 partial
     // round trips make the epilogue the bottleneck
-    static const int target = env ? std::max(1, std::atoi(env)) : 48;
+    static const int target = env ? std::max(1, std::atoi(env)) : 56;
     return std::max(1, (kblocks + target - 1) / target);
 }
 static size_t dyn_items(const LinearArgs* a, int L) {
