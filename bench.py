@@ -367,7 +367,8 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(f"M{m}")
+                js = json.load(f)
+            traffic = js.get(f"program_M{m}") if programs is not None else js.get(f"M{m}")
         except Exception:
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
