@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 // split tile's partials meet in L2: each item stores its int32 partial, bumps the tile's
 // arrival counter, and the last item to arrive sums the S partials and runs the
 // epilogue.  No clusters, no DSMEM; the grid is one CTA per SM.
-constexpr int kDynStages = 11;
+constexpr int kDynStages = 10;  // 10 x 20 KiB: leaves room for a co-resident act-quant CTA
 constexpr int kDynThreads = 512;        // 16 warps: two converter groups (4..7, 8..11), epilogue 12..15
 constexpr int kDynConvGroups = 2;
 constexpr int kDynEpi0 = 12;

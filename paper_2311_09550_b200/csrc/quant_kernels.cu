@@ -394,14 +394,12 @@ cudaError_t launch_act_quant_batch(int n, const void* const* x, const int* dtype
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (chunks <= 512) {
-        cfg.blockDim = dim3(512);
-        return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<512, 1>, b);
-    }
-    if (chunks <= 1024) {
-        cfg.blockDim = dim3(512);
-        return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<512, 2>, b);
-    }
+    // 256-thread CTAs (<= 16K registers, ~1 KiB smem): they stay co-resident with the decode
+    // program kernel running before them, so the PDL chain program -> act quant -> program
+    // lets the next program's CTAs start on every SM the previous one frees
+    cfg.blockDim = dim3(256);
+    if (chunks <= 512) return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<256, 2>, b);
+    if (chunks <= 1024) return cudaLaunchKernelEx(&cfg, act_quant_batch_kernel<256, 4>, b);
     return cudaErrorInvalidValue;  // K > 16384: the per-linear act_quant handles it
 }
 
