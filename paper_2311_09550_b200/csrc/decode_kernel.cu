@@ -987,6 +987,18 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                              d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
             };
             auto release_deferred = [&]() {
+                // The ring is full and the B tiles wait for the act quant (i.e. for the
+                // previous launch to finish): keep HBM busy by pulling the weights of the
+                // items most likely handed out next (second round) into L2 meanwhile.
+                if (lane == 0)
+                    for (int r2 = 1; r2 <= p.pf_units; ++r2) {
+                        const int it2 = static_cast<int>(blockIdx.x + r2 * gridDim.x);
+                        if (it2 >= p.n_items) break;
+                        const DynItem y = dyn_item(p, it2);
+                        const LinDesc& d2 = p.lin[y.l];
+                        bulk_prefetch_l2(d2.wp + (static_cast<size_t>(y.nt) * d2.kblocks + y.kb_lo) * kWBlockBytes,
+                                         static_cast<uint32_t>(y.kb_hi - y.kb_lo) * kWBlockBytes);
+                    }
                 pdl_wait();
                 waited = true;
                 for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], dst[i], dkb[i], dnb[i]);
@@ -1234,6 +1246,73 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     }
 }
 
+// K1 for the external activations of a program: one 128-thread CTA per token row,
+// each thread holding its <= 7 sixteen-element chunks PACKED (8 registers per chunk) across
+// the max pass and the quantize pass (quant16: the exact fast path + IEEE redo).  Small
+// enough (<= 80 registers x 128 threads, no shared arrays beyond 16 B) to stay
+// co-resident with a running decode program CTA, so in the PDL chain program -> K1 ->
+// program the next program's CTAs take every SM the previous one frees.
+constexpr int kRowThreads = 128;
+constexpr int kRowChunks = 7;  // K <= 128 * 7 * 16 = 14336
+struct RowBatch {
+    const unsigned short* x[kMaxLin];
+    size_t ldx[kMaxLin];
+    int M[kMaxLin], K[kMaxLin], Mp[kMaxLin], bf16[kMaxLin];
+    int8_t* q[kMaxLin];
+    float* s[kMaxLin];
+    int n, pdl;
+};
+
+template <bool BF16>
+__device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float* red) {
+    const unsigned short* row = b.x[i] + static_cast<size_t>(t) * b.ldx[i];
+    const int K = b.K[i];
+    const int nch = static_cast<int>(pad_k(K) / 16);
+    uint4 raw[kRowChunks][2];
+    uint32_t mb = 0u;
+#pragma unroll
+    for (int j = 0; j < kRowChunks; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c < nch) {
+            load16_raw(row, c * 16, K, false, raw[j][0], raw[j][1]);
+            mb = max(mb, absmax16_bits<BF16>(raw[j][0], raw[j][1]));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if ((threadIdx.x & 31) == 0) reinterpret_cast<uint32_t*>(red)[threadIdx.x >> 5] = mb;
+    __syncthreads();
+    uint32_t m = 0u;
+#pragma unroll
+    for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
+    float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
+    if (!(sc > 0.0f)) sc = kMinScale;
+    const float rcp = 1.0f / sc;
+    if (threadIdx.x == 0) b.s[i][t] = sc;
+#pragma unroll
+    for (int j = 0; j < kRowChunks; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c < nch) {
+            const uint4 qv = quant16<BF16>(raw[j][0], raw[j][1], sc, rcp, 0);
+            *reinterpret_cast<uint4*>(b.q[i] + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, b.Mp[i])) = qv;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __grid_constant__ RowBatch b) {
+    if (b.pdl) {
+        pdl_launch_dependents();
+        pdl_wait();
+    }
+    __shared__ float red[kRowThreads / 32];
+    int i = 0, t = blockIdx.x;
+    while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
+    if (b.bf16[i])
+        quant_row<true>(b, i, t, red);
+    else
+        quant_row<false>(b, i, t, red);
+}
+
 cudaError_t ensure_dyn_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
@@ -1470,7 +1549,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             bk[nb] = d.K;
             bq[nb] = q;
             bs[nb] = sa;
-            batch_ok &= d.K <= 16384;
+            batch_ok &= d.K <= kRowThreads * kRowChunks * 16 && (a[l].x_dtype == kDtypeF16 || a[l].x_dtype == kDtypeBF16);
             ++nb;
         }
     }
@@ -1481,7 +1560,31 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     if (nb > 0) {
         cudaError_t ea = cudaSuccess;
         if (batch_ok) {
-            ea = launch_act_quant_batch(nb, bx, bdt, bld, bm, bk, bq, bs, pdl, st);
+            RowBatch rb = {};
+            int rows = 0;
+            for (int i = 0; i < nb; ++i) {
+                rb.x[i] = static_cast<const unsigned short*>(bx[i]);
+                rb.ldx[i] = bld[i];
+                rb.M[i] = bm[i];
+                rb.K[i] = bk[i];
+                rb.Mp[i] = static_cast<int>(pad_m(bm[i]));
+                rb.bf16[i] = bdt[i] == kDtypeBF16 ? 1 : 0;
+                rb.q[i] = bq[i];
+                rb.s[i] = bs[i];
+                rows += bm[i];
+            }
+            rb.n = nb;
+            rb.pdl = pdl ? 1 : 0;
+            cudaLaunchConfig_t acfg = {};
+            acfg.gridDim = dim3(rows);
+            acfg.blockDim = dim3(kRowThreads);
+            acfg.stream = st;
+            cudaLaunchAttribute aattr;
+            aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            aattr.val.programmaticStreamSerializationAllowed = 1;
+            acfg.attrs = &aattr;
+            acfg.numAttrs = pdl ? 1 : 0;
+            ea = cudaLaunchKernelEx(&acfg, act_quant_rows_kernel, rb);
         } else {
             for (int i = 0; i < nb && ea == cudaSuccess; ++i)
                 ea = launch_act_quant(bx[i], bdt[i], bld[i], bm[i], bk[i], bq[i], bs[i], nullptr, nullptr,
@@ -1535,6 +1638,8 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) p.lin[l] = sorted[l];
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
+        static const char* pfi_env = std::getenv("ODY_DYN_PF_ITEMS");  // second-round items to L2
+        p.pf_units = pfi_env ? std::atoi(pfi_env) : 0;  // measured: guessing next items costs more
         p.S = 1;
         p.C = std::min(sms, ib);
         if (plan_log) std::fprintf(stderr, "[ody] dynamic schedule: %d items over %d CTAs\n", ib, p.C);
