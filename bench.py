@@ -386,29 +386,26 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
 
 
 def decode_sweep(args, dev, layers, stream):
-    """GB/s of each layer GEMM for M = 1..64 (configs[1] sweep)."""
+    """configs[1] sweep: the decoder layer's 4 linears at M = 1..64 as ONE linear program
+    per step (batched act quant + the dynamic decode kernel), rotating the weight copies;
+    GB/s = the step's algorithmic bytes / its device time (CUDA-graph replay, PDL)."""
     import torch
-    from paper_2311_09550_b200._lib import lib
     hbm, _ = peaks()
     res = {}
     for m in (1, 2, 4, 8, 16, 32, 64):
-        for _, n, k in LAYERS:
-            ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")
-        row = {}
-        for li, (name, n, k) in enumerate(LAYERS):
-            x = (torch.randn((m, k), device="cuda")).to(torch.float16)
-            out = torch.empty((m, n), dtype=torch.float16, device="cuda")
-            ws = [layers[c][li][1] for c in range(len(layers))]
+        xs = {k: (torch.randn((m, k), device="cuda")).to(torch.float16) for k in (HIDDEN, INTER)}
+        outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
+        progs = [dev.Program([dev.LinearCall(xs[w.k], w, outs[name]) for name, w in layers[c]])
+                 for c in range(len(layers))]
 
-            def fn(ws=ws):
-                for w in ws:
-                    dev.w4a8_linear(x, w, out=out, stream=stream, workspace=ws_buf)
+        def fn(progs=progs):
+            for pr in progs:
+                pr.run(pdl=True, stream=stream)
 
-            ms = _graph_time(fn, stream, reps=10) / len(ws)
-            gbs = linear_bytes(m, n, k) / (ms * 1e-3) / 1e9
-            row[name] = {"us": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3)}
-        res[f"M{m}"] = row
-    _ = lib
+        ms = _graph_time(fn, stream, reps=20) / len(progs)
+        gbs = step_bytes(m) / (ms * 1e-3) / 1e9
+        res[f"M{m}"] = {"us_per_step": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3),
+                        "fused": progs[0].fused}
     return res
 
 

@@ -893,13 +893,25 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 // split tile's partials meet in L2: each item stores its int32 partial, bumps the tile's
 // arrival counter, and the last item to arrive sums the S partials and runs the
 // epilogue.  No clusters, no DSMEM; the grid is one CTA per SM.
-constexpr int kDynStages = 10;  // 10 x 20 KiB: leaves room for a co-resident act-quant CTA
+
 constexpr int kDynThreads = 512;        // 16 warps: two converter groups (4..7, 8..11), epilogue 12..15
 constexpr int kDynConvGroups = 2;
 constexpr int kDynEpi0 = 12;
 constexpr int kItemSlots = 8;
-constexpr int kDynSmem = kDynStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
-static_assert(kDynSmem <= 227 * 1024, "smem budget");
+// Per-BN configuration of the dynamic kernel (BN = 16/32/64 tokens per MMA N).
+template <int BN>
+struct DynCfg {
+    static constexpr int kBBlock = BN * 128;                            // one B k-block tile
+    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock;  // weights + B tiles
+    static constexpr int kStages = (220 * 1024 - 3072) / kStageBytes < 10 ? (220 * 1024 - 3072) / kStageBytes : 10;
+    static constexpr int kSmem = kStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
+    // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
+    static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                       (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+    static_assert(kDBufs * BN <= kAColBase, "D buffers below the A stages");
+};
+
 
 struct DynItem {
     int l, nt, kb_lo, kb_hi, r;
@@ -918,7 +930,12 @@ __device__ __forceinline__ DynItem dyn_item(const PParams& p, int it) {
     return x;
 }
 
+template <int BN>
 __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
+    using C = DynCfg<BN>;
+    constexpr int kDynStages = C::kStages;
+    constexpr int kStageBytes = C::kStageBytes;
+    constexpr int kBBlockBytes = C::kBBlock;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -1067,7 +1084,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             const DynItem x = dyn_item(p, it);
             if (x.kb_hi <= x.kb_lo) continue;
             const int db = JD % kDBufs;
-            const uint32_t d_tmem = tmem + db * kBN;
+            const uint32_t d_tmem = tmem + db * BN;
             mbar_wait(&d_empty[db], ((JD / kDBufs) & 1) ^ 1);
             tc_fence_after();
             for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
@@ -1084,7 +1101,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     for (int c = 0; c < 4 * kUnitBlocks; ++c)
                         if (c < 4 * nb)
                             mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b0 + (c / 4) * kBBlockBytes + 32 * (c % 4)),
-                                      kIdesc, (kb > x.kb_lo || c > 0) ? 1u : 0u);
+                                      C::kIdesc, (kb > x.kb_lo || c > 0) ? 1u : 0u);
                     mma_commit(&a_empty[as]);
                     mma_commit(&w_empty[s]);
                     if (kb + nb >= x.kb_hi) mma_commit(&d_full[db]);
@@ -1147,7 +1164,6 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
         int JD = 0, cur_l = -1;
-        float sa[kBN];
         for (int j = 0;; ++j) {
             const int is = j % kItemSlots;
             mbar_wait(&i_full[is], (j / kItemSlots) & 1);
@@ -1157,28 +1173,30 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             if (it < 0) break;
             const DynItem x = dyn_item(p, it);
             const LinDesc& d = p.lin[x.l];
-            if (x.l != cur_l) {  // per-token scales of this linear (from the act-quant kernel)
-                if (cur_l < 0 && p.pdl) pdl_wait();
-                cur_l = x.l;
-#pragma unroll
-                for (int t = 0; t < kBN; ++t) sa[t] = t < d.M ? __ldcg(d.sa + t) : 0.0f;
-            }
+            if (cur_l < 0 && p.pdl) pdl_wait();  // token scales come from the act-quant kernel
+            cur_l = x.l;
             const int n = x.nt * kTileN + r;
             const float sw_n = n < d.N ? __ldg(d.sw + n) : 0.0f;  // in flight during the wait
-            uint32_t v[kBN];
+            uint32_t v[BN];
             if (x.kb_hi > x.kb_lo) {
                 const int db = JD % kDBufs;
                 mbar_wait(&d_full[db], (JD / kDBufs) & 1);
                 tc_fence_after();
-                tmem_ld_32x32b_x16(t_lane + db * kBN, v);
-                tmem_wait_ld();
+#pragma unroll
+                for (int tc = 0; tc < BN; tc += 16) {
+                    uint32_t w16[16];
+                    tmem_ld_32x32b_x16(t_lane + db * BN + tc, w16);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) v[tc + t] = w16[t];
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&d_empty[db]);
                 ++JD;
             } else {
 #pragma unroll
-                for (int t = 0; t < kBN; ++t) v[t] = 0u;
+                for (int t = 0; t < BN; ++t) v[t] = 0u;
             }
             bool fin = true;
             if (d.split > 1) {
@@ -1188,9 +1206,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 uint32_t* cnt = p.tile_cnt + d.tbase + x.nt;
                 if (x.r < d.split - 1) {
                     fin = false;
-                    int32_t* part = p.part + static_cast<size_t>(it) * kBN * kTileN;  // [t][row]
+                    int32_t* part = p.part + static_cast<size_t>(it) * BN * kTileN;  // [t][row]
 #pragma unroll
-                    for (int t = 0; t < kBN; ++t)
+                    for (int t = 0; t < BN; ++t)
                         if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
                     named_bar_sync(3, 128);  // this item's partial is written
                     if (r == 0) {
@@ -1204,19 +1222,19 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     }
                     named_bar_sync(3, 128);
                     __threadfence();
-                    const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * kBN * kTileN;
+                    const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * BN * kTileN;
                     for (int s2 = 0; s2 < d.split - 1; ++s2)
 #pragma unroll
-                        for (int t = 0; t < kBN; ++t)
-                            if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * kBN + t) * kTileN + r));
+                        for (int t = 0; t < BN; ++t)
+                            if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * BN + t) * kTileN + r));
                 }
             }
             if (fin && n < d.N) {
 #pragma unroll
-                for (int t = 0; t < kBN; ++t) {
+                for (int t = 0; t < BN; ++t) {
                     if (t < d.M) {
                         const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
-                        const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa[t], sw_n));
+                        const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(__ldg(d.sa + t), sw_n));
                         const size_t idx = static_cast<size_t>(t) * d.N + n;
                         if (d.out_dtype == kDtypeF32)
                             static_cast<float*>(d.out)[idx] = y;
@@ -1313,14 +1331,35 @@ __global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __
         quant_row<false>(b, i, t, red);
 }
 
+template <int BN>
 cudaError_t ensure_dyn_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   DynCfg<BN>::kSmem);
     });
     return err;
 }
+
+template <int BN>
+cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st) {
+    const cudaError_t ed = ensure_dyn_attr<BN>();
+    if (ed != cudaSuccess) return ed;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.C);
+    cfg.blockDim = dim3(kDynThreads);
+    cfg.dynamicSmemBytes = DynCfg<BN>::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN>, p);
+}
+
+int dyn_bn(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
 
 cudaError_t ensure_decode_attr() {
     static std::once_flag once;
@@ -1361,8 +1400,10 @@ int max_active_clusters(int S) {
     return n;
 }
 
+// Decode-width linear the program kernels accept: M <= 64 (the dynamic kernel; the
+// cluster kernel that quantizes dependent activations in-kernel takes M <= 16).
 bool lin_ok(const LinearArgs& a) {
-    return a.M >= 1 && a.M <= kBN && a.N >= 1 && a.K >= 1 &&
+    return a.M >= 1 && a.M <= 64 && a.N >= 1 && a.K >= 1 &&
            (a.x_dtype == kDtypeF16 || a.x_dtype == kDtypeBF16) &&
            (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0 &&
            (reinterpret_cast<uintptr_t>(a.sw) & 15) == 0;
@@ -1395,6 +1436,13 @@ DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms) {
         if (!lin_ok(a[l])) return best;
         chain |= deps && deps[l] >= 0;
         max_tiles = std::max(max_tiles, static_cast<int>(pad_n(a[l].N) / kTileN));
+    }
+    if (chain)
+        for (int l = 0; l < L; ++l)
+            if (a[l].M > kBN) return best;  // in-kernel quantization: M <= 16
+    if (!chain) {  // dynamic schedule: one CTA per SM, no cluster constraints
+        best = {1, std::min(sms, 1 << 20), std::min(sms, 1 << 20)};
+        return best;
     }
     double best_cost = 0;
     for (int S = 1; S <= kMaxSplit; ++S) {
@@ -1478,7 +1526,9 @@ bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms) 
 // shared by programs of different shapes never lands transient data in it --
 // [a8 codes + scales of the external x].
 size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L) {
-    size_t b = kZeroRegion + dyn_items(a, L) * kBN * kTileN * 4;  // + split partials
+    int mmax = 1;
+    for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
+    size_t b = kZeroRegion + dyn_items(a, L) * dyn_bn(mmax) * kTileN * 4;  // + split partials
     for (int l = 0; l < L; ++l)
         if (!deps || deps[l] < 0) b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
     return b;
@@ -1504,7 +1554,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     p.tile_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kProgramCounterRegion);
     p.acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kAccOffset);
     p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
-    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion + dyn_items(a, L) * kBN * kTileN * 4;
+    int mmax_s = 1;
+    for (int l = 0; l < L; ++l) mmax_s = std::max(mmax_s, a[l].M);
+    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion + dyn_items(a, L) * dyn_bn(mmax_s) * kTileN * 4;
     int nb = 0;
     const void* bx[kMaxLin];
     int bdt[kMaxLin], bm[kMaxLin], bk[kMaxLin];
@@ -1612,8 +1664,6 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     static const char* dyn_env = std::getenv("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
     const bool dyn = !chain && nb == L && !(dyn_env && dyn_env[0] == '0');
     if (dyn) {
-        const cudaError_t ed = ensure_dyn_attr();
-        if (ed != cudaSuccess) return ed;
         // Independent linears: hand the items out largest first (LPT), and end with the
         // linear of fewest bytes cut into ~12-block items, so the last items -- whose
         // duration is the tail -- are small.
@@ -1643,17 +1693,13 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         p.S = 1;
         p.C = std::min(sms, ib);
         if (plan_log) std::fprintf(stderr, "[ody] dynamic schedule: %d items over %d CTAs\n", ib, p.C);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(p.C);
-        cfg.blockDim = dim3(kDynThreads);
-        cfg.dynamicSmemBytes = kDynSmem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr;
-        attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr.val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = &attr;
-        cfg.numAttrs = prog_pdl ? 1 : 0;
-        return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel, p);
+        int mmax = 1;
+        for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
+        switch (dyn_bn(mmax)) {
+            case 16: return launch_dyn<16>(p, prog_pdl, st);
+            case 32: return launch_dyn<32>(p, prog_pdl, st);
+            default: return launch_dyn<64>(p, prog_pdl, st);
+        }
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.grid);

@@ -51,6 +51,7 @@ def _assert_bits(got, want):
     (1, 128, 128), (3, 130, 1000), (16, 1000, 4100), (7, 384, 64), (2, 257, 2049),
     (16, 5120, 16384),   # kb 128: the largest K the resident B holds (S = 8, 16 blocks/CTA)
     (5, 15360, 5120), (16, 27648, 5120), (11, 5120, 13824), (1, 5120, 5120),
+    (17, 640, 1536), (33, 5120, 5120), (64, 2048, 13824), (48, 130, 1000),  # BN 32 / 64 kernels
 ])
 def test_decode_linear_vs_oracle(m, n, k, oracle, torch_cuda, dev):
     torch = torch_cuda
@@ -179,7 +180,7 @@ def _two_kernel(dev, torch, x, w, odt):
         dev.lib().ody_dev_set_linear_mode(2)
 
 
-@pytest.mark.parametrize("m", [1, 3, 16])
+@pytest.mark.parametrize("m", [1, 3, 16, 32, 64])
 def test_program_independent_layer(m, torch_cuda, dev):
     """The 4 LLaMA-13B layer linears as ONE launch (independent inputs): every output is
     bit-identical to the same linear run alone."""
@@ -247,13 +248,13 @@ def test_program_dependency_chain(torch_cuda, dev):
 
 
 def test_program_fallback_and_errors(torch_cuda, dev):
-    """M > 16 falls back to one launch per linear (same results); a forward dependency
+    """M > 64 falls back to one launch per linear (same results); a forward dependency
     is rejected with EINVAL like the reference's argument checks."""
     torch = torch_cuda
     from paper_2311_09550_b200._lib import OdyError
     w, _, _ = _weights(torch, dev, 256, 512, seed=7)
-    x = torch.randn((40, 512), device="cuda").half()
-    out = torch.empty((40, 256), dtype=torch.float16, device="cuda")
+    x = torch.randn((80, 512), device="cuda").half()
+    out = torch.empty((80, 256), dtype=torch.float16, device="cuda")
     prog = dev.Program([dev.LinearCall(x, w, out)])
     assert not prog.fused
     prog.run()

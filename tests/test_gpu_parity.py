@@ -330,7 +330,8 @@ def test_fused_linear_matches_oracle(m, layer, linear_mode, oracle, torch_cuda, 
     if not np.array_equal(bits_of(got_np), bits_of(want)):
         bad = np.argwhere(got_np != want)
         pytest.fail(f"{len(bad)} mismatches, first {bad[:4].tolist()}")
-    assert dev.lib().ody_dev_linear_is_fused(m, n, k) == (1 if (linear_mode and m <= 16) else 0)
+    fused_upto = {0: 0, 1: 16, 2: 64}[linear_mode]  # decode program: M <= 64
+    assert dev.lib().ody_dev_linear_is_fused(m, n, k) == (1 if m <= fused_upto else 0)
 
 
 def test_fused_linear_input_dtypes(linear_mode, oracle, torch_cuda, dev):
