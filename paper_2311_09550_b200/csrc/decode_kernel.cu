@@ -997,11 +997,12 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             // get their B tiles once it returns (each lane records its own)
             bool waited = p.pdl == 0;
             int dq[kDynStages], dst[kDynStages], dkb[kDynStages], dnb[kDynStages], ndef = 0;
+            // programs quantize into a compact a8 layout (Mp == BN rows per k-block), so the B
+            // tiles of a unit are one contiguous run
             auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
                 mbar_expect_tx(&b_full[s], nb * kBBlockBytes);
-                for (int b = 0; b < nb; ++b)
-                    bulk_g2s(ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
-                             d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
+                bulk_g2s(ring + s * kStageBytes + kUnitBytes, d.qa + static_cast<size_t>(kb) * d.Mp * 128,
+                         nb * kBBlockBytes, &b_full[s], pol_b);
             };
             auto release_deferred = [&]() {
                 // The ring is full and the B tiles wait for the act quant (i.e. for the
@@ -1403,7 +1404,7 @@ int max_active_clusters(int S) {
 // Decode-width linear the program kernels accept: M <= 64 (the dynamic kernel; the
 // cluster kernel that quantizes dependent activations in-kernel takes M <= 16).
 bool lin_ok(const LinearArgs& a) {
-    return a.M >= 1 && a.M <= 64 && a.N >= 1 && a.K >= 1 &&
+    return a.M >= 1 && a.M <= 64 && a.N >= 1 && a.K >= 1 && a.K <= kRowThreads * kRowChunks * 16 &&
            (a.x_dtype == kDtypeF16 || a.x_dtype == kDtypeBF16) &&
            (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0 &&
            (reinterpret_cast<uintptr_t>(a.sw) & 15) == 0;
@@ -1565,6 +1566,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     float* bs[kMaxLin];
     bool batch_ok = true;
     int rot = 0;
+    int mmax_b = 1;
+    for (int l = 0; l < L; ++l) mmax_b = std::max(mmax_b, a[l].M);
+    const int b_rows = chain ? kBN : dyn_bn(mmax_b);
     for (int l = 0; l < L; ++l) {
         LinDesc& d = p.lin[l];
         d.x = a[l].x;
@@ -1593,7 +1597,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             cursor += round_up(pad_m(d.M) * 4, 256);
             d.qa = q;
             d.sa = sa;
-            d.Mp = static_cast<int>(pad_m(d.M));
+            d.Mp = b_rows;  // compact a8 layout: BN rows per k-block
             bx[nb] = a[l].x;
             bdt[nb] = a[l].x_dtype;
             bld[nb] = a[l].ldx;
@@ -1606,6 +1610,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         }
     }
     uint32_t* counters = static_cast<uint32_t*>(scratch);
+    (void)counters;
     for (int l = 0; l < L; ++l)
         if (p.lin[l].dep >= 0) p.lin[p.lin[l].dep].signal = 1;
     bool prog_pdl = pdl;
@@ -1619,7 +1624,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
                 rb.ldx[i] = bld[i];
                 rb.M[i] = bm[i];
                 rb.K[i] = bk[i];
-                rb.Mp[i] = static_cast<int>(pad_m(bm[i]));
+                rb.Mp[i] = b_rows;
                 rb.bf16[i] = bdt[i] == kDtypeBF16 ? 1 : 0;
                 rb.q[i] = bq[i];
                 rb.s[i] = bs[i];
