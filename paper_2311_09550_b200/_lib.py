@@ -86,6 +86,7 @@ SIGNATURES = {
     "ody_dev_program_is_fused": (c_int, [c_void_p, c_int]),
     "ody_dev_linear_is_fused": (c_int, [c_size_t, c_size_t, c_size_t]),
     "ody_dev_set_linear_mode": (None, [c_int]),
+    "ody_dev_set_prefill_min_m": (None, [c_int]),
     "ody_dev_set_trace": (None, [c_void_p]),
     "ody_dev_set_act_trace": (None, [c_void_p]),
     "ody_dev_a8_unpack": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p,

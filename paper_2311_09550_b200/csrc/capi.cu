@@ -660,6 +660,7 @@ size_t ody_dev_linear_workspace_bytes(size_t m, size_t n, size_t k) {
 }
 
 void ody_dev_set_linear_mode(int mode) { set_linear_mode(mode); }
+void ody_dev_set_prefill_min_m(int m) { set_prefill_min_m(m); }
 
 int ody_dev_linear_is_fused(size_t m, size_t n, size_t k) {
     return linear_is_fused(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0) ? 1 : 0;

@@ -1108,6 +1108,7 @@ size_t gemm_workspace_bytes(int M, int N, int K, int num_sms) {
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
+    if (prefill_eligible(a.M, a.N, a.K)) return launch_w4a8_prefill(a, st);  // prefill_kernel.cu
     const int sms = a.max_ctas > 0 ? a.max_ctas : device_sm_count();
     const SkPlan s = plan_for(a.M, a.N, a.K, sms);
     Params p = {};
