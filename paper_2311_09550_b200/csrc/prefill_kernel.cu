@@ -50,8 +50,8 @@ constexpr int kPThreads = 512;  // 16 warps
 constexpr int kPWarpProducer = 0;
 constexpr int kPWarpMma = 1;
 constexpr int kPWarpAlloc = 2;
-constexpr int kPWarpConv0 = 4;   // warps 4..11: two converter groups of 4 (alternate k-blocks)
-constexpr int kPConvGroups = 2;
+constexpr int kPWarpConv0 = 4;   // warps 4..11: converters
+constexpr int kPConvWarps = 8;
 constexpr int kPWarpEpi0 = 12;   // warps 12..15
 constexpr int kPTmemCols = 512;
 constexpr int kATileBytes = kTileN * kBlockK;  // 16 KiB of widened int8 weights
@@ -71,15 +71,16 @@ __device__ __forceinline__ void tre(unsigned long long* t, int slot, int j) {
     if (t && blockIdx.x < 2 && j < 16) t[2 * kTrK * 4 + (blockIdx.x * 16 + j) * 2 + slot] = globaltimer();
 }
 
-template <int BT, int AS_ = 4>
+template <int BT>
 struct PCfg {
     static constexpr int kHalfT = BT / 2;                  // tokens of B staged per CTA
     static constexpr int kBBytes = kHalfT * kBlockK;       // 16 / 8 KiB
-    // load ring: [B half tile | packed W block]; A ring: widened weights (SWIZZLE_128B)
+    // one ring; a stage = [B half tile | packed W block] (landed by the producer) + the
+    // widened A tile (written by the converter group that owns the stage), all released
+    // together by the MMA commit
     static constexpr int kLoadBytes = kBBytes + kWBlockBytes;
-    static constexpr int kAStages = AS_;
-    static constexpr int kLoadStages =
-        (204 * 1024 - kAStages * kATileBytes - kOutStageBytes) / kLoadBytes;
+    static constexpr int kLoadStages = (216 * 1024 - kOutStageBytes) / (kLoadBytes + kATileBytes);
+    static constexpr int kAStages = kLoadStages;
     static constexpr int kScaleBytes = 2 * BT * 4;         // per-token scales, per D buffer
     static constexpr int kSmemBytes = kAStages * kATileBytes + kLoadStages * kLoadBytes + kOutStageBytes +
                                       kScaleBytes + 1024 + 1024;
@@ -106,6 +107,7 @@ struct PParams {
     int pdl;
     int vec_out;  // output rows are 16-byte aligned (N * esz % 16 == 0, aligned base)
     unsigned long long* trace;  // diagnostics: CTAs 0/1, per k-block globaltimer (kTrK slots)
+    int cw;   // converter warps per k-block (1, 2 or 4)
     int dbg;  // diagnostics (ODY_PREFILL_DBG bits): 1 no loads, 2 no widening, 4 no MMAs, 8 no stores
 };
 
@@ -140,6 +142,16 @@ __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// Global -> shared 1-D bulk copy delivered to the same smem offset (and completing tx
+// bytes on the same-offset mbarrier) in every CTA of ctaMask.
+__device__ __forceinline__ void bulk_g2s_mc(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
@@ -171,9 +183,14 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
         : "memory");
 }
 
-template <int BT, int AS_>
+// CL = CTAs per cluster: 2 (one pair) or 4 (two pairs on adjacent weight tiles, same
+// tokens): each CTA then bulk-loads 1/(CL/2) of its activation half tile and multicasts
+// it to the same-rank CTA of every pair, cutting the per-SM L2 read bytes.
+template <int BT, int CL>
 __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParams p) {
-    using C = PCfg<BT, AS_>;
+    using C = PCfg<BT>;
+    constexpr int NP = CL / 2;                          // pairs per cluster
+    constexpr uint16_t kAllMask = (1u << CL) - 1u;
     constexpr int LS = C::kLoadStages, AS = C::kAStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -185,28 +202,31 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
     uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + kOutStageBytes + C::kScaleBytes);
     uint64_t* full = bars;                // [LS] producer tx (local)
     uint64_t* empty = full + LS;          // [LS] MMA commit (multicast to the pair)
-    uint64_t* ready = empty + LS;         // [AS] leader: both CTAs' converters (count 8)
-    uint64_t* a_empty = ready + AS;       // [AS] MMA commit (multicast)
-    uint64_t* d_full = a_empty + AS;      // [2] MMA commit (multicast)
+    uint64_t* ready = empty + LS;         // [AS] leader: both CTAs' converter warps
+    uint64_t* d_full = ready + AS;        // [2] MMA commit (multicast)
     uint64_t* d_empty = d_full + 2;       // [2] leader: both CTAs' epilogue warps (count 8)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
     const uint32_t a_base = smem_u32(aring), l_base = smem_u32(lring);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the pair's MMAs)
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1u;             // rank in the pair; 0 = leader (issues the MMAs)
+    const int pi = static_cast<int>(crank >> 1);  // pair index in the cluster
+    const uint32_t leader = crank & ~1u;
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pi));
+    uint16_t peer_mask = 0;                       // same pair rank in every pair (B multicast)
+#pragma unroll
+    for (int q = 0; q < NP; ++q) peer_mask |= static_cast<uint16_t>(1u << (2 * q + rank));
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     if (p.pdl) pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < LS; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], NP);  // every pair's MMAs released the stage
         }
-        for (int i = 0; i < AS; ++i) {
-            mbar_init(&ready[i], 8);
-            mbar_init(&a_empty[i], 1);
-        }
+        for (int i = 0; i < AS; ++i) mbar_init(&ready[i], 2 * p.cw);  // both CTAs' converter warps
         for (int i = 0; i < 2; ++i) {
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], 8);
@@ -229,8 +249,9 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             const uint64_t pol_a = l2_policy_evict_last();
             if (p.pdl) pdl_wait();  // activations come from the previous kernel
             int u = 0;
+            constexpr int kSlice = C::kBBytes / NP;  // this CTA's multicast share of B
             for (int tile = cid; tile < p.tiles; tile += ncl) {
-                const int np = tile / p.m_tiles, mt = tile % p.m_tiles;
+                const int np = (tile / p.m_tiles) * NP + pi, mt = tile % p.m_tiles;
                 const int nt = 2 * np + static_cast<int>(rank);
                 const int tok0 = mt * BT + static_cast<int>(rank) * C::kHalfT;
                 const bool has_w = nt < p.n_tiles;
@@ -250,14 +271,19 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                     if (has_w)
                         bulk_g2s(st + C::kBBytes, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
                                  kWBlockBytes, &full[s], pol_w);
-                    if (has_b)
-                        bulk_g2s(st, bsrc + static_cast<size_t>(kb) * p.Mp * kBlockK, C::kBBytes, &full[s],
-                                 pol_a);
+                    if (has_b) {
+                        const int8_t* src = bsrc + static_cast<size_t>(kb) * p.Mp * kBlockK + pi * kSlice;
+                        if (NP == 1)
+                            bulk_g2s(st, src, C::kBBytes, &full[s], pol_a);
+                        else
+                            bulk_g2s_mc(st + pi * kSlice, src, kSlice, &full[s], peer_mask, pol_a);
+                    }
                 }
             }
         }
     } else if (warp == kPWarpMma) {
         if (rank == 0) {
+            const uint16_t all_mask = kAllMask;
             int u = 0, j = 0;
             for (int tile = cid; tile < p.tiles; tile += ncl, ++j) {
                 const int db = j & 1;
@@ -276,58 +302,65 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                             if (!(p.dbg & 4))
                                 mma2_i8_ss(d_tmem, sw128_desc(ab + 32 * c), sw128_desc(bb + 32 * c), C::kIdesc,
                                            (kb > 0 || c > 0) ? 1u : 0u);
-                        mma2_commit_mc(&empty[s], 0x3);
-                        mma2_commit_mc(&a_empty[as], 0x3);
+                        mma2_commit_mc(&empty[s], all_mask);  // B slices came from every pair
                     }
                     __syncwarp();
                 }
-                if (elect_one()) mma2_commit_mc(&d_full[db], 0x3);
+                if (elect_one()) mma2_commit_mc(&d_full[db], pair_mask);
                 __syncwarp();
             }
         }
-    } else if (warp >= kPWarpConv0 && warp < kPWarpConv0 + 4 * kPConvGroups) {
-        const int g = (warp - kPWarpConv0) / 4;
-        const int r = 32 * (warp & 3) + lane;  // weight row of this CTA's tile
-        const uint32_t ready_leader = mapa_shared(smem_u32(ready), 0);
-        const uint32_t sw = static_cast<uint32_t>(r & 7);
+    } else if (warp >= kPWarpConv0 && warp < kPWarpConv0 + kPConvWarps) {
+        // p.cw warps widen one k-block (128 rows).  Group g of the kPConvWarps / p.cw
+        // groups OWNS the stages s with s % groups == g and takes their k-blocks in
+        // order (so no waiter ever runs a phase ahead on a barrier), while the groups'
+        // per-k-block fence + cluster-arrive latencies overlap.
+        const int cw = p.cw, groups = kPConvWarps / cw, rows_per = 4 / cw;
+        const int g = (warp - kPWarpConv0) / cw, wi = (warp - kPWarpConv0) % cw;
+        const uint32_t ready_leader = mapa_shared(smem_u32(ready), leader);
         const int total = ((p.tiles - cid + ncl - 1) / ncl) * p.kblocks;  // this pair's k-blocks
-        for (int u = g; u < total; u += kPConvGroups) {
-            const int s = u % LS, as = u % AS;
+        for (int u = 0; u < total; ++u) {
+            const int s = u % LS, as = s;
+            if (s % groups != g) continue;
             mbar_wait(&full[s], (u / LS) & 1);
-            if (r == 0) trk(p.trace, 1, u);
-            const uint32_t src = l_base + s * C::kLoadBytes + C::kBBytes + r * 16;
-            uint4 v[4];
+            if (wi == 0 && lane == 0) trk(p.trace, 1, u);
+#pragma unroll 1
+            for (int rr = 0; rr < rows_per; ++rr) {
+                const int r = (wi * rows_per + rr) * 32 + lane;  // weight row of this CTA's tile
+                const uint32_t sw = static_cast<uint32_t>(r & 7);
+                const uint32_t src = l_base + s * C::kLoadBytes + C::kBBytes + r * 16;
+                uint4 v[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) v[c] = lds128(src + c * 2048);
-            mbar_wait(&a_empty[as], ((u / AS) & 1) ^ 1);
-            const uint32_t dst = a_base + as * kATileBytes + r * 128;
+                for (int c = 0; c < 4; ++c) v[c] = lds128(src + c * 2048);
+                const uint32_t dst = a_base + as * kATileBytes + r * 128;
 #pragma unroll
-            for (int c = 0; c < (p.dbg & 2 ? 0 : 4); ++c) {
-                // word j of the row chunk: k = 32c+8j+0..3 low nibbles, +4..7 high nibbles
-                const uint4 lo = make_uint4((v[c].x << 4) & 0xF0F0F0F0u, v[c].x & 0xF0F0F0F0u,
-                                            (v[c].y << 4) & 0xF0F0F0F0u, v[c].y & 0xF0F0F0F0u);
-                const uint4 hi = make_uint4((v[c].z << 4) & 0xF0F0F0F0u, v[c].z & 0xF0F0F0F0u,
-                                            (v[c].w << 4) & 0xF0F0F0F0u, v[c].w & 0xF0F0F0F0u);
-                sts128(dst + (((2 * c) ^ sw) << 4), lo);      // k 32c .. 32c+15
-                sts128(dst + (((2 * c + 1) ^ sw) << 4), hi);  // k 32c+16 .. 32c+31
+                for (int c = 0; c < (p.dbg & 2 ? 0 : 4); ++c) {
+                    // word j of the row chunk: k = 32c+8j+0..3 low nibbles, +4..7 high nibbles
+                    const uint4 lo = make_uint4((v[c].x << 4) & 0xF0F0F0F0u, v[c].x & 0xF0F0F0F0u,
+                                                (v[c].y << 4) & 0xF0F0F0F0u, v[c].y & 0xF0F0F0F0u);
+                    const uint4 hi = make_uint4((v[c].z << 4) & 0xF0F0F0F0u, v[c].z & 0xF0F0F0F0u,
+                                                (v[c].w << 4) & 0xF0F0F0F0u, v[c].w & 0xF0F0F0F0u);
+                    sts128(dst + (((2 * c) ^ sw) << 4), lo);      // k 32c .. 32c+15
+                    sts128(dst + (((2 * c + 1) ^ sw) << 4), hi);  // k 32c+16 .. 32c+31
+                }
             }
             fence_proxy_async_shared();  // generic smem writes -> tensor-core reads
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ready_leader + as * 8);
-            if (r == 0) trk(p.trace, 2, u);
+            if (wi == 0 && lane == 0) trk(p.trace, 2, u);
         }
     } else if (warp >= kPWarpEpi0) {
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
-        const uint32_t d_empty_leader = mapa_shared(smem_u32(d_empty), 0);
+        const uint32_t d_empty_leader = mapa_shared(smem_u32(d_empty), leader);
         const int esz = (p.acc_out || p.out_dtype == kDtypeF32) ? 4 : 2;
         const uint32_t ob = smem_u32(ostage);
         if (p.pdl) pdl_wait();
         int j = 0;
         for (int tile = cid; tile < p.tiles; tile += ncl, ++j) {
             const int db = j & 1;
-            const int np = tile / p.m_tiles, mt = tile % p.m_tiles;
+            const int np = (tile / p.m_tiles) * NP + pi, mt = tile % p.m_tiles;
             const int n0 = (2 * np + static_cast<int>(rank)) * kTileN;
             const int n = n0 + r;
             const int t0 = mt * BT;
@@ -445,63 +478,63 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
     if (warp == kPWarpAlloc) tmem_dealloc2(tmem, kPTmemCols);
 }
 
-template <int BT, int AS_>
+template <int BT, int CL>
 cudaError_t prefill_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(w4a8_prefill_kernel<BT, AS_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   PCfg<BT, AS_>::kSmemBytes);
+        err = cudaFuncSetAttribute(w4a8_prefill_kernel<BT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   PCfg<BT>::kSmemBytes);
     });
     return err;
 }
 
-template <int BT, int AS_>
+template <int BT, int CL>
 int prefill_max_clusters() {
     static int n = [] {
-        if (prefill_attr<BT, AS_>() != cudaSuccess) return 0;
+        if (prefill_attr<BT, CL>() != cudaSuccess) return 0;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * 74);
+        cfg.gridDim = dim3(CL * (148 / CL));
         cfg.blockDim = dim3(kPThreads);
-        cfg.dynamicSmemBytes = PCfg<BT, AS_>::kSmemBytes;
+        cfg.dynamicSmemBytes = PCfg<BT>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.x = CL;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, w4a8_prefill_kernel<BT, AS_>, &cfg) != cudaSuccess || c <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&c, w4a8_prefill_kernel<BT, CL>, &cfg) != cudaSuccess || c <= 0) {
             cudaGetLastError();
-            c = device_sm_count() / 2;
+            c = device_sm_count() / CL;
         }
         return c;
     }();
     return n;
 }
 
-template <int BT, int AS_ = 4>
+template <int BT, int CL>
 cudaError_t launch_prefill_bt(PParams p, int max_ctas, cudaStream_t st) {
-    const cudaError_t e = prefill_attr<BT, AS_>();
+    const cudaError_t e = prefill_attr<BT, CL>();
     if (e != cudaSuccess) return e;
     p.m_tiles = (p.M + BT - 1) / BT;
-    p.tiles = p.pair_tiles * p.m_tiles;
-    int clusters = prefill_max_clusters<BT, AS_>();
-    if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / 2));
+    p.tiles = ((p.pair_tiles + CL / 2 - 1) / (CL / 2)) * p.m_tiles;  // cluster tiles
+    int clusters = prefill_max_clusters<BT, CL>();
+    if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / CL));
     clusters = std::min(clusters, p.tiles);
     static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
     if (plan_log)
-        std::fprintf(stderr, "[ody] prefill %dx%dx%d: BT %d tiles %d clusters %d stages %d\n", p.M, p.N, p.K,
-                     BT, p.tiles, clusters, PCfg<BT, AS_>::kLoadStages);
+        std::fprintf(stderr, "[ody] prefill %dx%dx%d: BT %d CL %d tiles %d clusters %d stages %d\n", p.M, p.N, p.K,
+                     BT, CL, p.tiles, clusters, PCfg<BT>::kLoadStages);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
+    cfg.gridDim = dim3(CL * clusters);
     cfg.blockDim = dim3(kPThreads);
-    cfg.dynamicSmemBytes = PCfg<BT, AS_>::kSmemBytes;
+    cfg.dynamicSmemBytes = PCfg<BT>::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     int na = 1;
@@ -512,7 +545,7 @@ cudaError_t launch_prefill_bt(PParams p, int max_ctas, cudaStream_t st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, w4a8_prefill_kernel<BT, AS_>, p);
+    return cudaLaunchKernelEx(&cfg, w4a8_prefill_kernel<BT, CL>, p);
 }
 
 }  // namespace
@@ -550,19 +583,17 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
         const void* o = a.acc_out ? static_cast<const void*>(a.acc_out) : a.out;
         p.vec_out = ((static_cast<size_t>(a.N) * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) ? 1 : 0;
     }
+    static const char* cw_env = std::getenv("ODY_PREFILL_CW");
+    p.cw = cw_env ? std::atoi(cw_env) : 1;
+    if (p.cw != 1 && p.cw != 2 && p.cw != 4) p.cw = 1;
     static const char* dbg_env = std::getenv("ODY_PREFILL_DBG");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
     static const char* bt_env = std::getenv("ODY_PREFILL_BT");
     const int bt = bt_env ? std::atoi(bt_env) : 256;
-    static const char* as_env = std::getenv("ODY_PREFILL_AS");
-    const int as = as_env ? std::atoi(as_env) : 4;
-    if (bt == 128) return launch_prefill_bt<128>(p, a.max_ctas, st);
-    switch (as) {
-        case 3: return launch_prefill_bt<256, 3>(p, a.max_ctas, st);
-        case 5: return launch_prefill_bt<256, 5>(p, a.max_ctas, st);
-        case 6: return launch_prefill_bt<256, 6>(p, a.max_ctas, st);
-        default: return launch_prefill_bt<256, 4>(p, a.max_ctas, st);
-    }
+    static const char* cl_env = std::getenv("ODY_PREFILL_CL");
+    const int cl = cl_env ? std::atoi(cl_env) : 4;
+    if (bt == 128) return launch_prefill_bt<128, 2>(p, a.max_ctas, st);
+    return cl == 2 ? launch_prefill_bt<256, 2>(p, a.max_ctas, st) : launch_prefill_bt<256, 4>(p, a.max_ctas, st);
 }
 
 }  // namespace odyb200
