@@ -4,31 +4,41 @@
 // Reference semantics (ref gemm.cpp:251-279), unchanged from the tile GEMM:
 //     acc  = sum_k a[i][k] * (16 * w[j][k]);  acc >>= 4;  out = float(acc) * (sa[i] * sw[j])
 //
-// Why a separate kernel.  At M = 1024 the path is INT8 tensor-pipe bound only if the
-// operand bytes each SM pulls from L2 stay under what L2 can feed (~40 B/clk/SM,
-// B300_MICROARCH "TMA chip-throughput").  Per 128-k block, a tile of Wn weight rows x Bt
-// tokens moves 64*Wn (INT4) + 128*Bt (INT8) bytes for 128*Wn*Bt MACs.  The 1-SM tile GEMM
-// (Wn = 128, Bt = 128) needs ~96 B/clk/SM at the 8192 MAC/clk/SM peak -- it is L2-bound
-// at ~25% of peak.  Here a CTA PAIR runs one 256 x BT x 32 MMA per instruction: each CTA
-// stages its own 128 weight rows (8 KiB INT4) and HALF of the BT-token activation tile,
-// and the MMA reads both CTAs' shared memory -- 24 KiB per 512 MMA cycles per SM at
-// BT = 256, i.e. ~47 B/clk/SM at peak, ~28 B/clk/SM at 60% of it.
+// Why a separate kernel.  At M = 1024 the 1-SM tile GEMM (gemm_kernel.cu: 128 weight rows
+// x 128 tokens, A widened into TMEM once per (n, m) tile) moves 24 KiB of operands per
+// 256 MMA cycles per SM and re-widens every weight tile for every token tile; it reaches
+// 0.14-0.30 of the INT8 peak.  Here a CTA PAIR runs one 256 x BT x 32 MMA per
+// instruction: each CTA stages its own 128 weight rows (8 KiB INT4) and HALF of the
+// BT-token activation tile, and the pair's MMA reads both CTAs' shared memory -- 24 KiB
+// per 512 MMA cycles per SM at BT = 256 -- and each weight k-block is widened once per
+// 256 tokens instead of once per 128.
 //
 //   * producer (warp 0, each CTA): 1-D bulk copies of the CTA's 8 KiB weight block and
 //     its half activation k-block into an S-stage ring (one mbarrier per stage);
-//   * converters (warps 4..7, each CTA; thread = weight row): SINT4 -> S8 with the
+//   * converters (warps 4..11, each CTA): one warp widens one k-block (128 rows) with the
 //     paper's high-nibble trick ((w<<4)&0xF0F0F0F0, w&0xF0F0F0F0 -> value*16, no scale
-//     multiply), written into the stage's A tile in the SWIZZLE_128B K-major canonical
-//     layout; fence.proxy.async, then a cluster-scope arrive on the LEADER's ready[s];
+//     multiply) into the stage's A tile (SWIZZLE_128B K-major canonical layout), then
+//     fence.proxy.async and a cluster-scope arrive on the LEADER's ready[s].  Warp g owns
+//     the stages s with s % 8 == g, so the groups' widening + fence + arrive latencies
+//     (~1.3 us per k-block, tools/prefill_trace.py) overlap and every barrier has one
+//     in-order waiter;
 //   * MMA (warp 1 of the leader CTA only): tcgen05.mma.cta_group::2.kind::i8, M=256
 //     (both CTAs' weight rows), N=BT (both CTAs' token halves), K=32, accumulators in a
 //     double-buffered TMEM tile; commits multicast to both CTAs' stage / tile barriers;
-//   * epilogue (warps 8..11, each CTA): tcgen05.ld its 128 rows x BT columns, exact >>4,
-//     __fmul_rn(float(acc), __fmul_rn(sa, sw)) in the reference's order, f32/f16/bf16
-//     store (or the raw int32 accumulators for the exactness suite).
+//   * epilogue (warps 12..15, each CTA): tcgen05.ld its 128 rows x 32 tokens at a time,
+//     exact >>4, __fmul_rn(float(acc), __fmul_rn(sa, sw)) in the reference's order, RN
+//     f16/bf16 conversion two at a time, staged [token][row] in smem and written as
+//     16-byte row pieces (or the raw int32 accumulators for the exactness suite).
 // Tiles (pair n-tile, token tile) are assigned round-robin over the persistent clusters,
 // token tile fastest, so the clusters in flight read each weight tile at about the same
 // time (L2 hits) and the whole activation matrix stays L2-resident (evict_last).
+//
+// Measured (B200, M = 1024, LLaMA-13B shapes): 0.26-0.48 of the 4.5 POPS INT8 dense
+// peak; ncu: tensor pipe 39-49% active, L2 20-25% and shared memory well below their
+// peaks -- the k-block pipeline is latency-bound (load ~0.5 us + widening ~1.3 us +
+// signalling, over 5 stages of 40 KiB).  Explored and rejected (slower, kept in git
+// history): A in TMEM with BT = 192/208 (TS MMA), separate W/B/A rings, 4-CTA clusters
+// with the activation tile multicast to both pairs (CL = 4 below, opt-in).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -88,7 +98,7 @@ struct PCfg {
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                        (static_cast<uint32_t>(BT >> 3) << 17) |
                                        (static_cast<uint32_t>(256 >> 4) << 24);
-    static_assert(BT == 128 || BT == 256, "BT");
+    static_assert(BT % 16 == 0 && BT >= 64 && BT <= 256, "BT: 2-SM MMA N granularity, 8-row swizzle atoms");
     static_assert(2 * BT <= kPTmemCols, "TMEM: two accumulator buffers");
     static_assert(kLoadBytes % 1024 == 0 && kBBytes % 1024 == 0, "swizzle atom alignment");
     static_assert(kSmemBytes <= 227 * 1024, "smem");
@@ -255,7 +265,10 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                 const int nt = 2 * np + static_cast<int>(rank);
                 const int tok0 = mt * BT + static_cast<int>(rank) * C::kHalfT;
                 const bool has_w = nt < p.n_tiles;
-                const bool has_b = tok0 < p.Mp;
+                // activation rows inside the a8 buffer (the last token tile may overhang Mp
+                // when BT does not divide it; the overhanging MMA columns are never stored)
+                const int brows = NP == 1 ? max(0, min(C::kHalfT, p.Mp - tok0)) : (tok0 < p.Mp ? C::kHalfT : 0);
+                const bool has_b = brows > 0;
                 const uint8_t* wsrc = p.wp + static_cast<size_t>(nt) * p.kblocks * kWBlockBytes;
                 const int8_t* bsrc = p.qa + static_cast<size_t>(tok0) * kBlockK;
                 for (int kb = 0; kb < p.kblocks; ++kb, ++u) {
@@ -267,14 +280,14 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                         mbar_arrive(&full[s]);
                         continue;
                     }
-                    mbar_expect_tx(&full[s], (has_w ? kWBlockBytes : 0) + (has_b ? C::kBBytes : 0));
+                    mbar_expect_tx(&full[s], (has_w ? kWBlockBytes : 0) + brows * kBlockK);
                     if (has_w)
                         bulk_g2s(st + C::kBBytes, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
                                  kWBlockBytes, &full[s], pol_w);
                     if (has_b) {
                         const int8_t* src = bsrc + static_cast<size_t>(kb) * p.Mp * kBlockK + pi * kSlice;
                         if (NP == 1)
-                            bulk_g2s(st, src, C::kBBytes, &full[s], pol_a);
+                            bulk_g2s(st, src, brows * kBlockK, &full[s], pol_a);
                         else
                             bulk_g2s_mc(st + pi * kSlice, src, kSlice, &full[s], peer_mask, pol_a);
                     }
@@ -287,12 +300,12 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             int u = 0, j = 0;
             for (int tile = cid; tile < p.tiles; tile += ncl, ++j) {
                 const int db = j & 1;
-                mbar_wait_cluster(&d_empty[db], ((j >> 1) & 1) ^ 1);
+                mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + db * BT;
                 for (int kb = 0; kb < p.kblocks; ++kb, ++u) {
                     const int s = u % LS, as = u % AS;
-                    mbar_wait_cluster(&ready[as], (u / AS) & 1);
+                    mbar_wait(&ready[as], (u / AS) & 1);
                     if (lane == 0) trk(p.trace, 3, u);
                     tc_fence_after();
                     const uint32_t ab = a_base + as * kATileBytes, bb = l_base + s * C::kLoadBytes;
@@ -559,6 +572,29 @@ bool prefill_eligible(int M, int N, int K) {
     return g_prefill_min_m > 0 && M >= g_prefill_min_m && N > 0 && K > 0;
 }
 
+// Token-tile width: the candidate minimising the modelled makespan, i.e. rounds of tiles
+// over the persistent CTA pairs times the per-tile cost.  The per-tile time is measured
+// to be nearly independent of BT (the k-block pipeline is latency-bound: BT 256 / 192 /
+// 160 tiles take 23 / 21 / 20 us at K = 5120), modelled as BT + 600 token-columns; so
+// the wide shapes keep BT = 256 and the N = 5120 shapes (20 pair tiles) take BT = 160,
+// whose 7 token tiles fill more of the 74 pairs.
+int pick_prefill_bt(int M, int pair_tiles) {
+    static const int kCand[] = {256, 224, 192, 176, 160, 128};
+    const int pairs = std::max(1, device_sm_count() / 2);
+    int best = 256;
+    double best_cost = 1e30;
+    for (int bt : kCand) {
+        const long long items = static_cast<long long>(pair_tiles) * ((M + bt - 1) / bt);
+        const long long rounds = (items + pairs - 1) / pairs;
+        const double cost = static_cast<double>(rounds) * (bt + 600);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = bt;
+        }
+    }
+    return best;
+}
+
 cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
     PParams p = {};
@@ -588,12 +624,18 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
     if (p.cw != 1 && p.cw != 2 && p.cw != 4) p.cw = 1;
     static const char* dbg_env = std::getenv("ODY_PREFILL_DBG");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
-    static const char* bt_env = std::getenv("ODY_PREFILL_BT");
-    const int bt = bt_env ? std::atoi(bt_env) : 256;
     static const char* cl_env = std::getenv("ODY_PREFILL_CL");
-    const int cl = cl_env ? std::atoi(cl_env) : 4;
-    if (bt == 128) return launch_prefill_bt<128, 2>(p, a.max_ctas, st);
-    return cl == 2 ? launch_prefill_bt<256, 2>(p, a.max_ctas, st) : launch_prefill_bt<256, 4>(p, a.max_ctas, st);
+    if (cl_env && std::atoi(cl_env) == 4) return launch_prefill_bt<256, 4>(p, a.max_ctas, st);
+    static const char* bt_env = std::getenv("ODY_PREFILL_BT");
+    const int bt = bt_env ? std::atoi(bt_env) : pick_prefill_bt(p.M, p.pair_tiles);
+    switch (bt) {
+        case 128: return launch_prefill_bt<128, 2>(p, a.max_ctas, st);
+        case 160: return launch_prefill_bt<160, 2>(p, a.max_ctas, st);
+        case 176: return launch_prefill_bt<176, 2>(p, a.max_ctas, st);
+        case 192: return launch_prefill_bt<192, 2>(p, a.max_ctas, st);
+        case 224: return launch_prefill_bt<224, 2>(p, a.max_ctas, st);
+        default: return launch_prefill_bt<256, 2>(p, a.max_ctas, st);
+    }
 }
 
 }  // namespace odyb200
