@@ -289,6 +289,7 @@ def run_b200(args):
         result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs,
                                            gemm_ws)
         result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
+        result["prefill"] = None if args.no_prefill else prefill_roofline(args, dev, layers, stream)
         result["e2e"] = e2e_c_abi(args, m)
         if not args.no_cpu:
             result["cpu_baseline"] = cpu_baseline(args, m)
@@ -383,6 +384,50 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
             "algorithmic_bytes_per_launch": {
                 nm: (gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k))
                 for nm, n, k in LAYERS}}
+
+
+INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 (datasheet); MEASURED_PEAKS.json has no INT8 figure
+
+
+def prefill_roofline(args, dev, layers, stream, m=1024):
+    """configs[2]: the LLaMA-13B layer GEMMs at prefill width M = 1024 -- INT8 tensor-pipe
+    bound.  Dominant kernel: w4a8_prefill_kernel (2-SM cta_group::2 FastGEMM) on
+    pre-quantized activations, timed with CUDA events over graph replays rotating the
+    weight copies; TOPS = 2*M*N*K / launch time, against the INT8 dense peak and against
+    2x the measured dense bf16 matmul throughput (the same tensor pipe at 1 byte/operand)."""
+    import torch
+    res = {}
+    tot_ops = tot_ms = 0.0
+    bf16 = None
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            bf16 = json.load(fh).get("bf16_tflops")
+    for li, (name, n, k) in enumerate(LAYERS):
+        x = (torch.randn((m, k), device="cuda") * 2).half()
+        a = dev.act_quant(x)
+        out = torch.empty((m, n), dtype=torch.float16, device="cuda")
+        gws = dev.Workspace.get(m, n, k, "cuda")
+        ws = [layers[c][li][1] for c in range(len(layers))]
+
+        def fn(ws=ws, a=a, out=out, gws=gws):
+            for w in ws:
+                dev.w4a8_gemm(a, w, out=out, stream=stream, workspace=gws)
+
+        ms = _graph_time(fn, stream, reps=10) / len(ws)
+        ops = 2.0 * m * n * k
+        tops = ops / (ms * 1e-3) / 1e12
+        res[name] = {"N": n, "K": k, "us": round(ms * 1e3, 2), "TOPS": round(tops, 1),
+                     "frac": round(tops / INT8_PEAK_TOPS, 3)}
+        tot_ops += ops
+        tot_ms += ms
+    tops = tot_ops / (tot_ms * 1e-3) / 1e12
+    return {"bound": "tensor", "M": m, "achieved": round(tops, 1), "peak": INT8_PEAK_TOPS, "unit": "TOP/s",
+            "frac": round(tops / INT8_PEAK_TOPS, 3),
+            "frac_of_2x_measured_bf16": round(tops / (2 * bf16), 3) if bf16 else None,
+            "kernel": "w4a8_prefill_kernel (2-SM tcgen05 kind::i8, 256 weight rows x BT tokens per CTA pair)",
+            "layer_us": round(tot_ms * 1e3, 1), "per_shape": res,
+            "traffic": "profiles/r1_prefill_ncu.md"}
 
 
 def decode_sweep(args, dev, layers, stream):
@@ -557,6 +602,7 @@ def main():
     ap.add_argument("--prefetch", type=int, default=1,
                     help="pass the next linear's weights as an L2 prefetch hint")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the M=1024 prefill GEMM roofline")
     ap.add_argument("--lowering", default="program", choices=list(LOWERINGS),
                     help="program: the layer's linears in ONE persistent launch; "
                          "decode: one cluster split-K kernel per linear (K1 fused per k-slice); "
