@@ -117,8 +117,7 @@ struct PParams {
     int pdl;
     int vec_out;  // output rows are 16-byte aligned (N * esz % 16 == 0, aligned base)
     unsigned long long* trace;  // diagnostics: CTAs 0/1, per k-block globaltimer (kTrK slots)
-    int cw;   // converter warps per k-block (1, 2 or 4)
-    int dbg;  // diagnostics (ODY_PREFILL_DBG bits): 1 no loads, 2 no widening, 4 no MMAs, 8 no stores
+    int dbg;  // diagnostics (ODY_PREFILL_DBG bits): 1 no loads, 4 no MMAs, 8 no stores
 };
 
 // ---------------------------------------------------------------- 2-SM PTX
@@ -236,7 +235,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], NP);  // every pair's MMAs released the stage
         }
-        for (int i = 0; i < AS; ++i) mbar_init(&ready[i], 2 * p.cw);  // both CTAs' converter warps
+        for (int i = 0; i < AS; ++i) mbar_init(&ready[i], 2);  // both CTAs' converter warp
         for (int i = 0; i < 2; ++i) {
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], 8);
@@ -324,35 +323,36 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             }
         }
     } else if (warp >= kPWarpConv0 && warp < kPWarpConv0 + kPConvWarps) {
-        // p.cw warps widen one k-block (128 rows).  Group g of the kPConvWarps / p.cw
-        // groups OWNS the stages s with s % groups == g and takes their k-blocks in
-        // order (so no waiter ever runs a phase ahead on a barrier), while the groups'
-        // per-k-block fence + cluster-arrive latencies overlap.
-        const int cw = p.cw, groups = kPConvWarps / cw, rows_per = 4 / cw;
-        const int g = (warp - kPWarpConv0) / cw, wi = (warp - kPWarpConv0) % cw;
+        // One warp widens one k-block (128 rows).  Warp g OWNS the stages s with
+        // s % kPConvWarps == g and takes their k-blocks in order (so no waiter ever runs a
+        // phase ahead on a barrier), while the warps' per-k-block widening + fence +
+        // cluster-arrive latencies overlap.
+        const int g = warp - kPWarpConv0;
         const uint32_t ready_leader = mapa_shared(smem_u32(ready), leader);
         const int total = ((p.tiles - cid + ncl - 1) / ncl) * p.kblocks;  // this pair's k-blocks
+        const uint32_t sw = static_cast<uint32_t>(lane & 7);  // == row & 7 for rows 32*rr + lane
         for (int u = 0; u < total; ++u) {
             const int s = u % LS, as = s;
-            if (s % groups != g) continue;
+            if (s % kPConvWarps != g) continue;
             mbar_wait(&full[s], (u / LS) & 1);
-            if (wi == 0 && lane == 0) trk(p.trace, 1, u);
-#pragma unroll 1
-            for (int rr = 0; rr < rows_per; ++rr) {
-                const int r = (wi * rows_per + rr) * 32 + lane;  // weight row of this CTA's tile
-                const uint32_t sw = static_cast<uint32_t>(r & 7);
-                const uint32_t src = l_base + s * C::kLoadBytes + C::kBBytes + r * 16;
-                uint4 v[4];
+            if (lane == 0) trk(p.trace, 1, u);
+            const uint32_t src = l_base + s * C::kLoadBytes + C::kBBytes + lane * 16;
+            uint4 v[4][4];  // all 16 loads in flight before the first widening
 #pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] = lds128(src + c * 2048);
-                const uint32_t dst = a_base + as * kATileBytes + r * 128;
+            for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-                for (int c = 0; c < (p.dbg & 2 ? 0 : 4); ++c) {
+                for (int c = 0; c < 4; ++c) v[rr][c] = lds128(src + rr * 512 + c * 2048);
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const uint32_t dst = a_base + as * kATileBytes + (rr * 32 + lane) * 128;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
                     // word j of the row chunk: k = 32c+8j+0..3 low nibbles, +4..7 high nibbles
-                    const uint4 lo = make_uint4((v[c].x << 4) & 0xF0F0F0F0u, v[c].x & 0xF0F0F0F0u,
-                                                (v[c].y << 4) & 0xF0F0F0F0u, v[c].y & 0xF0F0F0F0u);
-                    const uint4 hi = make_uint4((v[c].z << 4) & 0xF0F0F0F0u, v[c].z & 0xF0F0F0F0u,
-                                                (v[c].w << 4) & 0xF0F0F0F0u, v[c].w & 0xF0F0F0F0u);
+                    const uint4 w = v[rr][c];
+                    const uint4 lo = make_uint4((w.x << 4) & 0xF0F0F0F0u, w.x & 0xF0F0F0F0u,
+                                                (w.y << 4) & 0xF0F0F0F0u, w.y & 0xF0F0F0F0u);
+                    const uint4 hi = make_uint4((w.z << 4) & 0xF0F0F0F0u, w.z & 0xF0F0F0F0u,
+                                                (w.w << 4) & 0xF0F0F0F0u, w.w & 0xF0F0F0F0u);
                     sts128(dst + (((2 * c) ^ sw) << 4), lo);      // k 32c .. 32c+15
                     sts128(dst + (((2 * c + 1) ^ sw) << 4), hi);  // k 32c+16 .. 32c+31
                 }
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             fence_proxy_async_shared();  // generic smem writes -> tensor-core reads
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ready_leader + as * 8);
-            if (wi == 0 && lane == 0) trk(p.trace, 2, u);
+            if (lane == 0) trk(p.trace, 2, u);
         }
     } else if (warp >= kPWarpEpi0) {
         const int q = warp & 3;
@@ -619,9 +619,6 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
         const void* o = a.acc_out ? static_cast<const void*>(a.acc_out) : a.out;
         p.vec_out = ((static_cast<size_t>(a.N) * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) ? 1 : 0;
     }
-    static const char* cw_env = std::getenv("ODY_PREFILL_CW");
-    p.cw = cw_env ? std::atoi(cw_env) : 1;
-    if (p.cw != 1 && p.cw != 2 && p.cw != 4) p.cw = 1;
     static const char* dbg_env = std::getenv("ODY_PREFILL_DBG");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
     static const char* cl_env = std::getenv("ODY_PREFILL_CL");
