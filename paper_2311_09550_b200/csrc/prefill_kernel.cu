@@ -88,11 +88,14 @@ struct PCfg {
     // one ring; a stage = [B half tile | packed W block] (landed by the producer) + the
     // widened A tile (written by the converter group that owns the stage), all released
     // together by the MMA commit
-    static constexpr int kLoadBytes = kBBytes + kWBlockBytes;
-    static constexpr int kLoadStages = (216 * 1024 - kOutStageBytes) / (kLoadBytes + kATileBytes);
+    // stage = [B half tile | A tile]; the producer lands the packed W block in the first
+    // 8 KiB of the A tile and the converter warp, holding all of W in registers, widens it
+    // in place -- so a stage costs kBBytes + 16 KiB, not + 24 KiB
+    static constexpr int kLoadBytes = kBBytes + kATileBytes;
+    static constexpr int kLoadStages = (216 * 1024 - kOutStageBytes) / kLoadBytes;
     static constexpr int kAStages = kLoadStages;
     static constexpr int kScaleBytes = 2 * BT * 4;         // per-token scales, per D buffer
-    static constexpr int kSmemBytes = kAStages * kATileBytes + kLoadStages * kLoadBytes + kOutStageBytes +
+    static constexpr int kSmemBytes = kLoadStages * kLoadBytes + kOutStageBytes +
                                       kScaleBytes + 1024 + 1024;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BT, M=256 (2 CTAs)
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
@@ -204,8 +207,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    uint8_t* aring = smem;                                   // [AS][16 KiB]
-    uint8_t* lring = aring + AS * kATileBytes;               // [LS][B | W]
+    uint8_t* lring = smem;                                   // [LS][B | W -> A]
     uint8_t* ostage = lring + LS * C::kLoadBytes;            // epilogue staging
     float* sbuf = reinterpret_cast<float*>(ostage + kOutStageBytes);  // [2][BT]
     uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + kOutStageBytes + C::kScaleBytes);
@@ -215,7 +217,8 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
     uint64_t* d_full = ready + AS;        // [2] MMA commit (multicast)
     uint64_t* d_empty = d_full + 2;       // [2] leader: both CTAs' epilogue warps (count 8)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-    const uint32_t a_base = smem_u32(aring), l_base = smem_u32(lring);
+    const uint32_t l_base = smem_u32(lring);
+    const uint32_t a_base = l_base + C::kBBytes;  // A tile of stage s at a_base + s * kLoadBytes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                     mbar_wait(&ready[as], (u / AS) & 1);
                     if (lane == 0) trk(p.trace, 3, u);
                     tc_fence_after();
-                    const uint32_t ab = a_base + as * kATileBytes, bb = l_base + s * C::kLoadBytes;
+                    const uint32_t ab = a_base + as * C::kLoadBytes, bb = l_base + s * C::kLoadBytes;
                     if (elect_one()) {
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
@@ -342,9 +345,10 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) v[rr][c] = lds128(src + rr * 512 + c * 2048);
+            __syncwarp();  // every lane has read W before any lane overwrites it with A
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
-                const uint32_t dst = a_base + as * kATileBytes + (rr * 32 + lane) * 128;
+                const uint32_t dst = a_base + as * C::kLoadBytes + (rr * 32 + lane) * 128;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     // word j of the row chunk: k = 32c+8j+0..3 low nibbles, +4..7 high nibbles
