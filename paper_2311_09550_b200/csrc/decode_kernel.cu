@@ -1125,7 +1125,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             if (it < 0) break;
             const DynItem x = dyn_item(p, it);
             for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
-                if (U % kDynConvGroups != grp) continue;  // the other group widens this unit
+                // the group owning ring stage U % kDynStages widens this unit (stage
+                // ownership keeps every w_full waiter in phase order on odd-length rings)
+                if ((U % kDynStages) % kDynConvGroups != grp) continue;
                 const int nb = min(kUnitBlocks, x.kb_hi - kb);
                 const int s = U % kDynStages;
                 const int as = U % kAStages;

@@ -647,7 +647,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) w4a8_gemm_kernel(const Params 
         int u = 0;
         while (it.next(p)) {
             for (int kb = it.kb0; kb < it.kb1; kb += kUnitBlocks, ++u) {
-                if ((u % kConvGroups) != g) continue;
+                // a group owns the ring STAGES s with s % kConvGroups == g: alternating units
+                // over an odd-length ring let a group wait on w_full one phase ahead (an
+                // mbarrier parity wait then passes on the previous phase and widens stale
+                // weights -- seen as whole wrong tiles at BN = 64, 3 stages)
+                if (((u % C::kStages) % kConvGroups) != g) continue;
                 const int nb = min(kUnitBlocks, it.kb1 - kb);
                 const int s = u % C::kStages;
                 const int as = u % kAStages;

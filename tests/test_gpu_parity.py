@@ -345,3 +345,19 @@ def test_fused_linear_input_dtypes(linear_mode, oracle, torch_cuda, dev):
         want = oracle.fast_gemm(codes, sa, flat, sw, m, n, k, threads=THREADS)
         got = dev.w4a8_linear(x, wq, torch.float16)
         assert torch.equal(got.cpu(), torch.from_numpy(want).to(torch.float16))
+
+
+@pytest.mark.parametrize("m", [24, 48, 64])
+def test_repeated_gemm_is_deterministic(m, torch_cuda, dev):
+    """Regression for a converter-ring race: two converter groups alternating units over
+    an odd-length stage ring could wait one mbarrier phase ahead, pass on the previous
+    phase and widen stale weights (whole wrong 128-row tiles, ~1 run in 20 at BN = 64).
+    Groups now own ring stages; 40 repeats of each shape must be bit-identical."""
+    torch = torch_cuda
+    for n, k in ((27648, 5120), (5120, 13824)):
+        x = torch.randn((m, k), device="cuda").half()
+        w = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.05)
+        aq = dev.act_quant(x)
+        base = dev.w4a8_gemm(aq, w, accumulators=True)
+        for _ in range(40):
+            assert torch.equal(dev.w4a8_gemm(aq, w, accumulators=True), base)
