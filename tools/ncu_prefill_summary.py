@@ -84,10 +84,11 @@ def main():
                   f"{float(r['lts__throughput.avg.pct_of_peak_sustained_elapsed']):.1f} | "
                   f"{float(r['smsp__issue_active.avg.pct_of_peak_sustained_active']):.1f} | "
                   f"{mb('dram__bytes_read.sum'):.1f} | {mb('dram__bytes_write.sum'):.1f} |")
-    md += ["", "Reading: no unit is saturated (tensor pipe < 50%, L2 and L1 well below peak, DRAM "
-           "~ the weights once + the fp16 output) -- the per-k-block pipeline (bulk-copy latency, "
-           "INT4 widening into the smem A tile, fence.proxy.async + cross-CTA arrive, 5 stages of "
-           "40 KiB) is latency-bound. DESIGN.md section 4.5 lists the variants measured.", ""]
+    md += ["", "Reading: no unit is saturated (tensor pipe <= 57% of the cycles at the clock ncu saw, "
+           "1.72-1.81 GHz; L2 and L1 well below peak; DRAM ~ the weights once + the fp16 output) -- the "
+           "per-k-block pipeline (bulk-copy latency, INT4 widening in place in the smem A tile, "
+           "fence.proxy.async + cross-CTA arrive, 6-7 stages of B half tile + A tile) is latency-bound. "
+           "DESIGN.md section 4.5 lists the variants measured.", ""]
     ls = launches(a.launches)
     if ls:
         md += ["## Launch list (`ncu --metrics gpu__time_duration.sum`, same command)", "",
