@@ -120,6 +120,7 @@ struct PParams {
     int pdl;
     int vec_out;  // output rows are 16-byte aligned (N * esz % 16 == 0, aligned base)
     unsigned long long* trace;  // diagnostics: CTAs 0/1, per k-block globaltimer (kTrK slots)
+    int wreg;  // 1: converter warps load W straight into registers (no smem pass for W)
     int dbg;  // diagnostics (ODY_PREFILL_DBG bits): 1 no loads, 4 no MMAs, 8 no stores
 };
 
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
                         mbar_arrive(&full[s]);
                         continue;
                     }
-                    mbar_expect_tx(&full[s], (has_w ? kWBlockBytes : 0) + brows * kBlockK);
-                    if (has_w)
+                    const bool tma_w = has_w && !p.wreg;
+                    mbar_expect_tx(&full[s], (tma_w ? kWBlockBytes : 0) + brows * kBlockK);
+                    if (tma_w)
                         bulk_g2s(st + C::kBBytes, wsrc + static_cast<size_t>(kb) * kWBlockBytes,
                                  kWBlockBytes, &full[s], pol_w);
                     if (has_b) {
@@ -334,6 +336,60 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
         const uint32_t ready_leader = mapa_shared(smem_u32(ready), leader);
         const int total = ((p.tiles - cid + ncl - 1) / ncl) * p.kblocks;  // this pair's k-blocks
         const uint32_t sw = static_cast<uint32_t>(lane & 7);  // == row & 7 for rows 32*rr + lane
+        if (p.wreg) {
+            // W straight from global (L2) into registers, one k-block ahead: W never passes
+            // through shared memory, which the bulk copies, the widened A tiles and the MMA
+            // operand reads otherwise share (~80 KiB of smem traffic per k-block -> ~64).
+            // Warp g owns stage g (LS <= kPConvWarps) and its k-blocks g, g+LS, ...
+            const int g0 = g;
+            auto load_w = [&](int u, uint4 (&v)[4][4]) {
+                const int ti = u / p.kblocks, kb = u - ti * p.kblocks;
+                const int tile = cid + ti * ncl;
+                const int nt = 2 * ((tile / p.m_tiles) * NP + pi) + static_cast<int>(rank);
+                if (nt >= p.n_tiles) {
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) v[rr][c] = make_uint4(0, 0, 0, 0);
+                    return;
+                }
+                const uint4* src = reinterpret_cast<const uint4*>(
+                                       p.wp + (static_cast<size_t>(nt) * p.kblocks + kb) * kWBlockBytes) + lane;
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[rr][c] = __ldg(src + c * 128 + rr * 32);
+            };
+            if (g0 < LS && g0 < total) {
+                uint4 v[4][4];
+                load_w(g0, v);
+                for (int u = g0; u < total; u += LS) {
+                    const int s = g0, as = s;
+                    mbar_wait(&empty[s], ((u / LS) & 1) ^ 1);  // A tile free: MMA of u - LS done
+                    if (lane == 0) trk(p.trace, 1, u);
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr) {
+                        const uint32_t dst = a_base + as * C::kLoadBytes + (rr * 32 + lane) * 128;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 w = v[rr][c];
+                            const uint4 lo = make_uint4((w.x << 4) & 0xF0F0F0F0u, w.x & 0xF0F0F0F0u,
+                                                        (w.y << 4) & 0xF0F0F0F0u, w.y & 0xF0F0F0F0u);
+                            const uint4 hi = make_uint4((w.z << 4) & 0xF0F0F0F0u, w.z & 0xF0F0F0F0u,
+                                                        (w.w << 4) & 0xF0F0F0F0u, w.w & 0xF0F0F0F0u);
+                            sts128(dst + (((2 * c) ^ sw) << 4), lo);      // k 32c .. 32c+15
+                            sts128(dst + (((2 * c + 1) ^ sw) << 4), hi);  // k 32c+16 .. 32c+31
+                        }
+                    }
+                    fence_proxy_async_shared();  // generic smem writes -> tensor-core reads
+                    mbar_wait(&full[s], (u / LS) & 1);  // this CTA's B landed (the leader's MMA reads it)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(ready_leader + as * 8);
+                    if (lane == 0) trk(p.trace, 2, u);
+                    if (u + LS < total) load_w(u + LS, v);
+                }
+            }
+        } else
         for (int u = 0; u < total; ++u) {
             const int s = u % LS, as = s;
             if (s % kPConvWarps != g) continue;
@@ -623,6 +679,8 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
         const void* o = a.acc_out ? static_cast<const void*>(a.acc_out) : a.out;
         p.vec_out = ((static_cast<size_t>(a.N) * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) ? 1 : 0;
     }
+    static const char* wreg_env = std::getenv("ODY_PREFILL_WREG");
+    p.wreg = wreg_env ? std::atoi(wreg_env) : 1;
     static const char* dbg_env = std::getenv("ODY_PREFILL_DBG");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
     static const char* cl_env = std::getenv("ODY_PREFILL_CL");
