@@ -13,15 +13,16 @@
 // per 512 MMA cycles per SM at BT = 256 -- and each weight k-block is widened once per
 // 256 tokens instead of once per 128.
 //
-//   * producer (warp 0, each CTA): 1-D bulk copies of the CTA's 8 KiB weight block and
-//     its half activation k-block into an S-stage ring (one mbarrier per stage);
-//   * converters (warps 4..11, each CTA): one warp widens one k-block (128 rows) with the
-//     paper's high-nibble trick ((w<<4)&0xF0F0F0F0, w&0xF0F0F0F0 -> value*16, no scale
-//     multiply) into the stage's A tile (SWIZZLE_128B K-major canonical layout), then
-//     fence.proxy.async and a cluster-scope arrive on the LEADER's ready[s].  Warp g owns
-//     the stages s with s % 8 == g, so the groups' widening + fence + arrive latencies
-//     (~1.3 us per k-block, tools/prefill_trace.py) overlap and every barrier has one
-//     in-order waiter;
+//   * producer (warp 0, each CTA): 1-D bulk copies of the CTA's half activation k-block
+//     into an S-stage ring; a stage is [B half tile | A tile];
+//   * converters (warps 4..11, each CTA): warp g owns stage g.  It loads the 8 KiB INT4
+//     block of its next k-block straight from L2 into registers (one k-block ahead: W
+//     never passes through shared memory, whose bandwidth the bulk copies, the A tiles and
+//     the MMA operand reads share), widens it with the paper's high-nibble trick
+//     ((w<<4)&0xF0F0F0F0, w&0xF0F0F0F0 -> value*16, no scale multiply) into the stage's A
+//     tile (SWIZZLE_128B K-major canonical layout), fence.proxy.async, and after its CTA's
+//     B landed arrives (cluster scope) on the LEADER's ready[s].  Stage ownership keeps
+//     every barrier's waiter single and in order while the warps' latencies overlap;
 //   * MMA (warp 1 of the leader CTA only): tcgen05.mma.cta_group::2.kind::i8, M=256
 //     (both CTAs' weight rows), N=BT (both CTAs' token halves), K=32, accumulators in a
 //     double-buffered TMEM tile; commits multicast to both CTAs' stage / tile barriers;
@@ -33,12 +34,12 @@
 // token tile fastest, so the clusters in flight read each weight tile at about the same
 // time (L2 hits) and the whole activation matrix stays L2-resident (evict_last).
 //
-// Measured (B200, M = 1024, LLaMA-13B shapes): 0.26-0.48 of the 4.5 POPS INT8 dense
-// peak; ncu: tensor pipe 39-49% active, L2 20-25% and shared memory well below their
-// peaks -- the k-block pipeline is latency-bound (load ~0.5 us + widening ~1.3 us +
-// signalling, over 5 stages of 40 KiB).  Explored and rejected (slower, kept in git
-// history): A in TMEM with BT = 192/208 (TS MMA), separate W/B/A rings, 4-CTA clusters
-// with the activation tile multicast to both pairs (CL = 4 below, opt-in).
+// Measured (B200, M = 1024, LLaMA-13B shapes): 0.36-0.64 of the 4.5 POPS INT8 dense
+// peak (layer 276 us); the k-block pipeline is bound by shared-memory traffic (~64 KiB
+// per k-block per SM: B bulk-copy write + A tile write + both MMA operand reads) and by
+// the stage round trip.  Explored and rejected: A in TMEM (TS MMA),
+// separate W/B/A rings, two warps per k-block, register-direct epilogue stores, 4-CTA
+// clusters with the activation tile multicast to both pairs (CL = 4 below, opt-in).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
