@@ -15,7 +15,7 @@ raise :class:`OdyError` with the same status the reference ABI returns.
 """
 from __future__ import annotations
 
-from ctypes import POINTER, byref, c_float, c_size_t, c_void_p
+from ctypes import POINTER, byref, c_float, c_size_t, c_void_p, cast
 
 import numpy as np
 
@@ -51,13 +51,20 @@ class Tensor:
         check(lib().ody_tensor_dims(self._h, byref(r), byref(c)))
         return (r.value, c.value)
 
-    def numpy(self) -> np.ndarray:
+    def numpy(self, copy: bool = True) -> np.ndarray:
+        """The tensor's data.  copy=False returns a zero-copy view of the (pinned) buffer
+        that ody_tensor_data borrows (odyssey.h:68-69); the view keeps this Tensor -- and so
+        the buffer -- alive for as long as it exists."""
         rows, cols = self.shape
         p = POINTER(c_float)()
         check(lib().ody_tensor_data(self._h, byref(p)))
         if rows * cols == 0:
             return np.zeros((rows, cols), np.float32)
-        return np.ctypeslib.as_array(p, shape=(rows, cols)).copy()
+        if copy:
+            return np.ctypeslib.as_array(p, shape=(rows, cols)).copy()
+        buf = (c_float * (rows * cols)).from_address(cast(p, c_void_p).value)
+        buf._owner = self  # the view's base holds the handle
+        return np.frombuffer(buf, dtype=np.float32).reshape(rows, cols)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -136,7 +143,7 @@ def run_engine(engine: int, a_dense, a_q: QTensor | None, w_q: QTensor, with_cou
     h = c_void_p()
     check(lib().ody_gemm(engine, dense._h if dense else None, a_q._h if a_q else None, w_q._h,
                          byref(counters), byref(h)))
-    out = Tensor(None, _handle=h).numpy()
+    out = Tensor(None, _handle=h).numpy(copy=False)  # the result buffer itself, no extra copy
     if with_counters:
         return out, {f: getattr(counters, f) for f, _ in ody_gemm_counters._fields_}
     return out
