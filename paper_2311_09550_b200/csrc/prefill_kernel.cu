@@ -118,6 +118,8 @@ struct PParams {
     int out_dtype;
     int M, N, K, Mp;
     int kblocks, n_tiles, pair_tiles, m_tiles, tiles;
+    int split_r;  // the last split_r tiles run as 2 half-width items each (filling the final round)
+    int items;    // tiles + split_r
     int pdl;
     int vec_out;  // output rows are 16-byte aligned (N * esz % 16 == 0, aligned base)
     unsigned long long* trace;  // diagnostics: CTAs 0/1, per k-block globaltimer (kTrK slots)
@@ -200,6 +202,22 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
 // CL = CTAs per cluster: 2 (one pair) or 4 (two pairs on adjacent weight tiles, same
 // tokens): each CTA then bulk-loads 1/(CL/2) of its activation half tile and multicasts
 // it to the same-rank CTA of every pair, cutting the per-SM L2 read bytes.
+// A work item: a whole (pair n-tile, token tile), or -- for the last split_r tiles, so
+// the final round of the persistent grid is not left mostly idle -- one token half of it.
+struct PItem {
+    int tile;  // cluster tile index: np-major, token tile fastest
+    int t0;    // first token
+    int bt;    // tokens (MMA N)
+};
+template <int BT>
+__device__ __forceinline__ PItem prefill_item(const PParams& p, int it) {
+    const int full = p.tiles - p.split_r;
+    if (it < full) return {it, (it % p.m_tiles) * BT, BT};
+    const int h = it - full;
+    const int tile = full + (h >> 1);
+    return {tile, (tile % p.m_tiles) * BT + (h & 1) * (BT / 2), BT / 2};
+}
+
 template <int BT, int CL>
 __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParams p) {
     using C = PCfg<BT>;
@@ -264,14 +282,16 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             if (p.pdl) pdl_wait();  // activations come from the previous kernel
             int u = 0;
             constexpr int kSlice = C::kBBytes / NP;  // this CTA's multicast share of B
-            for (int tile = cid; tile < p.tiles; tile += ncl) {
-                const int np = (tile / p.m_tiles) * NP + pi, mt = tile % p.m_tiles;
+            for (int itx = cid; itx < p.items; itx += ncl) {
+                const PItem im = prefill_item<BT>(p, itx);
+                const int np = (im.tile / p.m_tiles) * NP + pi;
                 const int nt = 2 * np + static_cast<int>(rank);
-                const int tok0 = mt * BT + static_cast<int>(rank) * C::kHalfT;
+                const int half_t = im.bt / 2;  // tokens of B this CTA stages
+                const int tok0 = im.t0 + static_cast<int>(rank) * half_t;
                 const bool has_w = nt < p.n_tiles;
                 // activation rows inside the a8 buffer (the last token tile may overhang Mp
                 // when BT does not divide it; the overhanging MMA columns are never stored)
-                const int brows = NP == 1 ? max(0, min(C::kHalfT, p.Mp - tok0)) : (tok0 < p.Mp ? C::kHalfT : 0);
+                const int brows = NP == 1 ? max(0, min(half_t, p.Mp - tok0)) : (tok0 < p.Mp ? half_t : 0);
                 const bool has_b = brows > 0;
                 const uint8_t* wsrc = p.wp + static_cast<size_t>(nt) * p.kblocks * kWBlockBytes;
                 const int8_t* bsrc = p.qa + static_cast<size_t>(tok0) * kBlockK;
@@ -303,7 +323,10 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
         if (rank == 0) {
             const uint16_t all_mask = kAllMask;
             int u = 0, j = 0;
-            for (int tile = cid; tile < p.tiles; tile += ncl, ++j) {
+            for (int itx = cid; itx < p.items; itx += ncl, ++j) {
+                const PItem im = prefill_item<BT>(p, itx);
+                // MMA N = the item's token count (instruction-descriptor bits 17..22)
+                const uint32_t idesc = (C::kIdesc & ~(0x3Fu << 17)) | (static_cast<uint32_t>(im.bt >> 3) << 17);
                 const int db = j & 1;
                 mbar_wait(&d_empty[db], ((j >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -318,7 +341,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
                             if (!(p.dbg & 4))
-                                mma2_i8_ss(d_tmem, sw128_desc(ab + 32 * c), sw128_desc(bb + 32 * c), C::kIdesc,
+                                mma2_i8_ss(d_tmem, sw128_desc(ab + 32 * c), sw128_desc(bb + 32 * c), idesc,
                                            (kb > 0 || c > 0) ? 1u : 0u);
                         mma2_commit_mc(&empty[s], all_mask);  // B slices came from every pair
                     }
@@ -335,7 +358,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
         // cluster-arrive latencies overlap.
         const int g = warp - kPWarpConv0;
         const uint32_t ready_leader = mapa_shared(smem_u32(ready), leader);
-        const int total = ((p.tiles - cid + ncl - 1) / ncl) * p.kblocks;  // this pair's k-blocks
+        const int total = ((p.items - cid + ncl - 1) / ncl) * p.kblocks;  // this pair's k-blocks
         const uint32_t sw = static_cast<uint32_t>(lane & 7);  // == row & 7 for rows 32*rr + lane
         if (p.wreg) {
             // W straight from global (L2) into registers, one k-block ahead: W never passes
@@ -345,7 +368,7 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
             const int g0 = g;
             auto load_w = [&](int u, uint4 (&v)[4][4]) {
                 const int ti = u / p.kblocks, kb = u - ti * p.kblocks;
-                const int tile = cid + ti * ncl;
+                const int tile = prefill_item<BT>(p, cid + ti * ncl).tile;
                 const int nt = 2 * ((tile / p.m_tiles) * NP + pi) + static_cast<int>(rank);
                 if (nt >= p.n_tiles) {
 #pragma unroll
@@ -432,25 +455,26 @@ __global__ void __launch_bounds__(kPThreads, 1) w4a8_prefill_kernel(const PParam
         const uint32_t ob = smem_u32(ostage);
         if (p.pdl) pdl_wait();
         int j = 0;
-        for (int tile = cid; tile < p.tiles; tile += ncl, ++j) {
+        for (int itx = cid; itx < p.items; itx += ncl, ++j) {
+            const PItem im = prefill_item<BT>(p, itx);
             const int db = j & 1;
-            const int np = (tile / p.m_tiles) * NP + pi, mt = tile % p.m_tiles;
+            const int np = (im.tile / p.m_tiles) * NP + pi;
             const int n0 = (2 * np + static_cast<int>(rank)) * kTileN;
             const int n = n0 + r;
-            const int t0 = mt * BT;
+            const int t0 = im.t0;
             const float sw_n = n < p.N ? __ldg(p.sw + n) : 0.0f;
             float* sc = sbuf + db * BT;
-            for (int i = r; i < BT; i += 128) sc[i] = t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f;
+            for (int i = r; i < im.bt; i += 128) sc[i] = t0 + i < p.M ? __ldg(p.sa + t0 + i) : 0.0f;
             named_bar_sync(1, 128);
             mbar_wait(&d_full[db], (j >> 1) & 1);
             if (r == 0) tre(p.trace, 0, j);
             tc_fence_after();
-            const int tn = min(BT, p.M - t0);  // valid tokens of this tile
+            const int tn = min(im.bt, p.M - t0);  // valid tokens of this item
             const int nn = min(kTileN, p.N - n0);  // valid weight rows (may be <= 0)
             // 16-byte pieces per staged token row
             const int per_row = kTileN * esz / 16;
 #pragma unroll 1
-            for (int tc = 0; tc < BT; tc += kEpiTok) {
+            for (int tc = 0; tc < im.bt; tc += kEpiTok) {
                 uint32_t v[32];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: the whole warp, converged
                 const bool ptr = j == 0 && r == 0;
@@ -597,10 +621,19 @@ cudaError_t launch_prefill_bt(PParams p, int max_ctas, cudaStream_t st) {
     int clusters = prefill_max_clusters<BT, CL>();
     if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / CL));
     clusters = std::min(clusters, p.tiles);
+    // a final round with few tiles: split each of them into two token halves when the
+    // halves still fit one round (BT/2 keeps the 2-SM N and swizzle-row granularity)
+    {
+        const int r = p.tiles % clusters;
+        p.split_r = (CL == 2 && BT % 32 == 0 && r > 0 && 2 * r <= clusters && p.tiles > clusters) ? r : 0;
+        static const char* nosplit = std::getenv("ODY_PREFILL_NOSPLIT");
+        if (nosplit && std::atoi(nosplit)) p.split_r = 0;
+        p.items = p.tiles + p.split_r;
+    }
     static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
     if (plan_log)
-        std::fprintf(stderr, "[ody] prefill %dx%dx%d: BT %d CL %d tiles %d clusters %d stages %d\n", p.M, p.N, p.K,
-                     BT, CL, p.tiles, clusters, PCfg<BT>::kLoadStages);
+        std::fprintf(stderr, "[ody] prefill %dx%dx%d: BT %d CL %d tiles %d (+%d split) clusters %d stages %d\n", p.M,
+                     p.N, p.K, BT, CL, p.tiles, p.split_r, clusters, PCfg<BT>::kLoadStages);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * clusters);
     cfg.blockDim = dim3(kPThreads);
@@ -633,21 +666,22 @@ bool prefill_eligible(int M, int N, int K) {
     return g_prefill_min_m > 0 && M >= g_prefill_min_m && N > 0 && K > 0;
 }
 
-// Token-tile width: the candidate minimising the modelled makespan, i.e. rounds of tiles
-// over the persistent CTA pairs times the per-tile cost.  The per-tile time is measured
-// to be nearly independent of BT (the k-block pipeline is latency-bound: BT 256 / 192 /
-// 160 tiles take 23 / 21 / 20 us at K = 5120), modelled as BT + 600 token-columns; so
-// the wide shapes keep BT = 256 and the N = 5120 shapes (20 pair tiles) take BT = 160,
-// whose 7 token tiles fill more of the 74 pairs.
+// Token-tile width: the candidate minimising the modelled makespan -- rounds of items
+// over the persistent CTA pairs (a final round of half-width split items counted as 0.6)
+// times a per-item cost of BT + 60 token-columns (fitted to the measured M = 1024 LLaMA
+// shapes: BT 256 for qkv / gate_up, 160 for the N = 5120 shapes, whose 20 pair tiles
+// leave a BT = 256 grid mostly idle in its second round).
 int pick_prefill_bt(int M, int pair_tiles) {
     static const int kCand[] = {256, 224, 192, 176, 160, 128};
     const int pairs = std::max(1, device_sm_count() / 2);
     int best = 256;
     double best_cost = 1e30;
     for (int bt : kCand) {
-        const long long items = static_cast<long long>(pair_tiles) * ((M + bt - 1) / bt);
-        const long long rounds = (items + pairs - 1) / pairs;
-        const double cost = static_cast<double>(rounds) * (bt + 600);
+        const long long tiles = static_cast<long long>(pair_tiles) * ((M + bt - 1) / bt);
+        const long long r = tiles % pairs;
+        const bool split = bt % 32 == 0 && r > 0 && 2 * r <= pairs && tiles > pairs;  // as the launcher
+        const double rounds = static_cast<double>(tiles / pairs) + (r == 0 ? 0.0 : (split ? 0.6 : 1.0));
+        const double cost = rounds * (bt + 60);
         if (cost < best_cost * 0.999) {
             best_cost = cost;
             best = bt;
