@@ -84,10 +84,11 @@ def main():
                   f"{float(r['lts__throughput.avg.pct_of_peak_sustained_elapsed']):.1f} | "
                   f"{float(r['smsp__issue_active.avg.pct_of_peak_sustained_active']):.1f} | "
                   f"{mb('dram__bytes_read.sum'):.1f} | {mb('dram__bytes_write.sum'):.1f} |")
-    md += ["", "Reading: no unit is saturated (tensor pipe <= 57% of the cycles at the clock ncu saw, "
-           "1.72-1.81 GHz; L2 and L1 well below peak; DRAM ~ the weights once + the fp16 output) -- the "
-           "per-k-block pipeline (bulk-copy latency, INT4 widening in place in the smem A tile, "
-           "fence.proxy.async + cross-CTA arrive, 6-7 stages of B half tile + A tile) is latency-bound. "
+    md += ["", "Reading: no unit is saturated (tensor pipe <= 66% of the cycles at the clock ncu saw, "
+           "1.67-1.81 GHz under this power draw; L2 and L1 well below peak; DRAM ~ the weights once + the fp16 output) -- the "
+           "per-k-block pipeline is bound by shared-memory traffic (B bulk-copy write + widened A tile "
+           "write + both MMA operand reads, ~64 KiB per k-block per SM; W comes from L2 straight into "
+           "the converter warps' registers) and the stage round trip. "
            "DESIGN.md section 4.5 lists the variants measured.", ""]
     ls = launches(a.launches)
     if ls:
