@@ -207,7 +207,7 @@ int ody_dev_linear_is_fused(size_t m, size_t n, size_t k); /* 1: single fused ke
  * cluster split-K decode kernel (K1 per k-slice + K3 + K4 in one launch) where eligible
  * (m <= 16, 16-bit x), else 0. */
 void ody_dev_set_linear_mode(int mode);
-/* FastGEMM kernel choice by width: m >= min_m (default 256; env ODY_PREFILL) runs the
+/* FastGEMM kernel choice by width: m >= min_m (default 65; env ODY_PREFILL) runs the
  * 2-SM cta_group::2 prefill kernel (256 weight rows x 256 tokens per CTA pair), smaller m
  * the 1-SM tile GEMM.  0 disables the prefill kernel.  Results are identical either way. */
 void ody_dev_set_prefill_min_m(int min_m);

@@ -58,7 +58,7 @@ struct GemmArgs {
 };
 size_t gemm_workspace_bytes(int M, int N, int K, int num_sms);
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st);
-// Prefill widths (M >= 256, or ODY_PREFILL=<min M>; ODY_PREFILL=0 disables): the 2-SM
+// Prefill widths (M >= 65, or ODY_PREFILL=<min M>; ODY_PREFILL=0 disables): the 2-SM
 // cta_group::2 FastGEMM (prefill_kernel.cu).  launch_w4a8_gemm dispatches to it.
 bool prefill_eligible(int M, int N, int K);
 void set_prefill_min_m(int m);  // 0 disables

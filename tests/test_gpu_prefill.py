@@ -24,7 +24,7 @@ def torch_cuda():
 @pytest.fixture(scope="module")
 def dev():
     from paper_2311_09550_b200 import device
-    device.lib().ody_dev_set_prefill_min_m(256)
+    device.lib().ody_dev_set_prefill_min_m(65)
     return device
 
 
@@ -39,7 +39,8 @@ def _oracle_case(oracle, m, n, k, seed):
 
 # ragged shapes: odd 128-row tile counts (a pair's second CTA has no weights), token
 # counts that leave a half or whole empty 128-token half tile, K not a multiple of 128
-@pytest.mark.parametrize("m,n,k", [(256, 128, 128), (300, 384, 1000), (384, 200, 640),
+@pytest.mark.parametrize("m,n,k", [(65, 256, 384), (100, 640, 520), (128, 384, 1024), (200, 1000, 640),
+                                   (256, 128, 128), (300, 384, 1000), (384, 200, 640),
                                    (640, 1000, 2048), (1024, 640, 520), (1537, 256, 384)])
 def test_prefill_vs_oracle(m, n, k, oracle, torch_cuda, dev):
     torch = torch_cuda
@@ -71,7 +72,7 @@ def test_prefill_llama_equals_tile_gemm(layer, n, k, torch_cuda, dev):
         acc_ref = dev.w4a8_gemm(aq, wq, accumulators=True)
         y_ref = dev.w4a8_gemm(aq, wq, torch.float16)
     finally:
-        dev.lib().ody_dev_set_prefill_min_m(256)
+        dev.lib().ody_dev_set_prefill_min_m(65)
     assert torch.equal(acc, acc_ref)
     assert torch.equal(y, y_ref)
 
