@@ -40,6 +40,7 @@ def _oracle_case(oracle, m, n, k, seed):
 # ragged shapes: odd 128-row tile counts (a pair's second CTA has no weights), token
 # counts that leave a half or whole empty 128-token half tile, K not a multiple of 128
 @pytest.mark.parametrize("m,n,k", [(65, 256, 384), (100, 640, 520), (128, 384, 1024), (200, 1000, 640),
+                                   (96, 250, 256), (320, 300, 384),  # output rows not 16-byte aligned
                                    (256, 128, 128), (300, 384, 1000), (384, 200, 640),
                                    (640, 1000, 2048), (1024, 640, 520), (1537, 256, 384)])
 def test_prefill_vs_oracle(m, n, k, oracle, torch_cuda, dev):
