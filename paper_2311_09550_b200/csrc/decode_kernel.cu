@@ -1203,34 +1203,32 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             bool fin = true;
             if (d.split > 1) {
-                // Splits r < S-1 publish their partial and a release-increment (no round
-                // trip); split S-1 -- handed out last of its tile, so its peers are already
-                // in flight -- waits for the count, sums the partials and stores the tile.
+                // Every split publishes its partial and increments the tile counter; the LAST
+                // to arrive (old count == S-1) sums the others' partials and stores the tile.
+                // No epilogue ever waits for another CTA, so split items cannot convoy behind
+                // each other's epilogues (a fixed "last split" waiting for its peers did).
                 uint32_t* cnt = p.tile_cnt + d.tbase + x.nt;
-                if (x.r < d.split - 1) {
-                    fin = false;
-                    int32_t* part = p.part + static_cast<size_t>(it) * BN * kTileN;  // [t][row]
+                int32_t* part = p.part + static_cast<size_t>(it) * BN * kTileN;  // [t][row]
 #pragma unroll
-                    for (int t = 0; t < BN; ++t)
-                        if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
-                    named_bar_sync(3, 128);  // this item's partial is written
-                    if (r == 0) {
-                        __threadfence();
-                        red_release_add_u32(cnt, 1u);
-                    }
-                } else {
-                    if (r == 0) {
-                        while (ld_acquire_u32(cnt) < static_cast<uint32_t>(d.split - 1)) __nanosleep(32);
-                        *cnt = 0u;  // re-armed for the next launch
-                    }
-                    named_bar_sync(3, 128);
+                for (int t = 0; t < BN; ++t)
+                    if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
+                __threadfence();  // this thread's partial is visible before the count
+                named_bar_sync(3, 128);
+                if (r == 0) *flag = atomicAdd(cnt, 1u) == static_cast<uint32_t>(d.split - 1) ? 1u : 0u;
+                named_bar_sync(3, 128);
+                fin = *flag != 0u;
+                if (fin) {
                     __threadfence();
                     const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * BN * kTileN;
-                    for (int s2 = 0; s2 < d.split - 1; ++s2)
+                    for (int s2 = 0; s2 < d.split; ++s2) {
+                        if (s2 == x.r) continue;
 #pragma unroll
                         for (int t = 0; t < BN; ++t)
                             if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * BN + t) * kTileN + r));
+                    }
+                    if (r == 0) *cnt = 0u;  // every split arrived: re-armed for the next launch
                 }
+                named_bar_sync(3, 128);  // *flag is reused by the next item
             }
             if (fin && n < d.N) {
 #pragma unroll
