@@ -1203,22 +1203,21 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             bool fin = true;
             if (d.split > 1) {
-                // Every split publishes its partial and increments the tile counter; the LAST
-                // to arrive (old count == S-1) sums the others' partials and stores the tile.
-                // No epilogue ever waits for another CTA, so split items cannot convoy behind
-                // each other's epilogues (a fixed "last split" waiting for its peers did).
-                uint32_t* cnt = p.tile_cnt + d.tbase + x.nt;
+                // Per-ROW last-arriver reduction, no barrier and no waiting: thread r stores
+                // its row's partial into this item's slot, then an acq_rel increment of the
+                // row's counter (release: the store is visible before the count; acquire:
+                // the last arriver sees every other split's row).  The thread that arrives
+                // last for row r adds the other splits' rows and stores the outputs.  The
+                // row counters live in the program's zero region (p.acc, unused by this
+                // kernel) and are re-zeroed by their last arriver.
                 int32_t* part = p.part + static_cast<size_t>(it) * BN * kTileN;  // [t][row]
 #pragma unroll
                 for (int t = 0; t < BN; ++t)
                     if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
-                __threadfence();  // this thread's partial is visible before the count
-                named_bar_sync(3, 128);
-                if (r == 0) *flag = atomicAdd(cnt, 1u) == static_cast<uint32_t>(d.split - 1) ? 1u : 0u;
-                named_bar_sync(3, 128);
-                fin = *flag != 0u;
+                uint32_t* rc = reinterpret_cast<uint32_t*>(p.acc) + static_cast<size_t>(d.tbase + x.nt) * kTileN + r;
+                const uint32_t old = atom_add_acq_rel_u32(rc, 1u);
+                fin = old == static_cast<uint32_t>(d.split - 1);
                 if (fin) {
-                    __threadfence();
                     const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * BN * kTileN;
                     for (int s2 = 0; s2 < d.split; ++s2) {
                         if (s2 == x.r) continue;
@@ -1226,9 +1225,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         for (int t = 0; t < BN; ++t)
                             if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * BN + t) * kTileN + r));
                     }
-                    if (r == 0) *cnt = 0u;  // every split arrived: re-armed for the next launch
+                    *rc = 0u;  // every split of this row arrived: re-armed for the next launch
                 }
-                named_bar_sync(3, 128);  // *flag is reused by the next item
             }
             if (fin && n < d.N) {
 #pragma unroll
