@@ -100,6 +100,18 @@ SIGNATURES = {
 
 _lock = threading.Lock()
 _lib = None
+_path = LIB_PATH
+DIAG_LIB_PATH = os.path.join(PKG_DIR, "libodyssey_b200_diag.so")
+
+
+def use_diag_library() -> None:
+    """tools/ only: load the -DODY_DIAG build (``make -C paper_2311_09550_b200 diag``),
+    whose kernels honour the ODY_* ablation / plan-log environment knobs.  Must be
+    called before the first lib().  The product library never reads the environment."""
+    global _path
+    if _lib is not None:
+        raise RuntimeError("use_diag_library() after the library was loaded")
+    _path = DIAG_LIB_PATH
 
 
 class OdyError(RuntimeError):
@@ -131,11 +143,11 @@ def lib() -> ctypes.CDLL:
         return _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
+            if not os.path.exists(_path):
                 raise RuntimeError(
-                    f"{LIB_PATH} is missing: the W4A8 path has no CPU fallback. "
+                    f"{_path} is missing: the W4A8 path has no CPU fallback. "
                     "Build it with `make -C paper_2311_09550_b200` or __graft_entry__.build().")
-            handle = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_LOCAL)
+            handle = ctypes.CDLL(_path, mode=ctypes.RTLD_LOCAL)
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(handle, name)
                 fn.restype = res

@@ -196,6 +196,8 @@ ody_tensor* new_tensor(size_t rows, size_t cols) {
     return t;
 }
 
+int r_sms() { return device_sm_count(); }
+
 void sync(cudaStream_t st, const char* what) {
     cuda_check(cudaGetLastError(), what);
     cuda_check(cudaStreamSynchronize(st), what);
@@ -223,7 +225,8 @@ void run_gemm(const ody_qtensor* a_q, const ody_qtensor* w_q, float* out_dev, in
         if (r.workspace) cuda_check(cudaFree(r.workspace), "cudaFree");
         r.workspace = nullptr;
         cuda_check(cudaMalloc(&r.workspace, need), "cudaMalloc workspace");
-        cuda_check(cudaMemset(r.workspace, 0, need), "cudaMemset workspace");
+        // zeroed on the library stream: the GEMM launched next on it reads these counters
+        cuda_check(cudaMemsetAsync(r.workspace, 0, need, st), "cudaMemsetAsync workspace");
         r.workspace_bytes = need;
     }
     GemmArgs g = {};
@@ -558,7 +561,7 @@ ody_status ody_dev_w4a8_gemm(const void* q, const float* s_a, const void* w_pack
         g.max_ctas = max_ctas;
         g.pdl = pdl != 0;
         g.trace = g_trace;
-        if (workspace_bytes < gemm_workspace_bytes(g.M, g.N, g.K, max_ctas))
+        if (workspace_bytes < gemm_workspace_bytes(g.M, g.N, g.K, max_ctas > 0 ? max_ctas : r_sms()))
             fail(ODY_EINVAL, "ody_dev_w4a8_gemm: workspace too small");
         cuda_check(launch_w4a8_gemm(g, static_cast<cudaStream_t>(stream)), "w4a8_gemm launch");
     });
@@ -707,7 +710,7 @@ ody_status ody_dev_w4a8_linear_pf(const void* x, ody_dtype x_dtype, size_t ldx, 
         a.next_wp = static_cast<const uint8_t*>(next_w);
         a.next_bytes = next_w ? next_w_bytes : 0;
         a.trace = g_trace;
-        if (workspace_bytes < linear_scratch_bytes(a.M, a.N, a.K, max_ctas))
+        if (workspace_bytes < linear_scratch_bytes(a.M, a.N, a.K, max_ctas > 0 ? max_ctas : r_sms()))
             fail(ODY_EINVAL, "ody_dev_w4a8_linear: workspace too small");
         cuda_check(launch_w4a8_linear(a, static_cast<cudaStream_t>(stream)), "w4a8_linear launch");
     });

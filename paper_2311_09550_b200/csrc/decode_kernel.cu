@@ -1393,7 +1393,7 @@ int max_active_clusters(int S) {
             n = 0;
         }
     }
-    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    static const bool plan_log = ODY_DIAG_ENV("ODY_PLAN_LOG") != nullptr;
     if (plan_log) std::fprintf(stderr, "[ody] decode: max active clusters of %d = %d\n", S, n);
     cache[S] = n;
     return n;
@@ -1478,7 +1478,7 @@ DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms) {
 
 // Dynamic schedule: k-splits per tile so a work item streams <= 48 k-blocks (384 KiB).
 static int dyn_split(int kblocks) {
-    static const char* env = std::getenv("ODY_DYN_KB");  // diagnostics: target k-blocks per item
+    static const char* env = ODY_DIAG_ENV("ODY_DYN_KB");  // diagnostics: target k-blocks per item
     // measured (tools/program_trace.py, LLaMA-13B layer): whole 40-block tiles for
     // K = 5120 and 3 splits of 36 blocks for K = 13824 beat finer splits, whose L2 partial
     // round trips make the epilogue the bottleneck
@@ -1586,7 +1586,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         if (d.dep >= l) return cudaErrorInvalidValue;  // only earlier linears
         d.rot = chain ? 0 : rot % pl.C;
         rot += d.n_tiles;
-        static const char* pq_env = std::getenv("ODY_PROGRAM_PREQUANT");  // diagnostics: 0 = in-kernel K1
+        static const char* pq_env = ODY_DIAG_ENV("ODY_PROGRAM_PREQUANT");  // diagnostics: 0 = in-kernel K1
         const bool prequant = !(pq_env && pq_env[0] == '0');
         if (d.dep < 0 && prequant) {
             int8_t* q = reinterpret_cast<int8_t*>(cursor);
@@ -1653,18 +1653,18 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     p.next_wp = next_wp;
     p.next_bytes = next_wp ? (next_bytes & ~static_cast<size_t>(15)) : 0;
     p.trace = a[0].trace;
-    static const char* pf_env = std::getenv("ODY_DECODE_PF");
+    static const char* pf_env = ODY_DIAG_ENV("ODY_DECODE_PF");
     p.pf_units = pf_env ? std::atoi(pf_env) : 0;
-    static const char* dbg_env = std::getenv("ODY_DBG_DECODE");
+    static const char* dbg_env = ODY_DIAG_ENV("ODY_DBG_DECODE");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
-    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    static const bool plan_log = ODY_DIAG_ENV("ODY_PLAN_LOG") != nullptr;
     if (plan_log) {
         std::fprintf(stderr, "[ody] decode program L=%d: S %d C %d grid %d%s:", L, pl.S, pl.C, pl.grid,
                      chain ? " (chain)" : "");
         for (int l = 0; l < L; ++l) std::fprintf(stderr, " %dx%dx%d", a[l].M, a[l].N, a[l].K);
         std::fprintf(stderr, "\n");
     }
-    static const char* dyn_env = std::getenv("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
+    static const char* dyn_env = ODY_DIAG_ENV("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
     const bool dyn = !chain && nb == L && !(dyn_env && dyn_env[0] == '0');
     if (dyn) {
         // Independent linears: hand the items out largest first (LPT), and end with the
@@ -1674,7 +1674,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) order[l] = l;
         auto bytes_of = [&](int l) { return static_cast<long long>(p.lin[l].n_tiles) * p.lin[l].kblocks; };
         std::sort(order, order + L, [&](int x, int y) { return bytes_of(x) > bytes_of(y); });
-        static const char* tail_env = std::getenv("ODY_DYN_TAIL_KB");  // diagnostics: 0 = off
+        static const char* tail_env = ODY_DIAG_ENV("ODY_DYN_TAIL_KB");  // diagnostics: 0 = off
         const int tail_kb = tail_env ? std::atoi(tail_env) : 0;  // measured: finer tails cost more (L2 partials)
         LinDesc sorted[kMaxLin];
         for (int l = 0; l < L; ++l) sorted[l] = p.lin[order[l]];
@@ -1691,7 +1691,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) p.lin[l] = sorted[l];
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
-        static const char* pfi_env = std::getenv("ODY_DYN_PF_ITEMS");  // second-round items to L2
+        static const char* pfi_env = ODY_DIAG_ENV("ODY_DYN_PF_ITEMS");  // second-round items to L2
         p.pf_units = pfi_env ? std::atoi(pfi_env) : 0;  // measured: guessing next items costs more
         p.S = 1;
         p.C = std::min(sms, ib);

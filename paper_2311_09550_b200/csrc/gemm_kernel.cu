@@ -29,6 +29,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -1049,7 +1052,7 @@ static SkPlan plan_for(int M, int N, int K, int sms, bool fused = false) {
     s.tiles = n_tiles * s.m_tiles;
     const long long units = static_cast<long long>(s.tiles) * s.kblocks;
     s.split = 0;
-    static const char* mode_env = std::getenv("ODY_GEMM_SCHED");  // "sk" forces stream-K
+    static const char* mode_env = ODY_DIAG_ENV("ODY_GEMM_SCHED");  // "sk" forces stream-K
     const bool force_sk = mode_env && std::string(mode_env) == "sk";
     const int max_split =
         std::min({max_split_for_bn(s.bn, fused), 8, std::max(1, s.kblocks / 2)});
@@ -1103,11 +1106,28 @@ static SkPlan plan_for(int M, int N, int K, int sms, bool fused = false) {
     return s;
 }
 
-size_t gemm_workspace_bytes(int M, int N, int K, int num_sms) {
-    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+static size_t sk_workspace_bytes(int M, int N, int K, int sms) {
     const SkPlan s = plan_for(M, N, K, sms);
     return kCounterBytes + static_cast<size_t>(std::max(s.sk_tiles, 1)) * s.max_contrib * s.bn *
                                kTileN * sizeof(int32_t);
+}
+
+// num_sms > 0: the workspace of a launch on that many CTAs.  num_sms == 0 (the size
+// queries of the C ABI): the maximum over every CTA budget 1..#SMs, so a buffer sized by
+// the query is large enough whatever max_ctas the caller later passes (the stream-K
+// remainder does not shrink monotonically with the budget).
+size_t gemm_workspace_bytes(int M, int N, int K, int num_sms) {
+    if (num_sms > 0) return sk_workspace_bytes(M, N, K, num_sms);
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, size_t> cache;  // the queries run per call
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(M, N, K);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    size_t b = 0;
+    for (int P = 1; P <= device_sm_count(); ++P) b = std::max(b, sk_workspace_bytes(M, N, K, P));
+    cache.emplace(key, b);
+    return b;
 }
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st) {
@@ -1188,7 +1208,7 @@ static int max_active_clusters_fused(int G) {
 // classes then load and quantize 1/(G/S_eff) of the activations each.
 static int fused_cluster(const SkPlan& s) {
     const int S = std::max(1, s.split);
-    static const char* env = std::getenv("ODY_FUSE_CLUSTER");  // diagnostics override
+    static const char* env = ODY_DIAG_ENV("ODY_FUSE_CLUSTER");  // diagnostics override
     const int forced = env ? std::atoi(env) : 0;
     for (int G = 8; G >= 2; --G) {
         if (forced > 0 && G != forced) continue;
@@ -1216,7 +1236,7 @@ size_t linear_scratch_bytes(int M, int N, int K, int num_sms) {
     return std::max(gemm_path, program_scratch_bytes(&a, nullptr, 1));
 }
 
-static int g_linear_mode = 2;  // see kernels.h
+static thread_local int g_linear_mode = 2;  // see kernels.h; per calling thread, like the CUDA current device
 void set_linear_mode(int mode) { g_linear_mode = mode; }
 int linear_mode() { return g_linear_mode; }
 
@@ -1289,7 +1309,7 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     p.max_contrib = 1;
     p.split = s.split;
     p.cluster = fused_cluster(s);
-    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    static const bool plan_log = ODY_DIAG_ENV("ODY_PLAN_LOG") != nullptr;
     if (plan_log)
         std::fprintf(stderr, "[ody] fused %dx%dx%d: grid %d split %d dp_tiles %d cluster %d (max active %d)\n",
                      a.M, a.N, a.K, s.P, s.split, s.dp_tiles, p.cluster,
@@ -1306,7 +1326,7 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     p.ws_cnt = reinterpret_cast<uint32_t*>(gemm_ws);
     p.ws_slots = reinterpret_cast<int32_t*>(gemm_ws + kCounterBytes);
     p.pdl = a.pdl ? 1 : 0;
-    static const char* dbg_env = std::getenv("ODY_DBG_FUSE");
+    static const char* dbg_env = ODY_DIAG_ENV("ODY_DBG_FUSE");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
     p.trace = a.trace;
     return launch_bn<16, true>(p, s.P, a.pdl, st);

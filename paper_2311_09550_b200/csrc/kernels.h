@@ -1,10 +1,21 @@
 // kernels.h -- launch entry points of the sm_100a kernels (internal C++ API used by
 // the C-ABI layer in capi.cu).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstddef>
 #include <cstdint>
+
+// Diagnostic / ablation switches read from the environment (ODY_DBG_*, ODY_PREFILL_*,
+// ODY_DYN_*, ODY_PLAN_LOG, ...) exist only in a -DODY_DIAG build (make diag, used by
+// tools/).  The product library never reads the environment, so a stray variable can
+// neither change numerics nor inflate performance.
+#ifdef ODY_DIAG
+#define ODY_DIAG_ENV(name) std::getenv(name)
+#else
+#define ODY_DIAG_ENV(name) (static_cast<const char*>(nullptr))
+#endif
 
 namespace odyb200 {
 

@@ -626,11 +626,11 @@ cudaError_t launch_prefill_bt(PParams p, int max_ctas, cudaStream_t st) {
     {
         const int r = p.tiles % clusters;
         p.split_r = (CL == 2 && BT % 32 == 0 && r > 0 && 2 * r <= clusters && p.tiles > clusters) ? r : 0;
-        static const char* nosplit = std::getenv("ODY_PREFILL_NOSPLIT");
+        static const char* nosplit = ODY_DIAG_ENV("ODY_PREFILL_NOSPLIT");
         if (nosplit && std::atoi(nosplit)) p.split_r = 0;
         p.items = p.tiles + p.split_r;
     }
-    static const bool plan_log = std::getenv("ODY_PLAN_LOG") != nullptr;
+    static const bool plan_log = ODY_DIAG_ENV("ODY_PLAN_LOG") != nullptr;
     if (plan_log)
         std::fprintf(stderr, "[ody] prefill %dx%dx%d: BT %d CL %d tiles %d (+%d split) clusters %d stages %d\n", p.M,
                      p.N, p.K, BT, CL, p.tiles, p.split_r, clusters, PCfg<BT>::kLoadStages);
@@ -657,10 +657,13 @@ cudaError_t launch_prefill_bt(PParams p, int max_ctas, cudaStream_t st) {
 
 }  // namespace
 
-static int g_prefill_min_m = [] {
-    const char* env = std::getenv("ODY_PREFILL");
+// Per calling thread (like the CUDA current device): a switch set by one host thread
+// never changes the kernel choice of a launch issued concurrently by another.
+static int default_prefill_min_m() {
+    const char* env = ODY_DIAG_ENV("ODY_PREFILL");
     return env ? std::atoi(env) : 65;  // M = 128 / 192 / 256: 1.7-2.5x the tile GEMM; M = 64: the tile GEMM wins
-}();
+}
+static thread_local int g_prefill_min_m = default_prefill_min_m();
 void set_prefill_min_m(int m) { g_prefill_min_m = m; }
 bool prefill_eligible(int M, int N, int K) {
     return g_prefill_min_m > 0 && M >= g_prefill_min_m && N > 0 && K > 0;
@@ -714,13 +717,13 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st) {
         const void* o = a.acc_out ? static_cast<const void*>(a.acc_out) : a.out;
         p.vec_out = ((static_cast<size_t>(a.N) * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) ? 1 : 0;
     }
-    static const char* wreg_env = std::getenv("ODY_PREFILL_WREG");
+    static const char* wreg_env = ODY_DIAG_ENV("ODY_PREFILL_WREG");
     p.wreg = wreg_env ? std::atoi(wreg_env) : 1;
-    static const char* dbg_env = std::getenv("ODY_PREFILL_DBG");
+    static const char* dbg_env = ODY_DIAG_ENV("ODY_PREFILL_DBG");
     p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
-    static const char* cl_env = std::getenv("ODY_PREFILL_CL");
+    static const char* cl_env = ODY_DIAG_ENV("ODY_PREFILL_CL");
     if (cl_env && std::atoi(cl_env) == 4) return launch_prefill_bt<256, 4>(p, a.max_ctas, st);
-    static const char* bt_env = std::getenv("ODY_PREFILL_BT");
+    static const char* bt_env = ODY_DIAG_ENV("ODY_PREFILL_BT");
     const int bt = bt_env ? std::atoi(bt_env) : pick_prefill_bt(p.M, p.pair_tiles);
     switch (bt) {
         case 128: return launch_prefill_bt<128, 2>(p, a.max_ctas, st);

@@ -11,6 +11,8 @@ import torch
 
 sys.path.insert(0, ".")
 os.environ.setdefault("ODY_PLAN_LOG", "1")
+from paper_2311_09550_b200 import _lib as _l  # noqa: E402
+_l.use_diag_library()  # ODY_PLAN_LOG needs the -DODY_DIAG build
 from paper_2311_09550_b200 import device as dev  # noqa: E402
 from paper_2311_09550_b200._lib import lib  # noqa: E402
 
