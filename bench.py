@@ -290,7 +290,9 @@ def run_b200(args):
                    "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
                    "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
                    "cuda_graph": ("one graph per 4 steps (the 4 weight copies), PDL across steps" if use_graph else False), "pdl": bool(args.pdl),
-                   "l2_prefetch_next_weights": bool(args.prefetch),
+                   "l2_prefetch": ("dynamic kernel: second-round items L2-prefetched while the first "
+                                   "ring waits on the act-quant PDL edge" if programs is not None
+                                   else bool(args.prefetch)),
                    "lowering": args.lowering},
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps if world == 1 else None,
@@ -371,7 +373,7 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
                 pr.run(stream=stream)
 
         ms = _graph_time(fn, stream, reps=50) / len(programs)
-        launch = {"kernel": "w4a8_decode_kernel (linear program: the layer's 4 linears)",
+        launch = {"kernel": "w4a8_decode_dyn_kernel<16> (linear program: the layer's 4 linears)",
                   "us": round(ms * 1e3, 3), "bytes": step_bytes(m)}
         achieved = step_bytes(m) / (ms * 1e-3) / 1e9
     traffic = None
@@ -385,11 +387,13 @@ def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, program
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
-            "kernel": {"two_kernel": "w4a8_gemm_kernel (act_quant launched separately)",
-                       "fused_prologue": "w4a8_gemm_kernel<16,FUSE> (K1 fused)",
-                       "decode": "w4a8_decode_kernel (K1+K3+K4 in one launch)",
-                       "program": "w4a8_decode_kernel (K1+K3+K4 in one launch)"}[args.lowering] +
-                      " -- avg over the 4 layer shapes, bytes-weighted",
+            "kernel": ("act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (one linear program per step)"
+                       if programs is not None else
+                       {"two_kernel": "act_quant_kernel + w4a8_gemm_kernel",
+                        "fused_prologue": "w4a8_gemm_kernel<16,FUSE> (K1 fused)",
+                        "decode": "w4a8_decode_kernel (K1+K3+K4 in one launch)",
+                        "program": "w4a8_decode_kernel"}[args.lowering]),
+            "per_shape_kernel": "one ody_dev_w4a8_linear launch per linear (act quant + FastGEMM)",
             "per_shape": per,
             "program_launch": launch,
             "algorithmic_bytes_per_launch": {
@@ -547,21 +551,48 @@ class CpuReference:
         return gemm_bytes(m, n, k) + actq_bytes(m, k), dt
 
 
-def cpu_baseline(args, m):
+def cpu_model():
+    """`lscpu` model name (BASELINE.md §4 asks for it next to the core count)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(args, m, reps=5, warmup=2):
+    """BASELINE.md §4 / SURVEY §8(d): the reference CPU engine on the bench layer, 2
+    warm-ups then the median of `reps` timed passes (ref bench.cpp:158-178), all host
+    threads (ODYSSEY_THREADS = nproc).  A pass = the layer's 4 linears (act quant + FAST
+    GEMM each), the same step the GPU arm times."""
     threads = os.cpu_count() or 1
-    names = ["o", "down"]
+    names = [nm for nm, _, _ in LAYERS]
     cpu = CpuReference(m, threads, names)
-    cpu.run("o")  # warm
-    b = s = 0
-    for nm in names:
-        bb, ss = cpu.run(nm)
-        b += bb
-        s += ss
-    return {"value": round(b / s / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": cpu.kind,
-            "sample": f"one pass of the {'+'.join(names)} linears (act quant + FAST GEMM) at M={m}, "
-                      f"f32 host inputs, ODYSSEY_THREADS={threads}; the reference parallelises over "
-                      f"M rows only and unpacks nibbles serially (ref gemm.cpp:219-225)",
-            "seconds": round(s, 3)}
+
+    def one_pass():
+        b = s = 0
+        for nm in names:
+            bb, ss = cpu.run(nm)
+            b += bb
+            s += ss
+        return b, s
+
+    for _ in range(warmup):
+        one_pass()
+    runs = [one_pass() for _ in range(reps)]
+    med = statistics.median(s for _, s in runs)
+    b = runs[0][0]
+    return {"value": round(b / med / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": cpu.kind,
+            "cpu_model": cpu_model(),
+            "sample": f"the layer's 4 linears (act quant + FAST GEMM each) at M={m}, f32 host inputs, "
+                      f"ODYSSEY_THREADS={threads}; {warmup} warm-ups then the median of {reps} passes "
+                      f"(ref bench.cpp:158-178). The reference parallelises over M rows only and "
+                      f"unpacks nibbles serially (ref gemm.cpp:219-225)",
+            "ms_per_pass_median": round(med * 1e3, 3),
+            "ms_per_pass_all": [round(s * 1e3, 3) for _, s in runs]}
 
 
 def run_reference(args):

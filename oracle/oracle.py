@@ -174,6 +174,30 @@ class Oracle:
             raise ValueError("oracle: invalid gemm shape")
         return out
 
+    # ---- full-size checker (numpy, exact) ----
+    @staticmethod
+    def exact_accumulators(a_codes: np.ndarray, w_codes: np.ndarray) -> np.ndarray:
+        """ref gemm.cpp:229-249 at full LLaMA sizes: acc16[i,j] = sum_k a[i,k]*(16 w[j,k]).
+
+        Evaluated as a float64 BLAS matmul of the integer codes: every partial sum is an
+        integer of magnitude <= 128*8*2^17 < 2^53, so each f64 product and addition is
+        exact in any order and the result equals the reference's int32 sum bit for bit
+        (pinned against the C restatement in tests/test_oracle_golden.py)."""
+        a = np.ascontiguousarray(a_codes, np.int8).astype(np.float64)
+        w = np.ascontiguousarray(w_codes, np.int8).astype(np.float64)
+        dot = (a @ w.T).astype(np.int64)
+        return (dot * 16).astype(np.int32)
+
+    @staticmethod
+    def exact_epilogue(acc16: np.ndarray, sa: np.ndarray, sw: np.ndarray) -> np.ndarray:
+        """ref gemm.cpp:269-273: float(acc >> 4) * (sa * sw[j]), each an IEEE f32 RN op."""
+        sh = (np.asarray(acc16, np.int32) >> 4).astype(np.float32)
+        scale = np.asarray(sa, np.float32)[:, None] * np.asarray(sw, np.float32)[None, :]
+        return sh * scale
+
+    def exact_fast_gemm(self, a_codes, sa, w_codes, sw) -> np.ndarray:
+        return self.exact_epilogue(self.exact_accumulators(a_codes, w_codes), sa, sw)
+
     def dequantize_rows(self, codes: np.ndarray, scales: np.ndarray) -> np.ndarray:
         codes = np.ascontiguousarray(codes, np.int8)
         scales = np.ascontiguousarray(scales, np.float32)

@@ -137,14 +137,15 @@ LLAMA13B = {"qkv": (15360, 5120), "o": (5120, 5120), "gate_up": (27648, 5120),
 def test_llama_shapes_vs_oracle(m, layer, oracle, torch_cuda, dev):
     torch = torch_cuda
     n, k = LLAMA13B[layer]
-    if m == 1024 and layer == "down":
-        pytest.skip("covered by sampled check below (oracle cost)")
     r = oracle.rng(1000 + m)
     a = oracle.gaussian_fill(r, (m, k))
     w = oracle.gaussian_fill(r, (n, k), 0.1)
     codes, sa = oracle.quantize_activations(a)
-    _, packed, sw = oracle.quantize_weights(w)
-    want = oracle.fast_gemm(codes, sa, packed, sw, m, n, k, threads=THREADS)
+    wcodes, packed, sw = oracle.quantize_weights(w)
+    if m >= 256:  # full-size: the exact f64-BLAS checker (pinned to the C restatement)
+        want = oracle.exact_fast_gemm(codes, sa, wcodes, sw)
+    else:
+        want = oracle.fast_gemm(codes, sa, packed, sw, m, n, k, threads=THREADS)
     aq = dev.act_quant(torch.from_numpy(a).cuda())
     wq = dev.W4Weight.quantize(torch.from_numpy(w).cuda())
     got = dev.w4a8_gemm(aq, wq, torch.float32).cpu().numpy()

@@ -167,3 +167,49 @@ def test_oracle_matches_reference_capi(oracle):
             ref.free_qtensor(h)
         for h in (ah, wh):
             ref.free_tensor(h)
+
+
+def test_exact_blas_checker_matches_restatement(oracle, golden):
+    """The numpy full-size checker (f64 BLAS over integer codes, exact below 2^53) equals
+    the C restatement bit for bit: on every golden hot-path case and on a LLaMA-wide row
+    block with K = 13824 (the longest reduction the path runs)."""
+    for c in (x for x in golden if x["kind"] == "hot_path"):
+        a, w, gamma, beta = case_inputs(oracle, c)
+        codes, sa = oracle.quantize_activations(a)
+        wcodes, packed, sw = oracle.quantize_weights(w, gamma, beta)
+        acc = oracle.exact_accumulators(codes, wcodes)
+        assert np.array_equal(acc.reshape(-1), np.asarray(c["acc16"], np.int64).astype(np.int32))
+        out = oracle.exact_fast_gemm(codes, sa, wcodes, sw)
+        assert np.array_equal(bits_of(out).reshape(-1), np.asarray(c["out_bits"], np.uint32))
+    r = oracle.rng(4242)
+    m, n, k = 5, 96, 13824
+    a = oracle.gaussian_fill(r, (m, k)) * 3
+    w = oracle.gaussian_fill(r, (n, k), 0.1)
+    codes, sa = oracle.quantize_activations(a)
+    wcodes, packed, sw = oracle.quantize_weights(w)
+    want = oracle.fast_gemm(codes, sa, packed, sw, m, n, k, threads=4)
+    assert np.array_equal(bits_of(oracle.exact_fast_gemm(codes, sa, wcodes, sw)), bits_of(want))
+
+
+def acceptance_trials(oracle, trials=100):
+    """proj/tests/acceptance.cpp:80-86: Rng(101); per trial m, n, k = uniform_int(1, 64)
+    then a = N(0,1) m x k, w = 0.2 N(0,1) n x k (random_tensor, :49-53)."""
+    r = oracle.rng(101)
+    out = []
+    for _ in range(trials):
+        m, n, k = (oracle.uniform_int(r, 1, 64) for _ in range(3))
+        a = oracle.gaussian_fill(r, (m, k))
+        w = oracle.gaussian_fill(r, (n, k), 0.2)
+        out.append((m, n, k, a, w))
+    return out
+
+
+def test_acceptance_matrix_cases_oracle(oracle):
+    """acceptance.cpp:65-105 on the oracle: 100 random matrices, acc % 16 == 0 and
+    acc >> 4 == the int code dot."""
+    for m, n, k, a, w in acceptance_trials(oracle):
+        codes, _ = oracle.quantize_activations(a)
+        wcodes, packed, _ = oracle.quantize_weights(w)
+        acc = oracle.fast_accumulators(codes, packed, m, n, k)
+        assert np.all(acc % 16 == 0)
+        assert np.array_equal(acc >> 4, codes.astype(np.int64) @ wcodes.astype(np.int64).T)
