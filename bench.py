@@ -1,33 +1,42 @@
-"""bench.py -- W4A8 FastGEMM on B200: LLaMA-13B decoder-layer linears at decode M.
+"""bench.py -- W4A8 FastGEMM on B200 (OdysseyLLM's FastGEMM linear, arXiv 2311.09550).
 
-Workload (BASELINE.json configs[1], "LLaMA-13B linear shapes decode sweep M=1..64 on
-1xB200"): one STEP is one decoder layer's linear stack at decode batch M (default 16):
-    act_quant(x[M,5120])  -> qkv     GEMM (N=15360, K=5120)
-    act_quant(h[M,5120])  -> o       GEMM (N=5120,  K=5120)
-    act_quant(h[M,5120])  -> gate_up GEMM (N=27648, K=5120)
-    act_quant(g[M,13824]) -> down    GEMM (N=5120,  K=13824)
-i.e. 8 sm_100a kernel launches streaming 158.6 MB of INT4 weights.  Attention / norm /
-SiLU are outside the metric, so the step's inputs are fixed
-synthetic fp16 activations.
+HEADLINE (BASELINE.json configs[1]; the metric's "LLaMA-13B layer latency"): one STEP is
+one LLaMA-13B decoder layer's linear stack at decode batch M (default 16), run as the
+DEPENDENT chain a real layer executes (not four independent linears):
+    x[M,5120] -> qkv (15360x5120) -> o (5120x5120) on qkv[:, :5120]   (attention stand-in)
+              -> gate_up (27648x5120) -> down (5120x13824) on gate_up[:, :13824] (SiLU stand-in)
+Each linear quantizes its input per token (K1), runs the W4A8 FastGEMM (K3) and the
+dequantizing epilogue (K4), fp16 in / fp16 out.  At N = 1 the step is ONE linear program
+(the batched act-quant kernel + one persistent w4a8_decode_dyn_kernel launch: each
+dependent linear's input is quantized in-kernel once its producer finished).  At N > 1
+the same layer runs Megatron-TP over N GPUs through ody_tp_linear (column qkv/gate_up,
+row o/down with the MAX + exact int32 SUM NCCL all-reduces), one CUDA graph per step;
+strong scaling (the layer is fixed, its shards shrink).
 
-value  = algorithmic HBM bytes of the step / device time (CUDA events, CUDA-graph
-         replay, max over ranks), GB/s.  Bytes per GEMM = N*K/2 + M*K + 4N + 4M + 2*M*N;
-         per act-quant = 2*M*K + M*K + 4M.
-e2e    = the same bytes / wall time of the reference-facing C ABI with HOST buffers
-         (ody_tensor_create -> ody_quantize_activations -> ody_gemm(FAST) -> host f32),
-         H2D of the f32 activations and D2H of the f32 outputs inside the timed region.
-L2     : every step streams 158.6 MB of weights (> 126 MB L2) and steps rotate over
-         4 distinct weight copies (634 MB), so no weight byte is an L2 hit.
-N > 1  : Megatron TP of the same layer (qkv/gate_up column-, o/down row-parallel with
-         the bit-exact int32 NCCL all-reduce); strong scaling (total work fixed).
---impl reference: the reference's own CPU engine (oracle/_ref/libodyssey_ref.so, its
-         C ABI: ody_quantize_activations + ody_gemm(ODY_ENGINE_FAST)) on the host cores.
+value  = the step's algorithmic HBM bytes (all ranks) / device step time (CUDA events,
+         CUDA-graph replay, max over ranks), GB/s.  Bytes per linear = N*K/2 (INT4
+         weights) + 4N (channel scales) + 2MK (fp16 x) + 2MN (fp16 y) + 4M (token scales).
+e2e    = the same bytes / wall time through the reference-facing C ABI with HOST f32
+         buffers (ody_tensor_create -> ody_quantize_activations -> ody_gemm(FAST) ->
+         host f32, chained), H2D and D2H inside the timed region.
+L2     : each step streams 158.6 MB of weights (> 126 MB L2) and steps rotate over 4
+         distinct weight copies, so no timed weight byte is an L2 hit.
+Other BASELINE configs ride in the same JSON line (N = 1 unless stated):
+  config1   configs[0]: single GEMM M=16, N=K=4096 (one ody_dev_w4a8_linear per step)
+  sweep_M   configs[1]: the chain step at M = 1..64
+  prefill   configs[2]: the four 13B GEMMs at M = 1024 (INT8 tensor-pipe bound)
+  tp70b     configs[3]: LLaMA-2-70B decoder-layer linears, TP = N (all ranks)
+  stack13b  configs[4]: 40 LLaMA-13B layers, 1024-token prefill + 128 decode steps, TP = N
+--impl reference: the reference's own CPU engine (oracle/_ref/libodyssey_ref.so, its C
+         ABI: ody_quantize_activations + ody_gemm(ODY_ENGINE_FAST)) on the host cores.
+--gpus N without torchrun: re-launches itself under torch.distributed.run, N ranks.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,12 +49,20 @@ sys.path.insert(0, ROOT)
 HIDDEN, INTER = 5120, 13824
 LAYERS = [("qkv", 3 * HIDDEN, HIDDEN), ("o", HIDDEN, HIDDEN), ("gate_up", 2 * INTER, HIDDEN),
           ("down", HIDDEN, INTER)]
-METRIC = "W4A8 GEMM HBM GB/s (LLaMA-13B decoder-layer linears, decode)"
-LOWERINGS = {"two_kernel": 0, "fused_prologue": 1, "decode": 2, "program": 2}
+H70, I70, KV70 = 8192, 28672, 1024  # LLaMA-2-70B: hidden, intermediate, GQA kv width
+LAYERS70 = [("qkv", H70 + 2 * KV70, H70), ("o", H70, H70), ("gate_up", 2 * I70, H70), ("down", H70, I70)]
+METRIC = "W4A8 GEMM HBM GB/s (LLaMA-13B decoder-layer linear chain, decode)"
+INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 (datasheet); MEASURED_PEAKS.json has no INT8 figure
+
+
+def linear_bytes(m, n, k):
+    """Algorithmic HBM bytes of one W4A8 linear from fp16 x: packed INT4
+    weights, per-channel scales, fp16 activations in, fp16 outputs out, token scales."""
+    return n * k // 2 + 4 * n + 2 * m * k + 2 * m * n + 4 * m
 
 
 def gemm_bytes(m, n, k):
-    """Algorithmic HBM bytes of one W4A8 GEMM on quantized A."""
+    """One W4A8 GEMM on pre-quantized A (the reference CPU path's unit)."""
     return n * k // 2 + m * k + 4 * n + 4 * m + 2 * m * n
 
 
@@ -53,14 +70,8 @@ def actq_bytes(m, k):
     return 2 * m * k + m * k + 4 * m
 
 
-def linear_bytes(m, n, k):
-    """Algorithmic HBM bytes of one W4A8 linear from fp16 x: packed INT4 weights,
-    per-channel scales, fp16 activations in, fp16 outputs out, per-token scales."""
-    return n * k // 2 + 4 * n + 2 * m * k + 2 * m * n + 4 * m
-
-
-def step_bytes(m, world=1):
-    return sum(linear_bytes(m, n, k) for _, n, k in LAYERS)
+def step_bytes(m, layers=LAYERS):
+    return sum(linear_bytes(m, n, k) for _, n, k in layers)
 
 
 def peaks():
@@ -70,6 +81,14 @@ def peaks():
             d = json.load(f)
         return float(d.get("hbm_gbs", 6650.0)), "measured"
     return 6650.0, "fallback"
+
+
+def bf16_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("bf16_tflops")
+    return None
 
 
 class ClockSampler:
@@ -145,174 +164,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+
+
 # --------------------------------------------------------------------- B200 arm
-def run_b200(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_2311_09550_b200 import device as dev
-    from paper_2311_09550_b200._lib import lib
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    m = args.m
-    torch.manual_seed(1234)
-    copies = args.copies
-
-    # ---- weights: synthetic 0.1*N(0,1) f32, quantized + prepacked on the device ----
-    layers = []  # per copy: list of (name, W4Weight or tp layer)
-    if world == 1:
-        for _ in range(copies):
-            per = []
-            for name, n, k in LAYERS:
-                w = torch.randn((n, k), device="cuda") * 0.1
-                per.append((name, dev.W4Weight.quantize(w)))
-                del w
-            layers.append(per)
-    else:
-        from paper_2311_09550_b200.tp import TPDecoderLinears
-        for _ in range(copies):
-            ws = [torch.randn((n, k), device="cuda") * 0.1 for _, n, k in LAYERS]
-            layers.append(TPDecoderLinears(*ws))
-            del ws
-    torch.cuda.synchronize()
-
-    xs = {k: (torch.randn((m, k), device="cuda") * 2).to(torch.float16) for k in (HIDDEN, INTER)}
-    a_buf = {k: dev.A8(torch.empty(lib().ody_dev_a8_bytes(m, k), dtype=torch.uint8, device="cuda"),
-                       torch.empty(m, dtype=torch.float32, device="cuda"), m, k)
-             for k in (HIDDEN, INTER)}
-    outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
-    gemm_ws = dev.Workspace.for_shapes([(m, n, k) for _, n, k in LAYERS], "cuda")  # w4a8_gemm
-    for _, n, k in LAYERS:
-        ws_buf = dev.Workspace.get_linear(m, n, k, "cuda")  # w4a8_linear
-    stream = torch.cuda.Stream()
-    launches_per_step = 0
-    lib().ody_dev_set_linear_mode(LOWERINGS[args.lowering])
-
-    programs = None
-    if world == 1 and args.lowering == "program":
-        # one persistent launch per step: the layer's 4 linears as a linear program; the
-        # next step's first weights are passed as the L2 prefetch hint
-        programs = [dev.Program([dev.LinearCall(xs[w.k], w, outs[name]) for name, w in layers[c]],
-                                prefetch_next=layers[(c + 1) % copies][0][1] if args.prefetch else None)
-                    for c in range(copies)]
-
-    def step(copy_idx, pdl):
-        nonlocal launches_per_step
-        if programs is not None:
-            programs[copy_idx].run(pdl=pdl, stream=stream)
-            # fused: one batched act-quant launch + one program launch
-            launches_per_step = 2 if programs[copy_idx].fused else 2 * len(LAYERS)
-            return
-        if world == 1:
-            cnt = 0
-            seq = layers[copy_idx]
-            for li, (name, w) in enumerate(seq):
-                # public device API, one call per linear (see --lowering); the weights of
-                # the linear launched next are passed as an L2 prefetch hint
-                nxt = seq[li + 1][1] if li + 1 < len(seq) else layers[(copy_idx + 1) % copies][0][1]
-                dev.w4a8_linear(xs[w.k], w, out=outs[name], pdl=pdl, stream=stream,
-                                workspace=ws_buf, prefetch_next=nxt if args.prefetch else None)
-                cnt += 1 if lib().ody_dev_linear_is_fused(m, w.n, w.k) else 2
-            launches_per_step = cnt
-        else:
-            layers[copy_idx](xs[HIDDEN])
-
-    # ---- warmup (eager), then capture one graph per weight copy ----
-    with torch.cuda.stream(stream):
-        for i in range(max(args.warmup, 1)):
-            step(i % copies, args.pdl)
-    torch.cuda.synchronize()
-    graphs = []
-    use_graph = world == 1 and not args.no_graph
-    if use_graph:
-        for c in range(copies):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                step(c, args.pdl)
-            graphs.append(g)
-        # the steady-state loop: one graph holding `copies` consecutive steps, so PDL
-        # also overlaps the step boundaries inside it (a decode loop captured once)
-        multi = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(multi, stream=stream):
-            for c in range(copies):
-                step(c, args.pdl)
-        for i in range(args.warmup):
-            with torch.cuda.stream(stream):
-                graphs[i % copies].replay()
-                if i == 0:
-                    multi.replay()
-    torch.cuda.synchronize()
-
-    # ---- timed region ----
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            start.record(stream)
-            if use_graph:
-                for _ in range(args.steps // copies):
-                    multi.replay()
-                for i in range(args.steps % copies):
-                    graphs[i].replay()
-            else:
-                for i in range(args.steps):
-                    step(i % copies, args.pdl)
-            end.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    total_bytes = step_bytes(m)
-    value = total_bytes / (ms_step * 1e-3) / 1e9
-
-    result = {
-        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "s8 x s4(widened to s8) -> s32 accum, fp16 io",
-        "data": "synthetic: x fp16 2*N(0,1), W f32 0.1*N(0,1) quantized on device",
-        "config": {"workload": "llama13b_decoder_layer_linears_decode", "M": m,
-                   "layers": {nm: [n, k] for nm, n, k in LAYERS}, "hidden": HIDDEN,
-                   "intermediate": INTER, "parallelism": f"tp{world}" if world > 1 else "single",
-                   "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
-                   "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
-                   "cuda_graph": ("one graph per 4 steps (the 4 weight copies), PDL across steps" if use_graph else False), "pdl": bool(args.pdl),
-                   "l2_prefetch": ("dynamic kernel: second-round items L2-prefetched while the first "
-                                   "ring waits on the act-quant PDL edge" if programs is not None
-                                   else bool(args.prefetch)),
-                   "lowering": args.lowering},
-        "clocks": clk.summary(),
-        "gpu_launches": launches_per_step * args.steps if world == 1 else None,
-    }
-
-    if rank == 0 and world == 1:
-        result["roofline"] = gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs,
-                                           gemm_ws)
-        result["sweep_M"] = decode_sweep(args, dev, layers, stream) if args.sweep else None
-        result["prefill"] = None if args.no_prefill else prefill_roofline(args, dev, layers, stream)
-        result["e2e"] = e2e_c_abi(args, m)
-        if not args.no_cpu:
-            result["cpu_baseline"] = cpu_baseline(args, m)
-    if world > 1:
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(result))
-
-
 def _graph_time(fn, stream, reps, warm=3):
+    """Average device time of fn() (CUDA-graph replay, CUDA events on `stream`), ms."""
     import torch
     with torch.cuda.stream(stream):
         for _ in range(warm):
@@ -334,102 +190,233 @@ def _graph_time(fn, stream, reps, warm=3):
     return s.elapsed_time(e) / reps
 
 
-def gemm_roofline(args, dev, layers, a_buf, outs, ws_buf, stream, m, xs, programs=None, gemm_ws=None):
-    """Dominant kernel = the FastGEMM (HBM-bound at decode).  Its average launch
-    duration is timed with CUDA events on its own stream over graph replays that
-    rotate all weight copies (each launch streams fresh weights from HBM)."""
+def _max_over_ranks(ms, world):
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _weights_f32(n, k, seed):
+    """Synthetic 0.1 N(0,1) f32 weights, identical on every rank (seeded generator)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn((n, k), device="cuda", generator=g) * 0.1
+
+
+class ChainLayer:
+    """One decoder layer's linears as the dependent chain qkv -> o -> gate_up -> down,
+    ONE linear program (batched act quant + one persistent w4a8_decode_dyn_kernel; each
+    dependent linear's input is quantized in-kernel once its producer completed).  The
+    attention / SiLU stand-ins are column slices read in place.  M > 64 (prefill) lowers
+    to one act-quant + FastGEMM pair per linear, in stream order."""
+
+    def __init__(self, dev, ws, x, workspace=None):
+        import torch
+        m = x.shape[0]
+        self.x = x
+        self.outs = [torch.empty((m, w.n), dtype=torch.float16, device=x.device) for w in ws]
+        o, d = ws[1], ws[3]
+        self.prog = dev.Program([dev.LinearCall(x, ws[0], self.outs[0]),
+                                 dev.LinearCall(self.outs[0][:, :o.k], o, self.outs[1], dep=0),
+                                 dev.LinearCall(self.outs[1], ws[2], self.outs[2], dep=1),
+                                 dev.LinearCall(self.outs[2][:, :d.k], d, self.outs[3], dep=2)],
+                                workspace=workspace)
+        self.y = self.outs[3]
+
+    def run(self, pdl=True, stream=None):
+        self.prog.run(pdl=pdl, stream=stream)
+        return self.y
+
+
+class TPLayer:
+    """The same layer under Megatron TP over an ody_comm (ody_tp_linear per shard)."""
+
+    def __init__(self, dims, comm, seed):
+        from paper_2311_09550_b200.tp import TPDecoderLinears
+        ws = [_weights_f32(n, k, seed + i) for i, (_, n, k) in enumerate(dims)]
+        self.layer = TPDecoderLinears(*ws, comm=comm)
+        del ws
+
+    def run(self, x, stream=None):
+        return self.layer(x, stream=stream)
+
+    def local_bytes(self, m):
+        return sum(linear_bytes(m, n, k) for _, n, k in self.layer.shapes())
+
+
+def headline(args, dev, world, rank, comm, stream):
+    """The metric's step: one 13B decoder layer chain at M, rotating weight copies."""
+    import torch
+    m = args.m
+    x = (torch.randn((m, HIDDEN), device="cuda", generator=torch.Generator(device="cuda").manual_seed(7)) *
+         2).half()
+    if comm is None:
+        copies = []
+        for c in range(args.copies):
+            copies.append([dev.W4Weight.quantize(_weights_f32(n, k, 1000 * c + i)) for i, (_, n, k) in
+                           enumerate(LAYERS)])
+        ws_shared = None
+        layers = []
+        for c in range(args.copies):
+            layers.append(ChainLayer(dev, copies[c], x, workspace=ws_shared))
+            ws_shared = layers[-1].prog.workspace
+        step = lambda c: layers[c].run(pdl=True, stream=stream)  # noqa: E731
+        launches = 2
+        local_b = step_bytes(m)
+    else:
+        copies = None
+        layers = [TPLayer(LAYERS, comm, 1000 * c) for c in range(args.copies)]
+        step = lambda c: layers[c].run(x, stream=stream)  # noqa: E731
+        launches = 12  # per rank: column 2 + row 4 (absmax, act quant, program, epilogue), x2
+        local_b = layers[0].local_bytes(m)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for i in range(max(args.warmup, 1)):
+            step(i % args.copies)
+    torch.cuda.synchronize()
+    graphs = []
+    for c in range(args.copies):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(c)
+        graphs.append(g)
+    multi = torch.cuda.CUDAGraph()  # the steady-state decode loop: `copies` steps per graph
+    with torch.cuda.graph(multi, stream=stream):
+        for c in range(args.copies):
+            step(c)
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            graphs[i % args.copies].replay()
+        multi.replay()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for _ in range(args.steps // args.copies):
+                multi.replay()
+            for i in range(args.steps % args.copies):
+                graphs[i].replay()
+            end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    ms = _max_over_ranks(start.elapsed_time(end), world)
+    return {"layers": layers, "copies": copies, "x": x, "ms": ms, "clk": clk.summary(),
+            "launches": launches, "local_bytes": local_b, "graphs": graphs}
+
+
+def roofline(args, dev, h, stream):
+    """Dominant kernel at N = 1: the chain program launch (act_quant_rows_kernel +
+    w4a8_decode_dyn_kernel<16>), timed alone over graph replays of the weight copies back
+    to back (no PDL: each launch starts on an idle GPU); achieved = the layer's
+    algorithmic bytes / that launch time.  Also the same four linears as INDEPENDENT
+    inputs in one launch, and each linear alone (one ody_dev_w4a8_linear each)."""
+    import torch
     hbm, kind = peaks()
-    fused = args.lowering != "two_kernel"
-    if not fused:
-        for k in (HIDDEN, INTER):
-            dev.act_quant(xs[k], out=a_buf[k], stream=stream)
+    m = args.m
+    layers = h["layers"]
+
+    def chain():
+        for l in layers:
+            l.run(pdl=False, stream=stream)
+
+    ms = _graph_time(chain, stream, reps=50) / len(layers)
+    achieved = step_bytes(m) / (ms * 1e-3) / 1e9
+    xs = {k: (torch.randn((m, k), device="cuda") * 2).half() for k in (HIDDEN, INTER)}
+    ind = [dev.Program([dev.LinearCall(xs[w.k], w, torch.empty((m, w.n), dtype=torch.float16, device="cuda"))
+                        for w in cw]) for cw in h["copies"]]
+    ms_ind = _graph_time(lambda: [p.run(pdl=True, stream=stream) for p in ind], stream, reps=50) / len(ind)
     per = {}
-    tot_bytes = 0.0
-    tot_ms = 0.0
+    wsl = dev.Workspace.get_linear(m, 27648, 13824, "cuda")
     for li, (name, n, k) in enumerate(LAYERS):
-        ws = [layers[c][li][1] for c in range(len(layers))]
-
-        def fn(ws=ws, name=name, k=k):
-            for w in ws:
-                if not fused:
-                    dev.w4a8_gemm(a_buf[k], w, out=outs[name], stream=stream, workspace=gemm_ws)
-                else:
-                    dev.w4a8_linear(xs[k], w, out=outs[name], stream=stream, workspace=ws_buf)
-
-        ms = _graph_time(fn, stream, reps=200) / len(ws)
-        b = gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k)
-        per[name] = {"N": n, "K": k, "us": round(ms * 1e3, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1),
-                     "frac": round(b / (ms * 1e-3) / 1e9 / hbm, 4)}
-        tot_bytes += b
-        tot_ms += ms
-    achieved = tot_bytes / (tot_ms * 1e-3) / 1e9
-    launch = None
-    if programs is not None:
-        # the dominant kernel of the program lowering is the ONE program launch per step:
-        # algorithmic bytes of the layer / its average launch duration (graph of the copies,
-        # back to back, no PDL), each launch streaming fresh weights
-        def fn():
-            for pr in programs:
-                pr.run(stream=stream)
-
-        ms = _graph_time(fn, stream, reps=50) / len(programs)
-        launch = {"kernel": "w4a8_decode_dyn_kernel<16> (linear program: the layer's 4 linears)",
-                  "us": round(ms * 1e3, 3), "bytes": step_bytes(m)}
-        achieved = step_bytes(m) / (ms * 1e-3) / 1e9
+        out = torch.empty((m, n), dtype=torch.float16, device="cuda")
+        ws = [cw[li] for cw in h["copies"]]
+        t = _graph_time(lambda ws=ws, k=k, out=out: [dev.w4a8_linear(xs[k], w, out=out, stream=stream, pdl=True,
+                                                                      workspace=wsl) for w in ws],
+                        stream, reps=100) / len(ws)
+        b = linear_bytes(m, n, k)
+        per[name] = {"N": n, "K": k, "us": round(t * 1e3, 3), "GB/s": round(b / (t * 1e-3) / 1e9, 1),
+                     "frac": round(b / (t * 1e-3) / 1e9 / hbm, 4)}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                js = json.load(f)
-            traffic = js.get(f"program_M{m}") if programs is not None else js.get(f"M{m}")
+                traffic = json.load(f).get(f"chain_M{m}")
         except Exception:
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
-            "kernel": ("act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (one linear program per step)"
-                       if programs is not None else
-                       {"two_kernel": "act_quant_kernel + w4a8_gemm_kernel",
-                        "fused_prologue": "w4a8_gemm_kernel<16,FUSE> (K1 fused)",
-                        "decode": "w4a8_decode_kernel (K1+K3+K4 in one launch)",
-                        "program": "w4a8_decode_kernel"}[args.lowering]),
-            "per_shape_kernel": "one ody_dev_w4a8_linear launch per linear (act quant + FastGEMM)",
-            "per_shape": per,
-            "program_launch": launch,
-            "algorithmic_bytes_per_launch": {
-                nm: (gemm_bytes(m, n, k) if not fused else linear_bytes(m, n, k))
-                for nm, n, k in LAYERS}}
+            "kernel": "act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (the layer chain: ONE program launch)",
+            "launch_us": round(ms * 1e3, 3), "algorithmic_bytes_per_launch": step_bytes(m),
+            "independent_linears_program": {"us": round(ms_ind * 1e3, 3),
+                                            "GB/s": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9, 1),
+                                            "frac": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9 / hbm, 4),
+                                            "note": "same 4 linears on independent inputs (no dependencies), PDL"},
+            "per_shape": per, "per_shape_kernel": "one ody_dev_w4a8_linear launch per linear, PDL between copies"}
 
 
-INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 (datasheet); MEASURED_PEAKS.json has no INT8 figure
+def config1(args, dev, stream):
+    """configs[0]: single W4A8 linear M=16, N=K=4096 from fp16 x (K1+K3+K4), 24 rotating
+    weight copies (201 MB > L2), one launch each."""
+    import torch
+    hbm, _ = peaks()
+    m, n, k = 16, 4096, 4096
+    ws = [dev.W4Weight.quantize(_weights_f32(n, k, 77 + c)) for c in range(24)]
+    x = (torch.randn((m, k), device="cuda") * 2).half()
+    out = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    wsl = dev.Workspace.get_linear(m, n, k, "cuda")
+    ms = _graph_time(lambda: [dev.w4a8_linear(x, w, out=out, stream=stream, pdl=True, workspace=wsl) for w in ws],
+                     stream, reps=50) / len(ws)
+    b = linear_bytes(m, n, k)
+    return {"M": m, "N": n, "K": k, "us": round(ms * 1e3, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1),
+            "frac": round(b / (ms * 1e-3) / 1e9 / hbm, 4), "TOPS": round(2 * m * n * k / (ms * 1e-3) / 1e12, 2),
+            "kernel": "act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (program of one linear)"}
 
 
-def prefill_roofline(args, dev, layers, stream, m=1024):
-    """configs[2]: the LLaMA-13B layer GEMMs at prefill width M = 1024 -- INT8 tensor-pipe
-    bound.  Dominant kernel: w4a8_prefill_kernel (2-SM cta_group::2 FastGEMM) on
-    pre-quantized activations, timed with CUDA events over graph replays rotating the
-    weight copies; TOPS = 2*M*N*K / launch time, against the INT8 dense peak and against
-    2x the measured dense bf16 matmul throughput (the same tensor pipe at 1 byte/operand)."""
+def decode_sweep(args, dev, h, stream):
+    """configs[1] sweep: the chain step at M = 1..64 (one program launch per step)."""
+    import torch
+    hbm, _ = peaks()
+    res = {}
+    for m in (1, 2, 4, 8, 16, 32, 64):
+        x = (torch.randn((m, HIDDEN), device="cuda") * 2).half()
+        ls = [ChainLayer(dev, cw, x) for cw in h["copies"]]
+        ms = _graph_time(lambda ls=ls: [l.run(pdl=True, stream=stream) for l in ls], stream, reps=20) / len(ls)
+        gbs = step_bytes(m) / (ms * 1e-3) / 1e9
+        res[f"M{m}"] = {"us_per_step": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3),
+                        "fused": ls[0].prog.fused}
+        del ls
+    return res
+
+
+def prefill_roofline(args, dev, h, stream, m=1024):
+    """configs[2]: the 13B layer GEMMs at M = 1024 -- INT8 tensor-pipe bound.  Dominant
+    kernel: w4a8_prefill_kernel (2-SM cta_group::2 FastGEMM) on pre-quantized
+    activations, CUDA-event time over graph replays rotating the weight copies."""
     import torch
     res = {}
     tot_ops = tot_ms = 0.0
-    bf16 = None
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        with open(p) as fh:
-            bf16 = json.load(fh).get("bf16_tflops")
+    bf16 = bf16_peak()
     for li, (name, n, k) in enumerate(LAYERS):
         x = (torch.randn((m, k), device="cuda") * 2).half()
         a = dev.act_quant(x)
         out = torch.empty((m, n), dtype=torch.float16, device="cuda")
         gws = dev.Workspace.get(m, n, k, "cuda")
-        ws = [layers[c][li][1] for c in range(len(layers))]
-
-        def fn(ws=ws, a=a, out=out, gws=gws):
-            for w in ws:
-                dev.w4a8_gemm(a, w, out=out, stream=stream, workspace=gws)
-
-        ms = _graph_time(fn, stream, reps=10) / len(ws)
+        ws = [cw[li] for cw in h["copies"]]
+        ms = _graph_time(lambda ws=ws, a=a, out=out, gws=gws: [dev.w4a8_gemm(a, w, out=out, stream=stream,
+                                                                             workspace=gws) for w in ws],
+                         stream, reps=10) / len(ws)
         ops = 2.0 * m * n * k
         tops = ops / (ms * 1e-3) / 1e12
         res[name] = {"N": n, "K": k, "us": round(ms * 1e3, 2), "TOPS": round(tops, 1),
@@ -441,36 +428,120 @@ def prefill_roofline(args, dev, layers, stream, m=1024):
             "frac": round(tops / INT8_PEAK_TOPS, 3),
             "frac_of_2x_measured_bf16": round(tops / (2 * bf16), 3) if bf16 else None,
             "kernel": "w4a8_prefill_kernel (2-SM tcgen05 kind::i8, 256 weight rows x BT tokens per CTA pair)",
-            "layer_us": round(tot_ms * 1e3, 1), "per_shape": res,
-            "traffic": "profiles/r1_prefill_ncu.md"}
+            "layer_us": round(tot_ms * 1e3, 1), "per_shape": res, "traffic": "profiles/r2_prefill_ncu.md"}
 
 
-def decode_sweep(args, dev, layers, stream):
-    """configs[1] sweep: the decoder layer's 4 linears at M = 1..64 as ONE linear program
-    per step (batched act quant + the dynamic decode kernel), rotating the weight copies;
-    GB/s = the step's algorithmic bytes / its device time (CUDA-graph replay, PDL)."""
+def tp70b(args, dev, world, comm, stream):
+    """configs[3]: LLaMA-2-70B decoder-layer linears (hidden 8192, inter 28672, GQA kv
+    1024) at TP = N: column qkv/gate_up, row o/down (MAX + int32 SUM all-reduces).  At
+    N = 1 the unsharded layer runs as one chain program.  Decode M in {1, 16, 64} (2
+    rotating weight copies, 856 MB); prefill M = 1024 once."""
     import torch
     hbm, _ = peaks()
+    copies = 2
+    if comm is None:
+        cws = [[dev.W4Weight.quantize(_weights_f32(n, k, 7000 + 100 * c + i)) for i, (_, n, k) in
+                enumerate(LAYERS70)] for c in range(copies)]
+    else:
+        tls = [TPLayer(LAYERS70, comm, 7000 + 100 * c) for c in range(copies)]
     res = {}
-    for m in (1, 2, 4, 8, 16, 32, 64):
-        xs = {k: (torch.randn((m, k), device="cuda")).to(torch.float16) for k in (HIDDEN, INTER)}
-        outs = {name: torch.empty((m, n), dtype=torch.float16, device="cuda") for name, n, _ in LAYERS}
-        progs = [dev.Program([dev.LinearCall(xs[w.k], w, outs[name]) for name, w in layers[c]])
-                 for c in range(len(layers))]
+    for m in (1, 16, 64, 1024):
+        x = (torch.randn((m, H70), device="cuda", generator=torch.Generator(device="cuda").manual_seed(m)) *
+             2).half()
+        if comm is None:
+            ls = [ChainLayer(dev, cw, x) for cw in cws]
+            fn = lambda ls=ls: [l.run(pdl=True, stream=stream) for l in ls]  # noqa: E731
+            local = step_bytes(m, LAYERS70)
+        else:
+            fn = lambda x=x: [t.run(x, stream=stream) for t in tls]  # noqa: E731
+            local = tls[0].local_bytes(m)
+        ms = _max_over_ranks(_graph_time(fn, stream, reps=5 if m == 1024 else 30) / copies, world)
+        tot = step_bytes(m, LAYERS70)
+        ops = 2.0 * m * sum(n * k for _, n, k in LAYERS70)
+        res[f"M{m}"] = {"us_per_layer": round(ms * 1e3, 2), "GB/s": round(tot / (ms * 1e-3) / 1e9, 1),
+                        "TOPS": round(ops / (ms * 1e-3) / 1e12, 1),
+                        "per_rank_frac_hbm": round(local / (ms * 1e-3) / 1e9 / hbm, 3)}
+    return {"tp": world, "dims": {nm: [n, k] for nm, n, k in LAYERS70},
+            "path": "one chain program" if comm is None else "ody_tp_linear x4 (NCCL), one CUDA graph per layer",
+            "per_M": res}
 
-        def fn(progs=progs):
-            for pr in progs:
-                pr.run(pdl=True, stream=stream)
 
-        ms = _graph_time(fn, stream, reps=20) / len(progs)
-        gbs = step_bytes(m) / (ms * 1e-3) / 1e9
-        res[f"M{m}"] = {"us_per_step": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3),
-                        "fused": progs[0].fused}
-    return res
+def stack13b(args, dev, world, comm, stream, n_layers=40, prompt=1024, gen=128):
+    """configs[4]: 40 LLaMA-13B layers' linear stacks: a 1024-token prefill, then 128
+    decode steps at batch args.stack_m (default 1), each decode step = ONE CUDA graph of
+    the 40 layer chains (N = 1: 40 program launches + 40 batched act quants, PDL-chained;
+    N > 1: ody_tp_linear shards).  The layer output feeds the next layer; the last
+    layer's output feeds the next step (synthetic stand-in for the LM head + sampling)."""
+    import torch
+    hbm, _ = peaks()
+    mb = args.stack_m
+    w_bytes = n_layers * sum(n * k // 2 for _, n, k in LAYERS)
+    if comm is None:
+        ws = [[dev.W4Weight.quantize(_weights_f32(n, k, 90000 + 10 * L + i)) for i, (_, n, k) in enumerate(LAYERS)]
+              for L in range(n_layers)]
+    else:
+        tls = [TPLayer(LAYERS, comm, 90000 + 10 * L) for L in range(n_layers)]
+    torch.cuda.synchronize()
+
+    def build(m):
+        x0 = (torch.randn((m, HIDDEN), device="cuda") * 2).half()
+        if comm is None:
+            chain, x, wsp = [], x0, None
+            for L in range(n_layers):
+                chain.append(ChainLayer(dev, ws[L], x, workspace=wsp))
+                wsp = chain[-1].prog.workspace
+                x = chain[-1].y
+            def run():
+                for c in chain:
+                    c.run(pdl=True, stream=stream)
+                return chain[-1].y
+            return x0, run
+        def run():
+            x = x0
+            for t in tls:
+                x = t.run(x, stream=stream)
+            return x
+        return x0, run
+
+    # prefill: M = 1024 through every layer (act quant + prefill FastGEMM per linear)
+    x0p, runp = build(prompt)
+    ms_p = _max_over_ranks(_graph_time(runp, stream, reps=3, warm=1), world)
+    # decode: one graph per step; the step's output is copied into its input
+    x0d, rund = build(mb)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            rund()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        y = rund()
+        x0d.copy_(y)
+    with torch.cuda.stream(stream):
+        g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s.record(stream)
+        for _ in range(gen):
+            g.replay()
+        e.record(stream)
+    torch.cuda.synchronize()
+    ms_d = _max_over_ranks(s.elapsed_time(e) / gen, world)
+    floor_ms = w_bytes / (hbm * 1e9) * 1e3 / world
+    ops_p = 2.0 * prompt * n_layers * sum(n * k for _, n, k in LAYERS)
+    return {"layers": n_layers, "tp": world, "prefill_tokens": prompt, "decode_steps": gen, "decode_batch": mb,
+            "weight_bytes": w_bytes, "prefill_ms": round(ms_p, 3),
+            "prefill_TOPS": round(ops_p / (ms_p * 1e-3) / 1e12, 1),
+            "decode_ms_per_step": round(ms_d, 4), "decode_tokens_per_s": round(mb * 1e3 / ms_d, 1),
+            "decode_GB/s": round(w_bytes / (ms_d * 1e-3) / 1e9, 1),
+            "decode_hbm_floor_ms": round(floor_ms, 4), "decode_frac_of_floor": round(floor_ms / ms_d, 3),
+            "total_ms_1024in_128out": round(ms_p + gen * ms_d, 2),
+            "reference_paper_a100_13b_ms": 1139}
 
 
 def e2e_c_abi(args, m):
-    """Through the reference-facing C ABI with host buffers (api.py over ody_*)."""
+    """Through the reference-facing C ABI with HOST buffers (api.py over ody_*): the layer
+    chain, each linear's host f32 output feeding the next (slices as the stand-ins)."""
     import numpy as np
 
     from paper_2311_09550_b200 import api
@@ -480,14 +551,15 @@ def e2e_c_abi(args, m):
         w = (rs.standard_normal((n, k), dtype=np.float32) * 0.1).astype(np.float32)
         wq.append(api.quantize_weights(w))
         del w
-    xs = {k: (rs.standard_normal((m, k), dtype=np.float32) * 2) for k in (HIDDEN, INTER)}
+    x = rs.standard_normal((m, HIDDEN), dtype=np.float32) * 2
     h2d = sum(m * k * 4 for _, _, k in LAYERS)
     d2h = sum(m * n * 4 for _, n, _ in LAYERS)
 
     def one():
+        h = x
         for (_, n, k), w in zip(LAYERS, wq):
-            aq = api.quantize_activations_per_token(api.Tensor(xs[k]))
-            api.gemm_w4a8_fast(aq, w)
+            aq = api.quantize_activations_per_token(api.Tensor(np.ascontiguousarray(h[:, :k])))
+            h = api.gemm_w4a8_fast(aq, w)
 
     for _ in range(max(args.warmup, 3)):
         one()
@@ -498,8 +570,112 @@ def e2e_c_abi(args, m):
     dt = (time.perf_counter() - t0) / reps
     return {"value": round(step_bytes(m) / dt / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 4),
-            "path": "C ABI ody_tensor_create/ody_quantize_activations/ody_gemm(FAST), host f32 in/out",
+            "path": "C ABI ody_tensor_create/ody_quantize_activations/ody_gemm(FAST), host f32 in/out, chained",
             "timing": "host wall clock (the C-ABI calls are synchronous)"}
+
+
+def e2e_tp(args, h, stream, world):
+    """N > 1 (or --tp): end to end through the repo's TP API (TPDecoderLinears over an
+    ody_comm) with the step's activations copied in from pinned host memory and the
+    layer output copied back every step, host wall clock, max over ranks."""
+    import torch
+    m = args.m
+    x_host = (torch.randn((m, HIDDEN)) * 2).half().pin_memory()
+    y_host = torch.empty((m, HIDDEN), dtype=torch.float16).pin_memory()
+    layer, xdev = h["layers"][0], h["x"]
+
+    def one():
+        with torch.cuda.stream(stream):
+            xdev.copy_(x_host, non_blocking=True)
+            y = layer.run(xdev, stream=stream)
+            y_host.copy_(y, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(5):
+        one()
+    reps = 50
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    dt = _max_over_ranks((time.perf_counter() - t0) / reps * 1e3, world) * 1e-3
+    return {"value": round(step_bytes(m) / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": m * HIDDEN * 2,
+            "d2h_bytes_per_step": m * HIDDEN * 2, "ms_per_step": round(dt * 1e3, 4),
+            "path": "TPDecoderLinears(comm) eager: pinned H2D x -> 4 ody_tp_linear -> D2H y, per rank",
+            "timing": "host wall clock, max over ranks"}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_09550_b200 import device as dev
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = dev.Comm.from_process_group() if world > 1 else (dev.Comm(1, 0, dev.Comm.unique_id()) if args.tp
+                                                            else None)
+    stream = torch.cuda.Stream()
+    h = headline(args, dev, world, rank, comm, stream)
+    m = args.m
+    ms_step = h["ms"] / args.steps
+    value = step_bytes(m) / (ms_step * 1e-3) / 1e9
+    hbm, kind = peaks()
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "s8 x s4(widened to s8) -> s32 accum, fp16 io",
+        "data": "synthetic: x fp16 2*N(0,1), W f32 0.1*N(0,1) quantized on device",
+        "config": {"workload": "llama13b_decoder_layer_linear_chain_decode", "M": m,
+                   "layers": {nm: [n, k] for nm, n, k in LAYERS}, "hidden": HIDDEN, "intermediate": INTER,
+                   "chain": "qkv -> o(qkv[:, :5120]) -> gate_up -> down(gate_up[:, :13824])",
+                   "parallelism": f"tp{world}" if (world > 1 or comm is not None) else "single",
+                   "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
+                   "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",
+                   "cuda_graph": "one graph per 4 steps (the 4 weight copies)", "pdl": True,
+                   "step_latency_us": round(ms_step * 1e3, 2)},
+        "clocks": h["clk"],
+        "gpu_launches": h["launches"] * args.steps,
+    }
+    if world > 1 or comm is not None:
+        result["roofline"] = {"bound": "hbm", "per_rank": True, "achieved": round(
+            h["local_bytes"] / (ms_step * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(h["local_bytes"] / (ms_step * 1e-3) / 1e9 / hbm, 4), "traffic": None,
+            "kernel": "per rank: 4 x ody_tp_linear (act quant + w4a8_decode_dyn_kernel; row shards add row "
+                      "absmax, NCCL MAX + int32 SUM all-reduces, K4 epilogue)",
+            "local_bytes_per_step": h["local_bytes"]}
+    if world > 1 or comm is not None:
+        result["e2e"] = e2e_tp(args, h, stream, world)
+    if world == 1 and comm is None and not args.quick:
+        result["roofline"] = roofline(args, dev, h, stream)
+        result["config1"] = config1(args, dev, stream)
+        result["sweep_M"] = decode_sweep(args, dev, h, stream)
+        result["prefill"] = prefill_roofline(args, dev, h, stream)
+    h = None
+    torch.cuda.empty_cache()
+    if not args.quick:
+        result["tp70b"] = tp70b(args, dev, world, comm, stream)
+        torch.cuda.empty_cache()
+        result["stack13b"] = stack13b(args, dev, world, comm, stream)
+        torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
+        result["e2e"] = e2e_c_abi(args, m)
+        if not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline(args, m)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
 
 
 # --------------------------------------------------------------- CPU reference
@@ -596,6 +772,9 @@ def cpu_baseline(args, m, reps=5, warmup=2):
 
 
 def run_reference(args):
+    """The reference's own CPU engine (oracle/_ref: the reference compiled from its sources,
+    driven through its C ABI) on the same step: the layer's 4 linears, all host threads.
+    Rank 0 only under torchrun.  A bounded (~2 minute) sample of the requested steps."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -604,36 +783,45 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     cpu = CpuReference(m, threads, [nm for nm, _, _ in LAYERS])
     kind = cpu.kind
+
+    def one_step():
+        b = s = 0
+        for nm, _, _ in LAYERS:
+            bb, ss = cpu.run(nm)
+            b += bb
+            s += ss
+        return b, s
+
     t_w = time.perf_counter()
-    for i in range(args.warmup):
-        cpu.run(LAYERS[i % len(LAYERS)][0])
+    for _ in range(args.warmup):
+        one_step()
     per_step = (time.perf_counter() - t_w) / max(args.warmup, 1)
-    # bound the CPU run to ~2 minutes whatever K is: the metric is a rate, so the timed
-    # steps are a bounded sample of the K requested (stated in the line)
-    timed = min(args.steps, max(4, int(120.0 / max(per_step, 1e-3))))
-    times, tot_b = [], 0
-    for i in range(timed):
-        b, s = cpu.run(LAYERS[i % len(LAYERS)][0])
-        times.append(s)
-        tot_b += b
-    secs = sum(times)
-    value = tot_b / secs / 1e9
-    sample = (f"each step = one of the layer's 4 linears in rotation (act quant + FAST GEMM, "
-              f"M={m}), reference C ABI on {threads} host threads; {timed} of the {args.steps} "
-              f"requested steps timed (a ~2-minute bounded sample)")
+    timed = min(args.steps, max(5, int(120.0 / max(per_step, 1e-3))))
+    runs = [one_step() for _ in range(timed)]
+    secs = sum(s for _, s in runs)
+    value = sum(b for b, _ in runs) / secs / 1e9
+    sample = (f"each step = the layer's 4 linears (act quant + FAST GEMM each, M={m}), reference C ABI on "
+              f"{threads} host threads; {timed} of the {args.steps} requested steps timed (a bounded ~2-minute "
+              f"sample; median step {statistics.median(s for _, s in runs) * 1e3:.1f} ms)")
     out = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(secs / timed * 1e3, 3), "timed_steps": timed, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "s8 x s4 -> s32 (CPU)",
            "data": "synthetic: ref Rng(seed^0x9d2c5680) a~N(0,1), w~0.1 N(0,1)",
-           "config": {"workload": "llama13b_decoder_layer_linears_decode", "M": m,
+           "config": {"workload": "llama13b_decoder_layer_linear_chain_decode", "M": m,
                       "layers": {nm: [n, k] for nm, n, k in LAYERS}},
            "impl": "reference",
            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": kind,
-                            "sample": sample},
+                            "cpu_model": cpu_model(), "sample": sample},
            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -644,20 +832,17 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--m", type=int, default=16, help="decode batch (tokens) per step")
     ap.add_argument("--copies", type=int, default=4, help="distinct weight copies rotated")
-    ap.add_argument("--sweep", action="store_true", help="also report the M=1..64 GEMM sweep")
-    ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--pdl", type=int, default=1)
-    ap.add_argument("--prefetch", type=int, default=1,
-                    help="pass the next linear's weights as an L2 prefetch hint")
+    ap.add_argument("--stack-m", type=int, default=1, help="decode batch of the 40-layer stack (configs[4])")
+    ap.add_argument("--tp", action="store_true", help="N = 1: run the TP (ody_tp_linear / NCCL) path anyway")
+    ap.add_argument("--quick", action="store_true", help="headline only")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-prefill", action="store_true", help="skip the M=1024 prefill GEMM roofline")
-    ap.add_argument("--lowering", default="program", choices=list(LOWERINGS),
-                    help="program: the layer's linears in ONE persistent launch; "
-                         "decode: one cluster split-K kernel per linear (K1 fused per k-slice); "
-                         "fused_prologue: K1 fused via a cluster code all-gather; "
-                         "two_kernel: act_quant kernel + FastGEMM")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (rank 0 prints the line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

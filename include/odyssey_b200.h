@@ -194,6 +194,11 @@ typedef struct ody_linear_desc {
     ody_dtype out_dtype;
     float* s_a_out;          /* optional: the m per-token scales */
     int dep;                 /* -1, or index < this one whose out is this x */
+    const float* absmax_in;  /* optional (external x only): per-token row max overriding
+                              * max|x| -- a row-parallel TP shard passes the all-reduced max */
+    int32_t* acc_out;        /* optional: m x n int32 pre-shift accumulators written INSTEAD
+                              * of out (out may then be NULL) -- the row-parallel TP partial
+                              * that the int32 SUM all-reduce combines */
 } ody_linear_desc;
 size_t ody_dev_program_workspace_bytes(const ody_linear_desc* lin, int count);
 ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, void* workspace,
@@ -239,6 +244,32 @@ ody_status ody_qtensor_import_a8(size_t m, size_t k, const int8_t* codes, const 
 ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q, int32_t* acc);
 /* Library/device identification, e.g. "libodyssey_b200 sm_100a NVIDIA B200 (148 SMs)". */
 const char* ody_b200_version(void);
+
+/* ================================================================ part 4 */
+/* Tensor parallelism (the paper's 70B runs).
+ * ody_comm wraps an NCCL communicator (bound at run time from libnccl.so.2) over the
+ * calling thread's current CUDA device; one rank per GPU.  Rank 0 makes the unique id
+ * and the caller distributes its ODY_COMM_ID_BYTES bytes to every rank. */
+#define ODY_COMM_ID_BYTES 128
+typedef struct ody_comm ody_comm;
+ody_status ody_comm_unique_id(void* id);
+ody_status ody_comm_init(int nranks, int rank, const void* id, ody_comm** out);
+ody_status ody_comm_free(ody_comm* comm);
+ody_status ody_comm_dims(const ody_comm* comm, int* nranks, int* rank);
+
+/* Megatron linear shards.  COLUMN: W split along N (this rank's n rows), x replicated,
+ * out = this rank's [m, n] column block, no collective.  ROW: W and x split along K (this
+ * rank's k_local columns; W quantized with the FULL rows' scales,
+ * ody_dev_w4_quantize_with_scales): local row max -> all-reduce(MAX) -> K-shard FastGEMM
+ * into int32 pre-shift partials -> all-reduce(SUM, int32: exact and order-free) -> K4, so
+ * out ([m, n], replicated) is bit-identical to the unsharded linear.  Stream-ordered and
+ * CUDA-graph capturable.  workspace: ody_tp_linear_workspace_bytes, zeroed once. */
+typedef enum ody_tp_kind { ODY_TP_COLUMN = 0, ODY_TP_ROW = 1 } ody_tp_kind;
+size_t ody_tp_linear_workspace_bytes(ody_tp_kind kind, size_t m, size_t n, size_t k_local);
+ody_status ody_tp_linear(ody_comm* comm, ody_tp_kind kind, const void* x, ody_dtype x_dtype, size_t ldx,
+                         const void* w_packed, const float* s_w, size_t m, size_t n, size_t k_local,
+                         ody_dtype out_dtype, void* out, void* workspace, size_t workspace_bytes,
+                         void* stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

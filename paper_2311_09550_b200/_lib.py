@@ -35,7 +35,8 @@ class ody_linear_desc(ctypes.Structure):
     """include/odyssey_b200.h ody_linear_desc (one linear of a linear program)."""
     _fields_ = [("x", c_void_p), ("x_dtype", c_int), ("ldx", c_size_t), ("w_packed", c_void_p),
                 ("s_w", c_void_p), ("m", c_size_t), ("n", c_size_t), ("k", c_size_t), ("out", c_void_p),
-                ("out_dtype", c_int), ("s_a_out", c_void_p), ("dep", c_int)]
+                ("out_dtype", c_int), ("s_a_out", c_void_p), ("dep", c_int), ("absmax_in", c_void_p),
+                ("acc_out", c_void_p)]
 
 
 # name -> (restype, argtypes); the complete exported surface of odyssey_b200.h
@@ -96,6 +97,13 @@ SIGNATURES = {
     "ody_qtensor_import_a8": (c_int, [c_size_t, c_size_t, c_void_p, c_void_p, POINTER(c_void_p)]),
     "ody_gemm_accumulators": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ody_b200_version": (c_char_p, []),
+    "ody_comm_unique_id": (c_int, [c_void_p]),
+    "ody_comm_init": (c_int, [c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "ody_comm_free": (c_int, [c_void_p]),
+    "ody_comm_dims": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
+    "ody_tp_linear_workspace_bytes": (c_size_t, [c_int, c_size_t, c_size_t, c_size_t]),
+    "ody_tp_linear": (c_int, [c_void_p, c_int, c_void_p, c_int, c_size_t, c_void_p, c_void_p, c_size_t,
+                              c_size_t, c_size_t, c_int, c_void_p, c_void_p, c_size_t, c_void_p]),
 }
 
 _lock = threading.Lock()

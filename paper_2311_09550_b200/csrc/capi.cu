@@ -18,6 +18,11 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+
+#include <cstring>
+#include <memory>
+
 #include "../../include/odyssey_b200.h"
 #include "kernels.h"
 #include "layout.h"
@@ -592,6 +597,8 @@ bool program_args(const ody_linear_desc* lin, int count, int max_ctas, std::vect
         x.K = static_cast<int>(d.k);
         x.max_ctas = max_ctas;
         x.trace = g_trace;
+        x.absmax_in = d.absmax_in;
+        x.acc_out = d.acc_out;
         (*deps)[l] = d.dep;
     }
     return true;
@@ -627,7 +634,10 @@ ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, vo
         return einval("ody_dev_w4a8_linear_program: 1..8 linears per program");
     for (int l = 0; l < count; ++l) {
         const ody_linear_desc& d = lin[l];
-        if (!d.x || !d.w_packed || !d.s_w || !d.out) return einval("ody_dev_w4a8_linear_program: null argument");
+        if (!d.x || !d.w_packed || !d.s_w || (!d.out && !d.acc_out))
+            return einval("ody_dev_w4a8_linear_program: null argument");
+        if (d.absmax_in && d.dep >= 0)
+            return einval("ody_dev_w4a8_linear_program: absmax_in applies to external activations only");
         if (d.m == 0 || d.n == 0 || d.k == 0) return einval("ody_dev_w4a8_linear_program: empty operand");
         if (d.ldx < d.k) return einval("ody_dev_w4a8_linear_program: ldx < k");
         if (d.k > kMaxK) return einval("GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
@@ -836,6 +846,175 @@ ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q,
         cuda_check(cudaMemcpyAsync(acc, ad.p, m * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
         sync(st, "ody_gemm_accumulators");
     });
+}
+
+// ================================================================ part 4: TP
+// Megatron tensor parallelism through NCCL (SURVEY §8b "ody_tp_linear(comm, ...)", §8e).
+// NCCL is bound at run time (dlopen of libnccl.so.2): inside a PyTorch process this
+// resolves to the NCCL torch already loaded, from a plain C/C++ caller to the system one.
+}  // extern "C"
+
+namespace {
+
+struct ncclUniqueIdLike {  // ncclUniqueId: 128 opaque bytes, passed by value
+    char internal[ODY_COMM_ID_BYTES];
+};
+
+struct NcclApi {
+    void* h = nullptr;
+    int (*get_unique_id)(void*) = nullptr;
+    int (*comm_init_rank)(void**, int, ncclUniqueIdLike, int) = nullptr;
+    int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+    std::string err;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.h) {
+            api.err = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return;
+        }
+        api.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclGetUniqueId"));
+        api.comm_init_rank =
+            reinterpret_cast<int (*)(void**, int, ncclUniqueIdLike, int)>(dlsym(api.h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+            dlsym(api.h, "ncclAllReduce"));
+        api.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
+        api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
+        if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+            api.err = "libnccl.so.2 lacks the NCCL 2.x entry points";
+    });
+    if (!api.err.empty()) fail(ODY_EDEVICE, api.err);
+    return api;
+}
+
+void nccl_check(int rc, const char* what) {
+    if (rc != 0) {
+        const char* m = nccl().error_string ? nccl().error_string(rc) : "?";
+        fail(ODY_EDEVICE, std::string(what) + ": NCCL error " + std::to_string(rc) + " (" + m + ")");
+    }
+}
+
+// ncclDataType_t / ncclRedOp_t values (nccl.h, stable across NCCL 2.x)
+constexpr int kNcclInt32 = 2, kNcclFloat32 = 7;
+constexpr int kNcclSum = 0, kNcclMax = 2;
+
+size_t tp_round(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+
+ody_linear_desc tp_desc(const void* x, ody_dtype x_dtype, size_t ldx, const void* w_packed, const float* s_w,
+                        size_t m, size_t n, size_t k, ody_dtype out_dtype, void* out) {
+    ody_linear_desc d = {};
+    d.x = x;
+    d.x_dtype = x_dtype;
+    d.ldx = ldx;
+    d.w_packed = w_packed;
+    d.s_w = s_w;
+    d.m = m;
+    d.n = n;
+    d.k = k;
+    d.out = out;
+    d.out_dtype = out_dtype;
+    d.dep = -1;
+    return d;
+}
+
+}  // namespace
+
+struct ody_comm {
+    void* nccl = nullptr;  // ncclComm_t
+    int nranks = 0, rank = 0, device = 0;
+};
+
+extern "C" {
+
+ody_status ody_comm_unique_id(void* id) {
+    if (!id) return einval("ody_comm_unique_id: null argument");
+    return guarded([&] { nccl_check(nccl().get_unique_id(id), "ncclGetUniqueId"); });
+}
+
+ody_status ody_comm_init(int nranks, int rank, const void* id, ody_comm** out) {
+    if (!id || !out) return einval("ody_comm_init: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return einval("ody_comm_init: rank outside [0, nranks)");
+    return guarded([&] {
+        ncclUniqueIdLike uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        auto c = std::make_unique<ody_comm>();
+        cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
+        nccl_check(nccl().comm_init_rank(&c->nccl, nranks, uid, rank), "ncclCommInitRank");
+        c->nranks = nranks;
+        c->rank = rank;
+        *out = c.release();
+    });
+}
+
+ody_status ody_comm_free(ody_comm* c) {
+    if (!c) return ODY_OK;
+    return guarded([&] {
+        std::unique_ptr<ody_comm> own(c);
+        if (c->nccl) nccl_check(nccl().comm_destroy(c->nccl), "ncclCommDestroy");
+    });
+}
+
+ody_status ody_comm_dims(const ody_comm* c, int* nranks, int* rank) {
+    if (!c || !nranks || !rank) return einval("ody_comm_dims: null argument");
+    *nranks = c->nranks;
+    *rank = c->rank;
+    return ODY_OK;
+}
+
+size_t ody_tp_linear_workspace_bytes(ody_tp_kind kind, size_t m, size_t n, size_t k_local) {
+    ody_linear_desc d = tp_desc(nullptr, ODY_DTYPE_F16, k_local, nullptr, nullptr, m, n, k_local,
+                                ODY_DTYPE_F16, nullptr);
+    size_t b = ody_dev_program_workspace_bytes(&d, 1);
+    if (kind == ODY_TP_ROW) b = tp_round(b) + 2 * tp_round(m * 4) + tp_round(m * n * 4);
+    return b;
+}
+
+ody_status ody_tp_linear(ody_comm* comm, ody_tp_kind kind, const void* x, ody_dtype x_dtype, size_t ldx,
+                         const void* w_packed, const float* s_w, size_t m, size_t n, size_t k_local,
+                         ody_dtype out_dtype, void* out, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!comm || !x || !w_packed || !s_w || !out || !workspace) return einval("ody_tp_linear: null argument");
+    if (kind != ODY_TP_COLUMN && kind != ODY_TP_ROW) return einval("ody_tp_linear: unknown kind");
+    if (m == 0 || n == 0 || k_local == 0) return einval("ody_tp_linear: empty operand");
+    if (workspace_bytes < ody_tp_linear_workspace_bytes(kind, m, n, k_local))
+        return einval("ody_tp_linear: workspace too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ody_linear_desc d = tp_desc(x, x_dtype, ldx, w_packed, s_w, m, n, k_local, out_dtype, out);
+    if (kind == ODY_TP_COLUMN)  // x replicated, W split along N: no collective
+        return ody_dev_w4a8_linear_program(&d, 1, workspace, workspace_bytes, 0, 0, nullptr, 0, stream);
+    // Row-parallel: x and W split along K.
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    const size_t prog = tp_round(ody_dev_program_workspace_bytes(&d, 1));
+    float* amax = reinterpret_cast<float*>(ws + prog);
+    float* sa = reinterpret_cast<float*>(ws + prog + tp_round(m * 4));
+    int32_t* acc = reinterpret_cast<int32_t*>(ws + prog + 2 * tp_round(m * 4));
+    // 1. local row max -> MAX all-reduce: every rank quantizes its K-slice with the FULL
+    //    row's scale (ref quantize.cpp:113-132 on the unsharded row)
+    ody_status rc = ody_dev_row_absmax(x, x_dtype, ldx, m, k_local, amax, stream);
+    if (rc != ODY_OK) return rc;
+    rc = guarded([&] {
+        nccl_check(nccl().all_reduce(amax, amax, m, kNcclFloat32, kNcclMax, comm->nccl, st), "ncclAllReduce(max)");
+    });
+    if (rc != ODY_OK) return rc;
+    // 2. K-shard FastGEMM -> int32 pre-shift partial accumulators (+ the token scales)
+    d.out = nullptr;
+    d.absmax_in = amax;
+    d.acc_out = acc;
+    d.s_a_out = sa;
+    rc = ody_dev_w4a8_linear_program(&d, 1, workspace, prog, 0, 0, nullptr, 0, stream);
+    if (rc != ODY_OK) return rc;
+    // 3. exact, order-free int32 SUM all-reduce (== the unsharded accumulator, bit for bit)
+    rc = guarded([&] {
+        nccl_check(nccl().all_reduce(acc, acc, m * n, kNcclInt32, kNcclSum, comm->nccl, st), "ncclAllReduce(sum)");
+    });
+    if (rc != ODY_OK) return rc;
+    // 4. K4 once on the reduced accumulators: float(acc >> 4) * (sa * sw)
+    return ody_dev_dequant_epilogue(acc, sa, s_w, m, n, out_dtype, out, stream);
 }
 
 const char* ody_b200_version(void) {

@@ -110,6 +110,14 @@ struct LinDesc {
     int split;            // k-splits per tile
     int ibase;            // first work item of this linear
     int tbase;            // first tile of this linear in the program's tile numbering
+    // dynamic-schedule dependency chain (w4a8_decode_dyn_kernel)
+    int32_t* acc_out;     // optional: final int32 pre-shift accumulators (M x N) INSTEAD of out
+    uint32_t* done;       // items of this linear finished (a later linear depends on it), or NULL
+    uint32_t* amax_dst;   // per-token max |y| (f32 bits) over the output columns [amax_c0, amax_c1)
+    int amax_c0, amax_c1; //   that the dependent linear reads as its x
+    const uint32_t* dep_done;  // dependent linear: its producer's `done`, complete at dep_target
+    uint32_t dep_target;
+    const uint32_t* amax_src;  // dependent linear: per-token max |x| (its producer's amax_dst)
 };
 
 struct PParams {
@@ -973,7 +981,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         }
         for (int i = 0; i < kItemSlots; ++i) {
             mbar_init(&i_full[i], 1);
-            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4);  // MMA + converter + epilogue warps
+            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4 + 2);  // MMA + converter + epilogue + B warps
         }
         fence_mbar_init();
     }
@@ -1044,6 +1052,13 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 const LinDesc& d = p.lin[x.l];
                 const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
                 const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
+                // A dependent linear's B tiles are quantized in-kernel by the converters once
+                // its producer linear completes.  While it has not, keep HBM streaming: pull
+                // this whole item's weights into L2 (the ring then refills from L2).
+                const bool depi = d.dep_done != nullptr;
+                if (depi && lane == 0 && ld_acquire_u32(d.dep_done) < d.dep_target)
+                    bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
+                                     static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
                     if (!waited && U + k0 + 1 >= kDynStages) release_deferred();
                     const int k = k0 + lane;
@@ -1056,7 +1071,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
                         bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol);
-                        if (waited) {
+                        if (depi) {
+                            // no B copy: the B-quantizer warps write the tiles and arrive on b_full
+                        } else if (waited) {
                             issue_b(d, s, kb, nb);
                         } else {
                             dq[ndef] = x.l;
@@ -1084,6 +1101,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             if (it < 0) break;
             const DynItem x = dyn_item(p, it);
             if (x.kb_hi <= x.kb_lo) continue;
+            if (trc && lane == 0 && x.l < 4 && trc[10 + 4 * x.l] == 0) trc[10 + 4 * x.l] = globaltimer();
             const int db = JD % kDBufs;
             const uint32_t d_tmem = tmem + db * BN;
             mbar_wait(&d_empty[db], ((JD / kDBufs) & 1) ^ 1);
@@ -1110,6 +1128,88 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 __syncwarp();
             }
             ++JD;
+        }
+    } else if (warp == kWarpAlloc || warp == kWarpAlloc + 1) {
+        // B-quantizer (warps 2-3, idle once TMEM is allocated): for a DEPENDENT linear --
+        // x is an earlier linear's 16-bit output, complete once that linear's `done`
+        // reaches its item count -- quantize each unit's B tiles straight into the ring
+        // stage (quant16: bit-exact with the act-quant kernel), as soon as the stage's
+        // previous unit has been consumed (w_empty), so the x loads' L2 latency overlaps
+        // the weight stream; then arrive on b_full.  The token scale S = max/127 (IEEE;
+        // 0 -> 2^-24, ref quantize.cpp:22-35) comes from the row maxima the producer
+        // linear's epilogues accumulated.
+        constexpr int kTpt = 64 / BN < 1 ? 1 : 64 / BN;       // threads per token
+        constexpr int kCpt = 16 / kTpt;                        // 16-element chunks per thread per unit
+        const int qt = threadIdx.x - kWarpAlloc * 32;          // 0..63
+        const int bt = BN >= 64 ? qt : qt / kTpt;              // token row of this thread
+        const int bj = BN >= 64 ? 0 : qt % kTpt;
+        int U = 0;
+        bool pdl_done = false;
+        for (int j = 0;; ++j) {
+            const int is = j % kItemSlots;
+            mbar_wait(&i_full[is], (j / kItemSlots) & 1);
+            const int it = items[is];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&i_empty[is]);
+            if (it < 0) break;
+            const DynItem x = dyn_item(p, it);
+            const LinDesc& d = p.lin[x.l];
+            const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
+            if (d.dep_done == nullptr) {
+                U += nunits;
+                continue;
+            }
+            if (!pdl_done) {
+                if (p.pdl) pdl_wait();  // the previous launch re-armed the chain counters
+                pdl_done = true;
+            }
+            if (lane == 0)
+                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(20);
+            __syncwarp();
+            (void)ld_acquire_u32(d.dep_done);
+            if (trc && qt == 0 && x.l < 4 && trc[12 + 4 * x.l] == 0) trc[12 + 4 * x.l] = globaltimer();
+            const bool live = bt < d.M;
+            float sc = 1.0f, rcp = 1.0f;
+            if (live) {
+                sc = __uint_as_float(__ldcg(d.amax_src + bt)) / 127.0f;
+                if (!(sc > 0.0f)) sc = kMinScale;
+                rcp = 1.0f / sc;
+            }
+            const unsigned short* xrow = static_cast<const unsigned short*>(d.x) +
+                                         static_cast<size_t>(live ? bt : 0) * d.ldx;
+            for (int u = 0; u < nunits; ++u, ++U) {
+                const int s = U % kDynStages;
+                const int kb = x.kb_lo + kUnitBlocks * u;
+                const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                const uint32_t bb = smem_u32(ring) + s * kStageBytes + kUnitBytes;
+                constexpr int kBatch = kCpt < 8 ? kCpt : 8;  // chunk loads in flight per thread
+#pragma unroll
+                for (int cb = 0; cb < kCpt; cb += kBatch) {
+                    uint4 raw[kBatch][2];
+#pragma unroll
+                    for (int c2 = 0; c2 < kBatch; ++c2) {
+                        const int ch = bj * kCpt + cb + c2;
+                        const int b = ch >> 3, c = ch & 7;
+                        if (live && b < nb)
+                            load16_raw(xrow, (kb + b) * kBlockK + c * 16, d.K, true, raw[c2][0], raw[c2][1]);
+                    }
+                    // the stage's B region is free once its previous unit's MMAs completed
+                    if (cb == 0 && U >= kDynStages) mbar_wait(&w_empty[s], ((U / kDynStages) & 1) ^ 1);
+#pragma unroll
+                    for (int c2 = 0; c2 < kBatch; ++c2) {
+                        const int ch = bj * kCpt + cb + c2;
+                        const int b = ch >> 3, c = ch & 7;
+                        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                        if (live && b < nb)
+                            v = d.x_bf16 ? quant16<true>(raw[c2][0], raw[c2][1], sc, rcp, 0)
+                                         : quant16<false>(raw[c2][0], raw[c2][1], sc, rcp, 0);
+                        if (b < nb) sts128(bb + b * kBBlockBytes + bt * 128 + ((c ^ (bt & 7)) << 4), v);
+                    }
+                }
+                fence_proxy_async_shared();  // generic smem writes -> the MMA's async proxy
+                named_bar_sync(4, 64);
+                if (qt == 0) mbar_arrive(&b_full[s]);
+            }
         }
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kDynConvGroups) {
         const int q = warp & 3;
@@ -1228,20 +1328,61 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     *rc = 0u;  // every split of this row arrived: re-armed for the next launch
                 }
             }
-            if (fin && n < d.N) {
+            const bool depi = d.dep_done != nullptr;
+            if (depi) {
+                // in-kernel quantized x: the token scales follow from the producer's row
+                // maxima exactly as the converters derived them (complete by now: the MMAs
+                // consumed B tiles quantized after the producer finished)
+                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(32);
+            }
+            const bool own = fin && n < d.N;
+            const bool amx = d.amax_dst != nullptr && n >= d.amax_c0 && n < d.amax_c1;
 #pragma unroll
-                for (int t = 0; t < BN; ++t) {
-                    if (t < d.M) {
-                        const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
-                        const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(__ldg(d.sa + t), sw_n));
-                        const size_t idx = static_cast<size_t>(t) * d.N + n;
-                        if (d.out_dtype == kDtypeF32)
-                            static_cast<float*>(d.out)[idx] = y;
-                        else if (d.out_dtype == kDtypeF16)
-                            static_cast<__half*>(d.out)[idx] = __float2half_rn(y);
-                        else
-                            static_cast<__nv_bfloat16*>(d.out)[idx] = __float2bfloat16_rn(y);
+            for (int t = 0; t < BN; ++t) {
+                if (t < d.M) {
+                    const size_t idx = static_cast<size_t>(t) * d.N + n;
+                    if (d.acc_out) {
+                        if (own) d.acc_out[idx] = static_cast<int32_t>(v[t]);  // pre-shift (TP all-reduce)
+                        continue;
                     }
+                    float sa_t;
+                    if (depi) {
+                        sa_t = __uint_as_float(__ldcg(d.amax_src + t)) / 127.0f;
+                        if (!(sa_t > 0.0f)) sa_t = kMinScale;
+                        if (d.sa_out && own && x.nt == 0 && r == 0) d.sa_out[t] = sa_t;
+                    } else {
+                        sa_t = __ldg(d.sa + t);
+                    }
+                    const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                    const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa_t, sw_n));
+                    uint32_t mag = 0u;  // |stored value| as f32 bits (the dependent linear's x)
+                    if (d.out_dtype == kDtypeF32) {
+                        if (own) static_cast<float*>(d.out)[idx] = y;
+                    } else if (d.out_dtype == kDtypeF16) {
+                        const __half h = __float2half_rn(y);
+                        if (own) static_cast<__half*>(d.out)[idx] = h;
+                        mag = __float_as_uint(fabsf(__half2float(h)));
+                    } else {
+                        const __nv_bfloat16 h = __float2bfloat16_rn(y);
+                        if (own) static_cast<__nv_bfloat16*>(d.out)[idx] = h;
+                        mag = __float_as_uint(fabsf(__bfloat162float(h)));
+                    }
+                    if (d.amax_dst != nullptr) {  // warp-uniform: every lane joins the reduction
+                        mag = (own && amx) ? mag : 0u;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+                        if (lane == 0 && mag != 0u) atomicMax(d.amax_dst + t, mag);
+                    }
+                }
+            }
+            if (trc && r == 0 && x.l < 4) trc[11 + 4 * x.l] = globaltimer();
+            if (d.done != nullptr) {
+                // publish: every store (and row-max contribution) of this item happens
+                // before the release increment the dependent linear acquires
+                named_bar_sync(3, 128);
+                if (r == 0) {
+                    __threadfence();
+                    red_release_add_u32(d.done, 1u);
                 }
             }
         }
@@ -1257,6 +1398,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         if (atomicAdd(p.ctr + kMaxLin, 1u) == gridDim.x - 1) {
             *p.work = 0u;
             p.ctr[kMaxLin] = 0u;
+            for (int l = 0; l < p.L; ++l) {  // chain state of this launch (zero region)
+                if (p.lin[l].done) *p.lin[l].done = 0u;
+                if (p.lin[l].amax_dst)
+                    for (int t = 0; t < p.lin[l].M; ++t) p.lin[l].amax_dst[t] = 0u;
+            }
             __threadfence();
         }
         if (trc) trc[5] = globaltimer();
@@ -1277,6 +1423,7 @@ struct RowBatch {
     int M[kMaxLin], K[kMaxLin], Mp[kMaxLin], bf16[kMaxLin];
     int8_t* q[kMaxLin];
     float* s[kMaxLin];
+    const float* amax_in[kMaxLin];  // optional row max override (row-parallel TP: all-reduced max)
     int n, pdl;
 };
 
@@ -1302,6 +1449,7 @@ __device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float
     uint32_t m = 0u;
 #pragma unroll
     for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
+    if (b.amax_in[i]) m = __float_as_uint(b.amax_in[i][t]);  // the global max of a K-sharded row
     float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
     if (!(sc > 0.0f)) sc = kMinScale;
     const float rcp = 1.0f / sc;
@@ -1401,8 +1549,11 @@ int max_active_clusters(int S) {
 
 // Decode-width linear the program kernels accept: M <= 64 (the dynamic kernel; the
 // cluster kernel that quantizes dependent activations in-kernel takes M <= 16).
-bool lin_ok(const LinearArgs& a) {
-    return a.M >= 1 && a.M <= 64 && a.N >= 1 && a.K >= 1 && a.K <= kRowThreads * kRowChunks * 16 &&
+bool lin_ok(const LinearArgs& a, bool external = true) {
+    // external x goes through the batched act-quant kernel (K <= 14336); a dependent
+    // linear's x is quantized in-kernel by the B-quantizer warps (any K <= 2^17)
+    return a.M >= 1 && a.M <= 64 && a.N >= 1 && a.K >= 1 &&
+           (!external || a.K <= kRowThreads * kRowChunks * 16) &&
            (a.x_dtype == kDtypeF16 || a.x_dtype == kDtypeBF16) &&
            (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0 &&
            (reinterpret_cast<uintptr_t>(a.sw) & 15) == 0;
@@ -1416,10 +1567,46 @@ static size_t program_tiles(const LinearArgs* a, int L) {
     return t;
 }
 constexpr size_t kAccOffset = kProgramCounterRegion + kProgramMaxTiles * 4;
+// chain state inside the counter region: done[kMaxLin] at u32 64, row maxima [kMaxLin][64]
+constexpr int kChainDoneU32 = 64;
+constexpr size_t kChainAmaxOffset = 1024;
+constexpr int kChainMaxM = 64;
+static_assert(kChainAmaxOffset + kMaxLin * kChainMaxM * 4 <= kProgramCounterRegion, "counter region");
 // the last 4 KiB of the zero region are the two-kernel GEMM's stream-K counters when the
 // same scratch serves ody_dev_w4a8_linear's fallback (kLinearGemmCounters)
 constexpr size_t kZeroRegion = kAccOffset + kProgramMaxTiles * kBN * kTileN * 4 + kLinearGemmCounters;
 size_t program_zero_bytes() { return kZeroRegion; }
+
+// A dependency chain runs on the dynamic kernel when every dependent linear's x is a
+// column slice [c0, c0 + K) of its producer's 16-bit output (same tokens, row stride = the
+// producer's N) and every producer feeds one dependent linear: the producer's epilogues
+// then accumulate the slice's per-token max and the consumer quantizes in-kernel.
+static bool dyn_chain_slice(const LinearArgs* a, const int* deps, int L, int l, int* c0) {
+    const int d = deps[l];
+    if (d < 0 || d >= l) return false;
+    const LinearArgs& x = a[l];
+    const LinearArgs& y = a[d];
+    if (y.acc_out || x.absmax_in) return false;
+    if (x.x_dtype != y.out_dtype || (x.x_dtype != kDtypeF16 && x.x_dtype != kDtypeBF16)) return false;
+    if (x.M != y.M || x.ldx != static_cast<size_t>(y.N)) return false;
+    const std::ptrdiff_t off = static_cast<const uint8_t*>(x.x) - static_cast<const uint8_t*>(y.out);
+    if (off < 0 || off % 2 != 0) return false;
+    const std::ptrdiff_t col = off / 2;
+    if (col + x.K > y.N) return false;
+    *c0 = static_cast<int>(col);
+    return true;
+}
+static bool dyn_chain_ok(const LinearArgs* a, const int* deps, int L) {
+    if (!deps) return true;
+    int consumers[kMaxLin] = {};
+    for (int l = 0; l < L; ++l) {
+        if (deps[l] < 0) continue;
+        int c0;
+        if (!dyn_chain_slice(a, deps, L, l, &c0)) return false;
+        if (++consumers[deps[l]] > 1) return false;
+    }
+    return true;
+}
 
 // Cluster split S (uniform over the program) and cluster count C: minimise the busiest
 // CTA's k-blocks -- per linear for a dependency chain, over the whole program (tiles
@@ -1432,14 +1619,17 @@ DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms) {
     int max_tiles = 0;
     if (program_tiles(a, L) > kProgramMaxTiles) return best;
     for (int l = 0; l < L; ++l) {
-        if (!lin_ok(a[l])) return best;
+        if (!lin_ok(a[l], !(deps && deps[l] >= 0))) return best;
         chain |= deps && deps[l] >= 0;
         max_tiles = std::max(max_tiles, static_cast<int>(pad_n(a[l].N) / kTileN));
     }
-    if (chain)
-        for (int l = 0; l < L; ++l)
-            if (a[l].M > kBN) return best;  // in-kernel quantization: M <= 16
-    if (!chain) {  // dynamic schedule: one CTA per SM, no cluster constraints
+    static const char* dyn_env = ODY_DIAG_ENV("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
+    const bool dyn_allowed = !(dyn_env && dyn_env[0] == '0');
+    if (chain && !(dyn_allowed && dyn_chain_ok(a, deps, L))) {
+        for (int l = 0; l < L; ++l)  // the static cluster kernel: in-kernel K1 for M <= 16,
+            if (a[l].M > kBN || a[l].absmax_in || a[l].acc_out) return best;  // f16/bf16 out only
+    }
+    if (!chain || (dyn_allowed && dyn_chain_ok(a, deps, L))) {  // dynamic schedule: one CTA per SM
         best = {1, std::min(sms, 1 << 20), std::min(sms, 1 << 20)};
         return best;
     }
@@ -1562,11 +1752,14 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     size_t bld[kMaxLin];
     int8_t* bq[kMaxLin];
     float* bs[kMaxLin];
+    const float* bam[kMaxLin];
     bool batch_ok = true;
     int rot = 0;
     int mmax_b = 1;
     for (int l = 0; l < L; ++l) mmax_b = std::max(mmax_b, a[l].M);
-    const int b_rows = chain ? kBN : dyn_bn(mmax_b);
+    static const char* dynb_env = ODY_DIAG_ENV("ODY_PROGRAM_DYN");
+    const bool dyn_chain = chain && dyn_chain_ok(a, deps, L) && !(dynb_env && dynb_env[0] == '0');
+    const int b_rows = (chain && !dyn_chain) ? kBN : dyn_bn(mmax_b);
     for (int l = 0; l < L; ++l) {
         LinDesc& d = p.lin[l];
         d.x = a[l].x;
@@ -1583,6 +1776,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         d.kblocks = static_cast<int>(pad_k(a[l].K) / kBlockK);
         d.n_tiles = static_cast<int>(pad_n(a[l].N) / kTileN);
         d.dep = deps ? deps[l] : -1;
+        d.acc_out = a[l].acc_out;
         if (d.dep >= l) return cudaErrorInvalidValue;  // only earlier linears
         d.rot = chain ? 0 : rot % pl.C;
         rot += d.n_tiles;
@@ -1603,6 +1797,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             bk[nb] = d.K;
             bq[nb] = q;
             bs[nb] = sa;
+            bam[nb] = a[l].absmax_in;
             batch_ok &= d.K <= kRowThreads * kRowChunks * 16 && (a[l].x_dtype == kDtypeF16 || a[l].x_dtype == kDtypeBF16);
             ++nb;
         }
@@ -1626,6 +1821,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
                 rb.bf16[i] = bdt[i] == kDtypeBF16 ? 1 : 0;
                 rb.q[i] = bq[i];
                 rb.s[i] = bs[i];
+                rb.amax_in[i] = bam[i];
                 rows += bm[i];
             }
             rb.n = nb;
@@ -1642,7 +1838,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             ea = cudaLaunchKernelEx(&acfg, act_quant_rows_kernel, rb);
         } else {
             for (int i = 0; i < nb && ea == cudaSuccess; ++i)
-                ea = launch_act_quant(bx[i], bdt[i], bld[i], bm[i], bk[i], bq[i], bs[i], nullptr, nullptr,
+                ea = launch_act_quant(bx[i], bdt[i], bld[i], bm[i], bk[i], bq[i], bs[i], bam[i], nullptr,
                                       pdl || i > 0, st);
         }
         if (ea != cudaSuccess) return ea;
@@ -1665,7 +1861,52 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         std::fprintf(stderr, "\n");
     }
     static const char* dyn_env = ODY_DIAG_ENV("ODY_PROGRAM_DYN");  // diagnostics: 0 = static schedule
-    const bool dyn = !chain && nb == L && !(dyn_env && dyn_env[0] == '0');
+    int n_ext = 0;
+    for (int l = 0; l < L; ++l) n_ext += p.lin[l].dep < 0 ? 1 : 0;
+    const bool dyn = nb == n_ext && (!chain || dyn_chain_ok(a, deps, L)) && !(dyn_env && dyn_env[0] == '0');
+    if (dyn && chain) {
+        // Dependency chain on the dynamic kernel: items in PROGRAM order (a producer's items
+        // are all handed out before its dependent's), per-linear completion counters and
+        // per-token row maxima in the zero region (re-armed by the launch's last CTA).
+        uint32_t* done = counters + kChainDoneU32;
+        uint32_t* amax = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kChainAmaxOffset);
+        int ib = 0, tb = 0;
+        for (int l = 0; l < L; ++l) {
+            LinDesc& d = p.lin[l];
+            d.split = dyn_split(d.kblocks);
+            d.ibase = ib;
+            d.tbase = tb;
+            ib += d.n_tiles * d.split;
+            tb += d.n_tiles;
+        }
+        for (int l = 0; l < L; ++l) {
+            LinDesc& d = p.lin[l];
+            if (d.dep < 0) continue;
+            int c0 = 0;
+            dyn_chain_slice(a, deps, L, l, &c0);
+            LinDesc& y = p.lin[d.dep];
+            y.done = done + d.dep;
+            y.amax_dst = amax + d.dep * kChainMaxM;
+            y.amax_c0 = c0;
+            y.amax_c1 = c0 + d.K;
+            d.dep_done = y.done;
+            d.dep_target = static_cast<uint32_t>(y.n_tiles * y.split);
+            d.amax_src = y.amax_dst;
+        }
+        p.n_items = ib;
+        p.work = counters + kMaxLin + 1;
+        p.pf_units = 0;
+        p.S = 1;
+        p.C = std::min(sms, ib);
+        if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
+        int mmax = 1;
+        for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
+        switch (dyn_bn(mmax)) {
+            case 16: return launch_dyn<16>(p, prog_pdl, st);
+            case 32: return launch_dyn<32>(p, prog_pdl, st);
+            default: return launch_dyn<64>(p, prog_pdl, st);
+        }
+    }
     if (dyn) {
         // Independent linears: hand the items out largest first (LPT), and end with the
         // linear of fewest bytes cut into ~12-block items, so the last items -- whose

@@ -1266,12 +1266,13 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
     if (g_linear_mode == 2 && aligned && decode_eligible(a.M, a.N, a.K, a.x_dtype, sms))
         return launch_w4a8_decode(a, st);  // the whole buffer is its program scratch
     uint8_t* gemm_ws = ws + program_zero_bytes() - kCounterBytes;
-    if (!(aligned && a.x_dtype != kDtypeF32 && linear_is_fused(a.M, a.N, a.K, sms))) {
+    const bool tp_io = a.absmax_in != nullptr || a.acc_out != nullptr;  // row-parallel TP shard
+    if (tp_io || !(aligned && a.x_dtype != kDtypeF32 && linear_is_fused(a.M, a.N, a.K, sms))) {
         const size_t a8_off = linear_scratch_bytes(a.M, a.N, a.K, sms) - round_up(a8_bytes(a.M, a.K), 256) -
                               round_up(pad_m(a.M) * sizeof(float), 256);
         int8_t* q = reinterpret_cast<int8_t*>(ws + a8_off);
         float* sa = a.sa_out ? a.sa_out : reinterpret_cast<float*>(ws + a8_off + round_up(a8_bytes(a.M, a.K), 256));
-        cudaError_t e = launch_act_quant(a.x, a.x_dtype, a.ldx, a.M, a.K, q, sa, nullptr, nullptr,
+        cudaError_t e = launch_act_quant(a.x, a.x_dtype, a.ldx, a.M, a.K, q, sa, a.absmax_in, nullptr,
                                          a.pdl, st);
         if (e != cudaSuccess) return e;
         GemmArgs g = {};
@@ -1279,7 +1280,8 @@ cudaError_t launch_w4a8_linear(const LinearArgs& a, cudaStream_t st) {
         g.sa = sa;
         g.wp = a.wp;
         g.sw = a.sw;
-        g.out = a.out;
+        g.out = a.acc_out ? nullptr : a.out;
+        g.acc_out = a.acc_out;
         g.out_dtype = a.out_dtype;
         g.workspace = gemm_ws;
         g.workspace_bytes = gws;

@@ -258,9 +258,11 @@ class LinearCall:
     the same program whose ``out`` is (or contains) this ``x``, or -1."""
     x: torch.Tensor
     w: "W4Weight"
-    out: torch.Tensor
+    out: torch.Tensor | None
     dep: int = -1
     sa_out: torch.Tensor | None = None
+    absmax_in: torch.Tensor | None = None  # row-parallel TP: the all-reduced per-token max
+    acc_out: torch.Tensor | None = None    # int32 [m, n] pre-shift accumulators instead of out
 
 
 class Program:
@@ -279,14 +281,20 @@ class Program:
             if c.x.dim() != 2 or c.x.shape[1] != c.w.k or c.x.stride(1) != 1:
                 raise OdyError(1, "linear program: x must be [m, k] with unit column stride")
             m = c.x.shape[0]
-            if tuple(c.out.shape) != (m, c.w.n) or not c.out.is_contiguous():
-                raise OdyError(1, "linear program: out must be a contiguous [m, n] tensor")
+            tgt = c.acc_out if c.acc_out is not None else c.out
+            if tgt is None or tuple(tgt.shape) != (m, c.w.n) or not tgt.is_contiguous():
+                raise OdyError(1, "linear program: out (or acc_out) must be a contiguous [m, n] tensor")
+            if c.acc_out is not None and c.acc_out.dtype != torch.int32:
+                raise OdyError(1, "linear program: acc_out must be int32")
             d.x, d.x_dtype, d.ldx = c.x.data_ptr(), _DT[c.x.dtype], c.x.stride(0)
             d.w_packed, d.s_w = c.w.packed.data_ptr(), c.w.s.data_ptr()
             d.m, d.n, d.k = m, c.w.n, c.w.k
-            d.out, d.out_dtype = c.out.data_ptr(), _DT[c.out.dtype]
+            d.out = c.out.data_ptr() if c.out is not None else None
+            d.out_dtype = _DT[c.out.dtype] if c.out is not None else _DT[torch.float16]
             d.s_a_out = c.sa_out.data_ptr() if c.sa_out is not None else None
             d.dep = c.dep
+            d.absmax_in = c.absmax_in.data_ptr() if c.absmax_in is not None else None
+            d.acc_out = c.acc_out.data_ptr() if c.acc_out is not None else None
         self.descs = descs
         need = lib().ody_dev_program_workspace_bytes(descs, len(calls))
         if workspace is None or workspace.numel() < need:
@@ -305,7 +313,7 @@ class Program:
             self.descs, len(self.calls), self.workspace.data_ptr(), self.workspace.numel(), self.max_ctas,
             int(pdl), nxt.data_ptr() if nxt is not None else None, nxt.numel() if nxt is not None else 0,
             _stream(stream)))
-        return [c.out for c in self.calls]
+        return [c.acc_out if c.acc_out is not None else c.out for c in self.calls]
 
 
 class W4A8Linear:
@@ -330,3 +338,85 @@ class W4A8Linear:
 
     def __call__(self, x: torch.Tensor, pdl: bool = False) -> torch.Tensor:
         return w4a8_linear(x, self.weight, self.out_dtype, pdl=pdl)
+
+
+# ------------------------------------------------------------------ tensor parallelism
+ODY_TP_COLUMN, ODY_TP_ROW = 0, 1
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """An ody_comm (C ABI part 4): an NCCL communicator over this rank's current device.
+    Rank 0 makes ``unique_id()``; every rank passes the same bytes to ``Comm(...)``."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        import ctypes
+        if len(uid) != COMM_ID_BYTES:
+            raise OdyError(1, "ody_comm_init: the unique id is 128 bytes")
+        self._uid = ctypes.create_string_buffer(uid, COMM_ID_BYTES)
+        h = ctypes.c_void_p()
+        check(lib().ody_comm_init(nranks, rank, self._uid, ctypes.byref(h)))
+        self.handle = h
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+        check(lib().ody_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        """Bootstrap over an initialised torch.distributed group (the id travels as an
+        object broadcast from rank 0)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        return cls(world, rank, box[0])
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            check(lib().ody_comm_free(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TPWorkspace:
+    """Per-device workspace for ody_tp_linear (zeroed once, reused)."""
+
+    _per_device: dict = {}
+
+    @classmethod
+    def get(cls, kind: int, m: int, n: int, k_local: int, device) -> torch.Tensor:
+        dev = torch.device(device)
+        need = lib().ody_tp_linear_workspace_bytes(kind, m, n, k_local)
+        ws = cls._per_device.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+            cls._per_device[dev] = ws
+        return ws
+
+
+def tp_linear(comm: Comm, kind: int, x: torch.Tensor, w: W4Weight, out_dtype=torch.float16,
+              out: torch.Tensor | None = None, workspace: torch.Tensor | None = None, stream=None):
+    """One Megatron shard through ody_tp_linear: COLUMN (this rank's N rows, no
+    collective) or ROW (this rank's K columns; MAX + exact int32 SUM all-reduces)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.shape[1] != w.k or x.stride(1) != 1:
+        raise OdyError(1, "ody_tp_linear: x must be [m, k_local] with unit column stride")
+    m = x.shape[0]
+    if out is None:
+        out = torch.empty((m, w.n), dtype=out_dtype, device=x.device)
+    if workspace is None:
+        workspace = TPWorkspace.get(kind, m, w.n, w.k, x.device)
+    check(lib().ody_tp_linear(comm.handle, kind, x.data_ptr(), _DT[x.dtype], x.stride(0), w.packed.data_ptr(),
+                              w.s.data_ptr(), m, w.n, w.k, _DT[out.dtype], out.data_ptr(), workspace.data_ptr(),
+                              workspace.numel(), _stream(stream)))
+    return out

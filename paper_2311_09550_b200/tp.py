@@ -16,9 +16,13 @@ Row-parallel (o, down): W and x split along K.
   5. the dequantizing epilogue (K4) runs once on the reduced accumulators.
 The result is bit-identical to the single-GPU layer (and to the reference).
 
-The arithmetic is delegated to a backend (default: the sm_100a kernels through the C
-ABI).  Collectives go through torch.distributed (NCCL on GPUs; the CPU tests drive
-the same orchestration over gloo with a test backend).
+Two transports, one arithmetic:
+  * ``comm=device.Comm`` (the product path on GPUs): each shard is ONE ody_tp_linear call
+    of the C ABI -- K1, the K-shard FastGEMM, NCCL MAX/SUM all-reduces and K4 all
+    stream-ordered in the library (CUDA-graph capturable);
+  * ``comm=None``: the same steps orchestrated here over torch.distributed with a
+    backend for the arithmetic (default: the sm_100a kernels through the C ABI; the CPU
+    tests drive it over gloo with the oracle's arithmetic).
 """
 from __future__ import annotations
 
@@ -78,15 +82,21 @@ def _split(total: int, world: int, rank: int):
 class ColumnParallelW4A8Linear:
     """y[:, shard] = x @ W[shard, :]^T ; output stays N-sharded."""
 
-    def __init__(self, w_full, group=None, backend=None):
+    def __init__(self, w_full, group=None, backend=None, comm=None, out_dtype=torch.float16):
         self.group = group
-        self.rank, self.world = _rank_world(group)
-        self.backend = backend or DeviceBackend()
+        self.comm = comm
+        self.out_dtype = out_dtype
+        self.rank, self.world = (comm.rank, comm.nranks) if comm is not None else _rank_world(group)
+        self.backend = backend or DeviceBackend(out_dtype)
         n = w_full.shape[0]
         self.n0, self.n1 = _split(n, self.world, self.rank)
         self.weight = self.backend.quantize(w_full[self.n0:self.n1].contiguous())
 
-    def __call__(self, x):
+    def __call__(self, x, out=None, stream=None):
+        if self.comm is not None:
+            from . import device
+            return device.tp_linear(self.comm, device.ODY_TP_COLUMN, x, self.weight, self.out_dtype, out=out,
+                                    stream=stream)
         a = self.backend.act_quant(x)
         return self.backend.gemm(a, self.weight)
 
@@ -94,18 +104,24 @@ class ColumnParallelW4A8Linear:
 class RowParallelW4A8Linear:
     """y = sum_r x[:, Kr] @ W[:, Kr]^T, reduced exactly in int32 before the epilogue."""
 
-    def __init__(self, w_full, group=None, backend=None):
+    def __init__(self, w_full, group=None, backend=None, comm=None, out_dtype=torch.float16):
         self.group = group
-        self.rank, self.world = _rank_world(group)
-        self.backend = backend or DeviceBackend()
+        self.comm = comm
+        self.out_dtype = out_dtype
+        self.rank, self.world = (comm.rank, comm.nranks) if comm is not None else _rank_world(group)
+        self.backend = backend or DeviceBackend(out_dtype)
         k = w_full.shape[1]
         self.k0, self.k1 = _split(k, self.world, self.rank)
         scales = self.backend.full_row_scales(w_full)  # scale of the FULL row, pre-sharding
         self.weight = self.backend.quantize_with_scales(w_full[:, self.k0:self.k1].contiguous(),
                                                         scales)
 
-    def __call__(self, x_local):
+    def __call__(self, x_local, out=None, stream=None):
         """x_local: this rank's K-slice [M, K/P] of the activations."""
+        if self.comm is not None:
+            from . import device
+            return device.tp_linear(self.comm, device.ODY_TP_ROW, x_local, self.weight, self.out_dtype, out=out,
+                                    stream=stream)
         amax = self.backend.row_absmax(x_local)
         if self.world > 1:
             dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=self.group)
@@ -121,16 +137,40 @@ class TPDecoderLinears:
     qkv and gate_up column-parallel, o and down row-parallel.  Attention, norm and SiLU
     are stand-ins (slices), never part of the GEMM metric."""
 
-    def __init__(self, w_qkv, w_o, w_gate_up, w_down, group=None, backend=None):
-        self.qkv = ColumnParallelW4A8Linear(w_qkv, group, backend)
-        self.o = RowParallelW4A8Linear(w_o, group, backend)
-        self.gate_up = ColumnParallelW4A8Linear(w_gate_up, group, backend)
-        self.down = RowParallelW4A8Linear(w_down, group, backend)
+    def __init__(self, w_qkv, w_o, w_gate_up, w_down, group=None, backend=None, comm=None):
+        self.qkv = ColumnParallelW4A8Linear(w_qkv, group, backend, comm)
+        self.o = RowParallelW4A8Linear(w_o, group, backend, comm)
+        self.gate_up = ColumnParallelW4A8Linear(w_gate_up, group, backend, comm)
+        self.down = RowParallelW4A8Linear(w_down, group, backend, comm)
+        self.comm = comm
+        self._bufs = None
 
-    def __call__(self, x):
+    def shapes(self):
+        """(kind, n, k_local) of this rank's four shards, in layer order."""
+        return [(0, self.qkv.weight.n, self.qkv.weight.k), (1, self.o.weight.n, self.o.weight.k),
+                (0, self.gate_up.weight.n, self.gate_up.weight.k), (1, self.down.weight.n, self.down.weight.k)]
+
+    def __call__(self, x, stream=None):
+        if self.comm is not None:
+            return self._forward_comm(x, stream)
         qkv = self.qkv(x)                                  # [M, 3H/P] local heads
         h_local = qkv[:, : self.o.k1 - self.o.k0]          # stand-in for local attention
         h = self.o(h_local.contiguous())                   # [M, H] replicated
         gu = self.gate_up(h)                               # [M, 2I/P]
         act_local = gu[:, : self.down.k1 - self.down.k0]   # stand-in for SiLU(g)*u
         return self.down(act_local.contiguous())           # [M, H]
+
+    def _forward_comm(self, x, stream):
+        """Preallocated outputs (CUDA-graph friendly): the stand-in slices are views with
+        the producer's row stride, read in place by the next shard."""
+        m = x.shape[0]
+        if self._bufs is None or self._bufs[0].shape[0] != m:
+            mk = lambda n: torch.empty((m, n), dtype=torch.float16, device=x.device)  # noqa: E731
+            self._bufs = (mk(self.qkv.weight.n), mk(self.o.weight.n), mk(self.gate_up.weight.n),
+                          mk(self.down.weight.n))
+        qkv, h, gu, y = self._bufs
+        self.qkv(x, out=qkv, stream=stream)
+        self.o(qkv[:, : self.o.k1 - self.o.k0], out=h, stream=stream)
+        self.gate_up(h, out=gu, stream=stream)
+        self.down(gu[:, : self.down.k1 - self.down.k0], out=y, stream=stream)
+        return y

@@ -263,3 +263,67 @@ def test_program_fallback_and_errors(torch_cuda, dev):
     o2 = torch.empty((4, 256), dtype=torch.float16, device="cuda")
     with pytest.raises(OdyError):
         dev.Program([dev.LinearCall(x2, w, o2, dep=0)]).run()
+
+
+@pytest.mark.parametrize("m,xdt", [(1, "f16"), (16, "bf16"), (32, "f16"), (64, "bf16")])
+def test_program_chain_vs_oracle(m, xdt, oracle, torch_cuda, dev):
+    """Dependency chain on the dynamic kernel (producer epilogues accumulate the consumer's
+    per-token row max; the consumer quantizes its B tiles in-kernel): every linear's
+    output bit-exact vs the oracle applied step by step to the same 16-bit intermediates.
+    Includes a split-K producer (K = 13824) and a ragged N."""
+    torch = torch_cuda
+    dt = torch.float16 if xdt == "f16" else torch.bfloat16
+    dims = [(3000, 1024), (13824, 1000), (1000, 13824), (640, 1000)]  # x1 = out0[:, 8:1008]
+    ws = [_weights(torch, dev, n, k, seed=300 + i, scale=0.05) for i, (n, k) in enumerate(dims)]
+    x0 = (torch.randn((m, 1024), device="cuda") * 2).to(dt)
+    outs = [torch.empty((m, n), dtype=dt, device="cuda") for n, _ in dims]
+    calls = [dev.LinearCall(x0, ws[0][0], outs[0]),
+             dev.LinearCall(outs[0][:, 8:1008], ws[1][0], outs[1], dep=0),
+             dev.LinearCall(outs[1], ws[2][0], outs[2], dep=1),
+             dev.LinearCall(outs[2], ws[3][0], outs[3], dep=2)]
+    prog = dev.Program(calls)
+    assert prog.fused
+    for rep in range(3):
+        for o in outs:
+            o.zero_()
+        prog.run(pdl=rep > 0)
+        torch.cuda.synchronize()
+        h = x0.float().cpu().numpy()
+        for i, ((n, k), (_, flat, sw), o) in enumerate(zip(dims, ws, outs)):
+            xin = np.ascontiguousarray(h[:, 8:1008]) if i == 1 else h
+            want, _ = _want(oracle, xin, flat, sw, m, n, k)
+            got = o.float().cpu().numpy()
+            want16 = torch.from_numpy(want).to(dt).float().numpy()
+            assert np.array_equal(bits_of(got), bits_of(want16)), (rep, i, int((got != want16).sum()))
+            h = got
+
+
+def test_program_row_parallel_shards(oracle, torch_cuda, dev):
+    """Row-parallel TP building block: two K-shards of one linear in ONE program, each
+    quantized with the FULL row's max (absmax_in) and emitting int32 pre-shift partials
+    (acc_out).  partial_0 + partial_1 == the unsharded accumulators bit for bit, and the
+    K4 epilogue of the sum == the unsharded linear."""
+    torch = torch_cuda
+    for m in (1, 16, 48):
+        n, k = 1000, 2048
+        rs = np.random.default_rng(m)
+        w = torch.from_numpy(rs.standard_normal((n, k), dtype=np.float32) * 0.05).cuda()
+        x = (torch.randn((m, k), device="cuda") * 2).half()
+        full = dev.W4Weight.quantize(w)
+        shards = [dev.W4Weight.quantize_with_scales(w[:, :k // 2].contiguous(), full.s),
+                  dev.W4Weight.quantize_with_scales(w[:, k // 2:].contiguous(), full.s)]
+        amax = dev.row_absmax(x)
+        accs = [torch.empty((m, n), dtype=torch.int32, device="cuda") for _ in range(2)]
+        xs = [x[:, :k // 2].contiguous(), x[:, k // 2:].contiguous()]
+        prog = dev.Program([dev.LinearCall(xs[i], shards[i], None, absmax_in=amax, acc_out=accs[i])
+                            for i in range(2)])
+        assert prog.fused
+        prog.run()
+        aq = dev.act_quant(x)
+        want_acc = dev.w4a8_gemm(aq, full, accumulators=True)
+        codes = aq.codes().cpu().numpy()
+        flat = full.to_flat().cpu().numpy()
+        assert np.array_equal(want_acc.cpu().numpy(), oracle.fast_accumulators(codes, flat, m, n, k, THREADS))
+        assert torch.equal(accs[0] + accs[1], want_acc), m
+        y = dev.dequant_epilogue(accs[0] + accs[1], aq.s, full.s, torch.float16)
+        assert torch.equal(y, dev.w4a8_gemm(aq, full, torch.float16)), m

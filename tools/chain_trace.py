@@ -1,0 +1,61 @@
+"""Per-CTA timeline of ONE dependent-chain program launch (the LLaMA-13B layer
+qkv -> o -> gate_up -> down, slices as attention / SiLU stand-ins) on the dynamic
+kernel: per linear, each CTA's first MMA, dependency release and last epilogue
+(diagnostics, GPU box only)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2311_09550_b200 import device as dev  # noqa: E402
+from paper_2311_09550_b200._lib import lib  # noqa: E402
+
+H, I = 5120, 13824
+LAYERS = [("qkv", 3 * H, H), ("o", H, H), ("gate_up", 2 * I, H), ("down", H, I)]
+
+
+def main(m=16):
+    ws = [dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1) for _, n, k in LAYERS]
+    x = (torch.randn((m, H), device="cuda") * 2).half()
+    outs = [torch.empty((m, n), dtype=torch.float16, device="cuda") for _, n, _ in LAYERS]
+    prog = dev.Program([dev.LinearCall(x, ws[0], outs[0]),
+                        dev.LinearCall(outs[0][:, :H], ws[1], outs[1], dep=0),
+                        dev.LinearCall(outs[1], ws[2], outs[2], dep=1),
+                        dev.LinearCall(outs[2][:, :I], ws[3], outs[3], dep=2)])
+    for _ in range(3):
+        prog.run()
+    torch.cuda.synchronize()
+    buf = torch.zeros(148 * 32 + 512, dtype=torch.int64, device="cuda")
+    lib().ody_dev_set_trace(buf.data_ptr())
+    prog.run()
+    lib().ody_dev_set_trace(None)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(20):
+        prog.run()
+    e.record()
+    torch.cuda.synchronize()
+    print(f"M={m} chain program: {s.elapsed_time(e) * 1e3 / 20:.2f} us/launch (incl. act quant)")
+    t = buf[:148 * 32].view(148, 32).cpu().numpy()
+    t = t[t[:, 0] > 0]
+    base = t[:, 0].min()
+
+    def stat(col):
+        v = t[:, col]
+        v = v[v > 0]
+        if not len(v):
+            return "        -          "
+        v = (v - base) / 1e3
+        return f"{v.min():6.2f}/{np.median(v):6.2f}/{v.max():6.2f} n={len(v):3d}"
+    print(f"CTAs {len(t)}  (min/median/max us from the first CTA entry)")
+    for nm, col in [("entry", 0), ("setup", 1), ("producer done", 6), ("epilogues done", 4), ("exit", 5)]:
+        print(f"  {nm:14s} {stat(col)}")
+    for i, (name, _, _) in enumerate(LAYERS):
+        print(f"  {name:8s} first MMA {stat(10 + 4 * i)}  dep released {stat(12 + 4 * i)}  last epilogue {stat(11 + 4 * i)}")
+
+
+if __name__ == "__main__":
+    for m in (1, 16):
+        main(m)
