@@ -98,6 +98,21 @@ ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out);
 ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q,
                     const ody_qtensor* w_q, ody_gemm_counters* counters, ody_tensor** out);
 
+/* Reference OTF files and float oracles (ref odyssey.h:71-75, 80-81, 100-101).
+ * ody_qtensor_read builds the DEVICE qtensor straight from an `odyssey quantize` output
+ * directory (payload.otf packed-i4 + scales.otf + scheme.txt, ref otf.cpp:121-202):
+ * per-channel 4-bit weights are prepacked into the kernel layout, per-token 8-bit
+ * activations into the a8 layout.  ody_optimize_clipping is the LWC grid search
+ * (ref clip.cpp:55-103) run on the GPU, bit-exact.  ody_matmul_f32 is the reference's
+ * fixed-order f32 matmul (its test oracle), on the GPU. */
+ody_status ody_tensor_write(const ody_tensor* t, const char* path);          /* ref odyssey.h:71 */
+ody_status ody_tensor_read(const char* path, ody_tensor** out);              /* :72 */
+ody_status ody_matmul_f32(const ody_tensor* a, const ody_tensor* b_transposed, ody_tensor** out); /* :75 */
+ody_status ody_qtensor_write(const ody_qtensor* q, const char* dir);         /* :80 */
+ody_status ody_qtensor_read(const char* dir, ody_qtensor** out);             /* :81 */
+ody_status ody_optimize_clipping(const ody_tensor* w, int bits, float grid_min, float grid_step,
+                                 float* gamma, float* beta, float* mse_before, float* mse_after); /* :100 */
+
 /* ================================================================ part 2 */
 
 typedef enum ody_dtype { ODY_DTYPE_F32 = 0, ODY_DTYPE_F16 = 1, ODY_DTYPE_BF16 = 2 } ody_dtype;

@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "core/bench.hpp"
+#include "core/clip.hpp"
+#include "core/otf.hpp"
 #include "core/gemm.hpp"
 #include "core/quantize.hpp"
 #include "core/rng.hpp"
@@ -162,6 +164,109 @@ void checksum_case(const std::string& name, std::uint64_t seed, std::size_t m, s
     end_case();
 }
 
+// The comparison engines (gemm.cpp:105-311) on one seeded input: f32 outputs + counters.
+// w8a8: 8-bit per-channel weights; finegrained: 4-bit per-group (group g); asymmetric:
+// run_engine's uint4-offset path over the per-channel 4-bit codes; w4a16: per-group
+// 4-bit weights against the dense activations.
+void engine_case(const std::string& name, std::uint64_t seed, std::size_t m, std::size_t n, std::size_t k,
+                 std::size_t g) {
+    Rng rng(seed);
+    DenseTensor a(m, k);
+    for (auto& v : a.data()) v = static_cast<float>(rng.gaussian());
+    DenseTensor w(n, k);
+    for (auto& v : w.data()) v = static_cast<float>(rng.gaussian() * 0.1);
+    QuantizedTensor a_q = quantize_activations_per_token(a, 8);
+    QuantizedTensor w4 = quantize_weights(w, per_channel(4));
+    QuantizedTensor w8 = quantize_weights(w, per_channel(8));
+    QuantScheme grp = per_channel(4);
+    grp.granularity = Granularity::PerGroup;
+    grp.group_size = g;
+    QuantizedTensor wg = quantize_weights(w, grp);
+    begin_case("engines", name);
+    out_json += "\"seed\":" + std::to_string(seed) + ",\"m\":" + std::to_string(m) + ",\"n\":" +
+                std::to_string(n) + ",\"k\":" + std::to_string(k) + ",\"group\":" + std::to_string(g) + ",";
+    emit_int_list("w8_codes", w8.payload_i8);
+    out_json += ",";
+    emit_float_bits("w8_scales_bits", w8.scales);
+    out_json += ",";
+    emit_hex("wg_packed", wg.payload_i4.bytes());
+    out_json += ",";
+    emit_float_bits("wg_scales_bits", wg.scales);
+    struct E {
+        const char* key;
+        Engine e;
+        const QuantizedTensor* wq;
+    } es[] = {{"w8a8", Engine::W8A8, &w8},
+              {"finegrained", Engine::W4A8FineGrained, &wg},
+              {"asymmetric", Engine::W4A8Asymmetric, &w4},
+              {"fast", Engine::W4A8Fast, &w4},
+              {"w4a16", Engine::W4A16Grouped, &wg}};
+    for (const E& e : es) {
+        GemmCounters c;
+        DenseTensor out = run_engine(e.e, a, a_q, *e.wq, &c);
+        out_json += ",";
+        emit_float_bits((std::string(e.key) + "_out_bits").c_str(), out.data());
+        out_json += ",\"" + std::string(e.key) + "_counters\":[" + std::to_string(c.int8_mac_ops) + "," +
+                    std::to_string(c.dequant_events) + "," + std::to_string(c.zero_point_sub_ops) + "," +
+                    std::to_string(c.final_scale_ops) + "]";
+    }
+    end_case();
+}
+
+// LWC grid search (clip.cpp:55-103) on a seeded weight, grid (0.5, 0.01) and (0.3, 0.07).
+void lwc_case(const std::string& name, std::uint64_t seed, std::size_t n, std::size_t k, int bits, float gmin,
+              float gstep) {
+    Rng rng(seed);
+    DenseTensor w(n, k);
+    for (auto& v : w.data()) v = static_cast<float>(rng.gaussian() * 0.1);
+    if (n > 2) {  // an outlier channel and an all-zero channel
+        w.at(1, 0) = 3.0f;
+        for (std::size_t c = 0; c < k; ++c) w.at(2, c) = 0.0f;
+    }
+    ClipResult r = optimize_clipping(w, bits, ClipGrid{gmin, gstep});
+    begin_case("lwc", name);
+    out_json += "\"seed\":" + std::to_string(seed) + ",\"n\":" + std::to_string(n) + ",\"k\":" +
+                std::to_string(k) + ",\"bits\":" + std::to_string(bits) + ",\"gmin_bits\":" +
+                std::to_string(bits_of(gmin)) + ",\"gstep_bits\":" + std::to_string(bits_of(gstep)) + ",";
+    emit_float_bits("w_bits", w.data());
+    out_json += ",";
+    emit_float_bits("gamma_bits", r.gamma);
+    out_json += ",";
+    emit_float_bits("beta_bits", r.beta);
+    out_json += ",";
+    emit_float_bits("mse_before_bits", r.mse_before);
+    out_json += ",";
+    emit_float_bits("mse_after_bits", r.mse_after);
+    end_case();
+}
+
+// The OTF bytes write_tensor (otf.cpp:121-153) produces for a small 4-bit tensor.
+void otf_case() {
+    Rng rng(4242);
+    DenseTensor w(3, 5);
+    for (auto& v : w.data()) v = static_cast<float>(rng.gaussian() * 0.1);
+    QuantizedTensor q = quantize_weights(w, per_channel(4));
+    const std::string dir = "/tmp/ody_golden_otf";
+    write_tensor(q, dir);
+    auto slurp = [](const std::string& p) {
+        std::vector<std::uint8_t> b;
+        FILE* f = std::fopen(p.c_str(), "rb");
+        int c;
+        while (f && (c = std::fgetc(f)) != EOF) b.push_back(static_cast<std::uint8_t>(c));
+        if (f) std::fclose(f);
+        return b;
+    };
+    begin_case("otf", "w4_3x5");
+    emit_float_bits("w_bits", w.data());
+    out_json += ",";
+    emit_hex("payload_otf", slurp(dir + "/payload.otf"));
+    out_json += ",";
+    emit_hex("scales_otf", slurp(dir + "/scales.otf"));
+    out_json += ",";
+    emit_hex("scheme_txt", slurp(dir + "/scheme.txt"));
+    end_case();
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -231,6 +336,15 @@ int main(int argc, char** argv) {
     checksum_case("cfg1_m16_n4096_k4096", 1, 16, 4096, 4096);
     checksum_case("o_m1_n5120_k5120", 1, 1, 5120, 5120);
     checksum_case("mixed_m64_n384_k5120", 1, 64, 384, 5120);
+
+    // Comparison engines and the LWC grid search (row 4).
+    engine_case("engines_m5_n40_k64_g16", 501, 5, 40, 64, 16);
+    engine_case("engines_m16_n130_k384_g128", 502, 16, 130, 384, 128);
+    engine_case("engines_m3_n7_k96_g32", 503, 3, 7, 96, 32);
+    lwc_case("lwc_n6_k64_b4", 601, 6, 64, 4, 0.5f, 0.01f);
+    lwc_case("lwc_n5_k300_b4_coarse", 602, 5, 300, 4, 0.3f, 0.07f);
+    lwc_case("lwc_n4_k128_b8", 603, 4, 128, 8, 0.5f, 0.01f);
+    otf_case();
 
     out_json += "\n]}\n";
     FILE* f = std::fopen(path, "w");

@@ -308,3 +308,148 @@ void oracle_quantize_with_scale(const float* x, size_t n, int bits, float scale,
     const int32_t hi = (1 << (bits - 1)) - 1;
     for (size_t i = 0; i < n; ++i) codes[i] = (int8_t)clamp_code(x[i] / scale, lo, hi);
 }
+
+/* ---------------------------------------------- comparison engines */
+/* proj/src/core/quantize.cpp:75-111 with PerGroup granularity: one symmetric scale per
+ * (row, group of g columns); scales laid out [row][group] (tensor.cpp:117-125). */
+int oracle_quantize_weights_per_group(const float* w, size_t n, size_t k, size_t g, int bits, int8_t* codes,
+                                      float* scales) {
+    if (g == 0 || k % g) return ORACLE_EINVAL;
+    const size_t groups = k / g;
+    for (size_t r = 0; r < n; ++r)
+        for (size_t gi = 0; gi < groups; ++gi) {
+            int rc = oracle_quantize_symmetric(w + r * k + gi * g, g, bits, 1.0f, 1.0f, codes + r * k + gi * g,
+                                               &scales[r * groups + gi]);
+            if (rc) return rc;
+        }
+    return ORACLE_OK;
+}
+
+/* proj/src/core/gemm.cpp:281-311 -- W8A8: acc = sum a*w (int32), out = float(acc)*(sa*sw) */
+void oracle_gemm_w8a8(const int8_t* a, const float* sa, const int8_t* w, const float* sw, size_t m, size_t n,
+                      size_t k, float* out) {
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            int32_t acc = 0;
+            for (size_t kk = 0; kk < k; ++kk) acc += (int32_t)a[i * k + kk] * (int32_t)w[j * k + kk];
+            out[i * n + j] = (float)acc * (sa[i] * sw[j]);
+        }
+}
+
+/* proj/src/core/gemm.cpp:123-161 -- fine-grained: per group an int32 sub-sum, then
+ * acc += float(sub) * (sa * s_group) in f32, groups in order */
+void oracle_gemm_finegrained(const int8_t* a, const float* sa, const int8_t* w, const float* ws, size_t g,
+                             size_t m, size_t n, size_t k, float* out) {
+    const size_t groups = k / g;
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            float acc = 0.0f;
+            for (size_t gi = 0; gi < groups; ++gi) {
+                int32_t sub = 0;
+                for (size_t kk = 0; kk < g; ++kk)
+                    sub += (int32_t)a[i * k + gi * g + kk] * (int32_t)w[j * k + gi * g + kk];
+                acc += (float)sub * (sa[i] * ws[j * groups + gi]);
+            }
+            out[i * n + j] = acc;
+        }
+}
+
+/* proj/src/core/gemm.cpp:163-202 + 56-75 -- asymmetric (offset) path: nibble u = q + 8,
+ * widened and 8 subtracted, acc = sum a*(u - 8), out = float(acc)*(sa*sw) */
+void oracle_gemm_asymmetric(const int8_t* a, const float* sa, const int8_t* w, const float* sw, size_t m,
+                            size_t n, size_t k, float* out) {
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            int32_t acc = 0;
+            for (size_t kk = 0; kk < k; ++kk) {
+                const uint8_t u = (uint8_t)(w[j * k + kk] + 8); /* pack_uint4_offset */
+                acc += (int32_t)a[i * k + kk] * ((int32_t)u - 8);
+            }
+            out[i * n + j] = (float)acc * (sa[i] * sw[j]);
+        }
+}
+
+/* proj/src/core/gemm.cpp:105-121 -- W4A16: f32 activations against dequantized weights,
+ * acc += a * (float(code) * scale), sequential over k (scales [row][group], g = group) */
+void oracle_gemm_w4a16(const float* a, const int8_t* w, const float* ws, size_t g, size_t m, size_t n, size_t k,
+                       float* out) {
+    const size_t groups = k / g;
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            float acc = 0.0f;
+            for (size_t kk = 0; kk < k; ++kk) {
+                const float wf = (float)w[j * k + kk] * ws[j * groups + kk / g];
+                acc += a[i * k + kk] * wf;
+            }
+            out[i * n + j] = acc;
+        }
+}
+
+/* ------------------------------------------------------------ LWC (clip.cpp) */
+/* proj/src/core/clip.cpp:11-24 -- candidate grid */
+size_t oracle_clip_candidates(float gmin, float step, float* out, size_t cap) {
+    size_t n = 0;
+    for (int i = 0; n + 1 < cap; ++i) {
+        float v = gmin + (float)i * step;
+        if (v >= 1.0f - 1e-6f) break;
+        out[n++] = v;
+    }
+    out[n++] = 1.0f;
+    return n;
+}
+
+/* proj/src/core/clip.cpp:40-51 */
+static double mse_for_scale(const float* w, size_t k, int bits, float scale) {
+    const float lo = (float)(-(1 << (bits - 1)));
+    const float hi = (float)((1 << (bits - 1)) - 1);
+    double acc = 0.0;
+    for (size_t i = 0; i < k; ++i) {
+        float c = roundf(w[i] / scale);
+        c = fmin_ref(fmax_ref(c, lo), hi);
+        double e = (double)w[i] - (double)c * (double)scale;
+        acc += e * e;
+    }
+    return acc / (double)k;
+}
+
+/* proj/src/core/clip.cpp:55-103 -- per row: the (gamma, beta) pair minimising the MSE,
+ * ties to larger gamma+beta, then larger gamma */
+int oracle_optimize_clipping(const float* w, size_t n, size_t k, int bits, float gmin, float step, float* gamma,
+                             float* beta, float* mse_before, float* mse_after) {
+    if (n * k == 0 || !(gmin > 0.0f && gmin <= 1.0f) || !(step > 0.0f)) return ORACLE_EINVAL;
+    float cand[4096];
+    const size_t nc = oracle_clip_candidates(gmin, step, cand, 4096);
+    const float qmax = (float)((1 << (bits - 1)) - 1);
+    for (size_t r = 0; r < n; ++r) {
+        const float* ch = w + r * k;
+        float wmax = ch[0], wmin = ch[0];
+        for (size_t i = 0; i < k; ++i) {
+            wmax = fmax_ref(wmax, ch[i]);
+            wmin = fmin_ref(wmin, ch[i]);
+        }
+        double best = 0.0, ident = 0.0;
+        float bg = 1.0f, bb = 1.0f;
+        int first = 1;
+        for (size_t gi = 0; gi < nc; ++gi)
+            for (size_t bi = 0; bi < nc; ++bi) {
+                const float g = cand[gi], b = cand[bi];
+                float s = fmax_ref(fabsf(g * wmax), fabsf(b * wmin)) / qmax;
+                if (!(s > 0.0f)) s = kMinScale;
+                const double mse = mse_for_scale(ch, k, bits, s);
+                if (g == 1.0f && b == 1.0f) ident = mse;
+                const int better = first || mse < best ||
+                                   (mse == best && (g + b > bg + bb || (g + b == bg + bb && g > bg)));
+                if (better) {
+                    best = mse;
+                    bg = g;
+                    bb = b;
+                    first = 0;
+                }
+            }
+        gamma[r] = bg;
+        beta[r] = bb;
+        mse_before[r] = (float)ident;
+        mse_after[r] = (float)best;
+    }
+    return ORACLE_OK;
+}

@@ -62,6 +62,20 @@ class Oracle:
                                             c_size_t, c_size_t, c_int, c_void_p]
         L.oracle_dequantize_rows.argtypes = [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p]
         L.oracle_quantize_with_scale.argtypes = [c_void_p, c_size_t, c_int, c_float, c_void_p]
+        L.oracle_quantize_weights_per_group.argtypes = [c_void_p, c_size_t, c_size_t, c_size_t, c_int,
+                                                        c_void_p, c_void_p]
+        for nm in ("oracle_gemm_w8a8", "oracle_gemm_asymmetric"):
+            getattr(L, nm).argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t,
+                                       c_void_p]
+            getattr(L, nm).restype = None
+        L.oracle_gemm_finegrained.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t,
+                                              c_size_t, c_size_t, c_void_p]
+        L.oracle_gemm_finegrained.restype = None
+        L.oracle_gemm_w4a16.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_size_t,
+                                        c_void_p]
+        L.oracle_gemm_w4a16.restype = None
+        L.oracle_optimize_clipping.argtypes = [c_void_p, c_size_t, c_size_t, c_int, c_float, c_float, c_void_p,
+                                               c_void_p, c_void_p, c_void_p]
         L.oracle_fnv1a.argtypes = [c_void_p, c_size_t]
         L.oracle_fnv1a.restype = c_uint64
         self.L = L
@@ -138,7 +152,7 @@ class Oracle:
             b.ctypes.data if b is not None else None, codes.ctypes.data, s.ctypes.data)
         if rc:
             raise ValueError("oracle: invalid weight tensor / clip")
-        return codes, self.pack_int4(codes.reshape(-1)), s
+        return codes, (self.pack_int4(codes.reshape(-1)) if bits == 4 else None), s
 
     def pack_int4(self, codes: np.ndarray) -> np.ndarray:
         codes = np.ascontiguousarray(codes, np.int8).reshape(-1)
@@ -173,6 +187,67 @@ class Oracle:
                                         sw.ctypes.data, m, n, k, threads, out.ctypes.data):
             raise ValueError("oracle: invalid gemm shape")
         return out
+
+    # ---- comparison engines + LWC (ref gemm.cpp:105-311, clip.cpp:55-103) ----
+    def quantize_weights_per_group(self, w: np.ndarray, g: int, bits: int = 4):
+        """-> (codes int8 [n,k], scales f32 [n, k/g])."""
+        w = np.ascontiguousarray(w, np.float32)
+        n, k = w.shape
+        codes = np.empty((n, k), np.int8)
+        s = np.empty((n, k // g), np.float32)
+        if self.L.oracle_quantize_weights_per_group(w.ctypes.data, n, k, g, bits, codes.ctypes.data, s.ctypes.data):
+            raise ValueError("oracle: invalid per-group quantization")
+        return codes, s
+
+    def _eng(self, fn, *arrays_and_dims):
+        return fn(*arrays_and_dims)
+
+    def gemm_w8a8(self, a_codes, sa, w_codes, sw):
+        a, w = np.ascontiguousarray(a_codes, np.int8), np.ascontiguousarray(w_codes, np.int8)
+        sa, sw = np.ascontiguousarray(sa, np.float32), np.ascontiguousarray(sw, np.float32)
+        m, k = a.shape
+        n = w.shape[0]
+        out = np.empty((m, n), np.float32)
+        self.L.oracle_gemm_w8a8(a.ctypes.data, sa.ctypes.data, w.ctypes.data, sw.ctypes.data, m, n, k,
+                                out.ctypes.data)
+        return out
+
+    def gemm_asymmetric(self, a_codes, sa, w_codes, sw):
+        a, w = np.ascontiguousarray(a_codes, np.int8), np.ascontiguousarray(w_codes, np.int8)
+        sa, sw = np.ascontiguousarray(sa, np.float32), np.ascontiguousarray(sw, np.float32)
+        m, k = a.shape
+        n = w.shape[0]
+        out = np.empty((m, n), np.float32)
+        self.L.oracle_gemm_asymmetric(a.ctypes.data, sa.ctypes.data, w.ctypes.data, sw.ctypes.data, m, n, k,
+                                      out.ctypes.data)
+        return out
+
+    def gemm_finegrained(self, a_codes, sa, w_codes, wscales, g):
+        a, w = np.ascontiguousarray(a_codes, np.int8), np.ascontiguousarray(w_codes, np.int8)
+        sa, ws = np.ascontiguousarray(sa, np.float32), np.ascontiguousarray(wscales, np.float32)
+        m, k = a.shape
+        n = w.shape[0]
+        out = np.empty((m, n), np.float32)
+        self.L.oracle_gemm_finegrained(a.ctypes.data, sa.ctypes.data, w.ctypes.data, ws.ctypes.data, g, m, n, k,
+                                       out.ctypes.data)
+        return out
+
+    def gemm_w4a16(self, a, w_codes, wscales, g):
+        a, w = np.ascontiguousarray(a, np.float32), np.ascontiguousarray(w_codes, np.int8)
+        ws = np.ascontiguousarray(wscales, np.float32)
+        m, k = a.shape
+        n = w.shape[0]
+        out = np.empty((m, n), np.float32)
+        self.L.oracle_gemm_w4a16(a.ctypes.data, w.ctypes.data, ws.ctypes.data, g, m, n, k, out.ctypes.data)
+        return out
+
+    def optimize_clipping(self, w, bits=4, gmin=0.5, gstep=0.01):
+        w = np.ascontiguousarray(w, np.float32)
+        n, k = w.shape
+        outs = [np.empty(n, np.float32) for _ in range(4)]
+        if self.L.oracle_optimize_clipping(w.ctypes.data, n, k, bits, gmin, gstep, *[o.ctypes.data for o in outs]):
+            raise ValueError("oracle: invalid clip grid")
+        return tuple(outs)
 
     # ---- full-size checker (numpy, exact) ----
     @staticmethod

@@ -97,6 +97,13 @@ SIGNATURES = {
     "ody_qtensor_import_a8": (c_int, [c_size_t, c_size_t, c_void_p, c_void_p, POINTER(c_void_p)]),
     "ody_gemm_accumulators": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ody_b200_version": (c_char_p, []),
+    "ody_tensor_write": (c_int, [c_void_p, c_char_p]),
+    "ody_tensor_read": (c_int, [c_char_p, POINTER(c_void_p)]),
+    "ody_matmul_f32": (c_int, [c_void_p, c_void_p, POINTER(c_void_p)]),
+    "ody_qtensor_write": (c_int, [c_void_p, c_char_p]),
+    "ody_qtensor_read": (c_int, [c_char_p, POINTER(c_void_p)]),
+    "ody_optimize_clipping": (c_int, [c_void_p, c_int, c_float, c_float, POINTER(c_float), POINTER(c_float),
+                                      POINTER(c_float), POINTER(c_float)]),
     "ody_comm_unique_id": (c_int, [c_void_p]),
     "ody_comm_init": (c_int, [c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "ody_comm_free": (c_int, [c_void_p]),

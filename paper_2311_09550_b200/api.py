@@ -24,7 +24,8 @@ from ._lib import (ODY_ENGINE_FAST, ODY_PER_CHANNEL, OdyError, check, lib,  # no
 
 __all__ = ["Tensor", "QTensor", "quantize_activations_per_token", "quantize_weights",
            "gemm_w4a8_fast", "gemm_w4a8_fast_accumulators", "run_engine", "dequantize",
-           "import_w4", "import_a8", "counters_fast", "OdyError"]
+           "import_w4", "import_a8", "counters_fast", "matmul_f32", "optimize_clipping",
+           "write_tensor", "read_tensor", "write_qtensor", "read_qtensor", "OdyError"]
 
 
 def _fptr(a: np.ndarray):
@@ -98,6 +99,10 @@ class QTensor:
         check(lib().ody_qtensor_export(self._h, codes.ctypes.data_as(c_void_p),
                                        scales.ctypes.data_as(c_void_p)))
         return codes, scales
+
+    def write(self, directory: str) -> None:
+        """ody_qtensor_write: the reference's OTF directory (otf.cpp:121-153)."""
+        check(lib().ody_qtensor_write(self._h, directory.encode()))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -199,3 +204,51 @@ def counters_fast(m: int, n: int, k: int) -> dict:
     return {"int8_mac_ops": m * n * k, "dequant_events": m * n, "zero_point_sub_ops": 0,
             "final_scale_ops": m * n}
 
+
+
+def matmul_f32(a, b_transposed) -> np.ndarray:
+    """ref tensor.cpp:176-196 (fixed-order f32 dots) via ody_matmul_f32."""
+    ta, tb = _as_tensor(a), _as_tensor(b_transposed)
+    h = c_void_p()
+    check(lib().ody_matmul_f32(ta._h, tb._h, byref(h)))
+    return Tensor(None, _handle=h).numpy()
+
+
+def optimize_clipping(w, bits: int = 4, grid_min: float = 0.5, grid_step: float = 0.01):
+    """ref clip.cpp:55-103 LWC grid search (GPU) via ody_optimize_clipping:
+    -> (gamma, beta, mse_before, mse_after), one value per channel."""
+    t = _as_tensor(w)
+    n = t.shape[0]
+    outs = [np.empty(n, np.float32) for _ in range(4)]
+    check(lib().ody_optimize_clipping(t._h, bits, grid_min, grid_step, *[_fptr(o) for o in outs]))
+    return tuple(outs)
+
+
+def write_tensor(t, path: str) -> None:
+    check(lib().ody_tensor_write(_as_tensor(t)._h, path.encode()))
+
+
+def read_tensor(path: str) -> np.ndarray:
+    h = c_void_p()
+    check(lib().ody_tensor_read(path.encode(), byref(h)))
+    return Tensor(None, _handle=h).numpy()
+
+
+def write_qtensor(q: QTensor, directory: str) -> None:
+    q.write(directory)
+
+
+def read_qtensor(directory: str) -> QTensor:
+    """ody_qtensor_read: an `odyssey quantize` output directory straight into the device
+    layout (per-channel INT4 weights -> prepacked tiles; per-token INT8 -> a8)."""
+    import os
+    h = c_void_p()
+    check(lib().ody_qtensor_read(directory.encode(), byref(h)))
+    kind = "w4"
+    try:
+        with open(os.path.join(directory, "scheme.txt")) as f:
+            if "bits=8" in f.read():
+                kind = "a8"
+    except OSError:
+        pass
+    return QTensor(h, kind)

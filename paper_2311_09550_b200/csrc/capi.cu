@@ -20,8 +20,12 @@
 
 #include <dlfcn.h>
 
+#include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <map>
 #include <memory>
+#include <vector>
 
 #include "../../include/odyssey_b200.h"
 #include "kernels.h"
@@ -845,6 +849,247 @@ ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q,
         run_gemm(a_q, w_q, nullptr, ad.p, st);
         cuda_check(cudaMemcpyAsync(acc, ad.p, m * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
         sync(st, "ody_gemm_accumulators");
+    });
+}
+
+// ================================================================ OTF files (ref otf.cpp)
+// The reference's on-disk tensors: "OTF1" magic, dtype code, ndim, u64 dims, payload.
+// A quantized tensor is a directory: payload.otf (packed-i4 / i8), scales.otf (f32
+// [rows, groups]), scheme.txt.  Reading one builds the DEVICE qtensor directly (prepack
+// into the kernel layout) -- the ingest path from `odyssey quantize` checkpoints.
+}  // extern "C"
+
+namespace {
+
+enum : uint8_t { kOtfF32 = 0, kOtfI8 = 1, kOtfPackedI4 = 2, kOtfI32 = 3 };
+
+struct OtfRaw {
+    uint8_t dtype = 0;
+    std::vector<uint64_t> dims;
+    std::vector<uint8_t> payload;
+    uint64_t numel() const {
+        uint64_t n = 1;
+        for (auto d : dims) n *= d;
+        return n;
+    }
+};
+
+size_t otf_payload_bytes(uint8_t dtype, uint64_t numel) {  // ref otf.cpp:16-24
+    switch (dtype) {
+        case kOtfF32: return numel * 4;
+        case kOtfI8: return numel;
+        case kOtfPackedI4: return (numel + 1) / 2;
+        case kOtfI32: return numel * 4;
+    }
+    fail(ODY_EPARSE, "unsupported dtype code");
+}
+
+void otf_write(const OtfRaw& t, const std::string& path) {  // ref otf.cpp:45-63
+    if (t.dims.empty() || t.dims.size() > 255) fail(ODY_EINVAL, "write_tensor: bad ndim");
+    if (t.payload.size() != otf_payload_bytes(t.dtype, t.numel()))
+        fail(ODY_EINVAL, "write_tensor: payload size does not match dims");
+    std::string h("OTF1", 4);
+    h.push_back(static_cast<char>(t.dtype));
+    h.push_back(static_cast<char>(t.dims.size()));
+    for (auto d : t.dims)
+        for (int i = 0; i < 8; ++i) h.push_back(static_cast<char>((d >> (8 * i)) & 0xFF));
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) fail(ODY_EIO, "write_tensor: cannot open " + path);
+    const bool ok = std::fwrite(h.data(), 1, h.size(), f) == h.size() &&
+                    std::fwrite(t.payload.data(), 1, t.payload.size(), f) == t.payload.size();
+    std::fclose(f);
+    if (!ok) fail(ODY_EIO, "write_tensor: write failed for " + path);
+}
+
+OtfRaw otf_read(const std::string& path) {  // ref otf.cpp:65-92
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) fail(ODY_EIO, "read_tensor: cannot open " + path);
+    std::vector<uint8_t> b;
+    uint8_t buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof(buf), f)) > 0) b.insert(b.end(), buf, buf + n);
+    std::fclose(f);
+    if (b.size() < 6) fail(ODY_EPARSE, "read_tensor: truncated header in " + path);
+    if (std::memcmp(b.data(), "OTF1", 4) != 0) fail(ODY_EPARSE, "read_tensor: bad magic in " + path);
+    if (b[4] > 3) fail(ODY_EPARSE, "read_tensor: unsupported dtype code " + std::to_string(b[4]) + " in " + path);
+    OtfRaw t;
+    t.dtype = b[4];
+    const size_t ndim = b[5], off = 6 + ndim * 8;
+    if (b.size() < off) fail(ODY_EPARSE, "read_tensor: truncated dims in " + path);
+    for (size_t i = 0; i < ndim; ++i) {
+        uint64_t d = 0;
+        for (int j = 0; j < 8; ++j) d |= static_cast<uint64_t>(b[6 + i * 8 + j]) << (8 * j);
+        t.dims.push_back(d);
+    }
+    if (b.size() - off != otf_payload_bytes(t.dtype, t.numel()))
+        fail(ODY_EPARSE, "read_tensor: truncated payload in " + path);
+    t.payload.assign(b.begin() + static_cast<std::ptrdiff_t>(off), b.end());
+    return t;
+}
+
+std::vector<float> otf_floats(const OtfRaw& r) {
+    if (r.dtype != kOtfF32) fail(ODY_EPARSE, "expected f32 tensor");
+    std::vector<float> v(r.numel());
+    std::memcpy(v.data(), r.payload.data(), r.payload.size());
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+ody_status ody_tensor_write(const ody_tensor* t, const char* path) {
+    if (!t || !path) return einval("ody_tensor_write: null argument");
+    return guarded([&] {
+        OtfRaw r;
+        r.dtype = kOtfF32;
+        r.dims = {t->rows, t->cols};
+        r.payload.resize(t->rows * t->cols * 4);
+        std::memcpy(r.payload.data(), t->data, r.payload.size());
+        otf_write(r, path);
+    });
+}
+
+ody_status ody_tensor_read(const char* path, ody_tensor** out) {
+    if (!path || !out) return einval("ody_tensor_read: null argument");
+    return guarded([&] {
+        OtfRaw r = otf_read(path);  // ref otf.cpp:155-162 read_dense
+        if (r.dtype != kOtfF32) fail(ODY_EPARSE, std::string("read_dense: ") + path + " is not f32");
+        if (r.dims.size() != 2) fail(ODY_EPARSE, "read_dense: expected 2 dims");
+        std::vector<float> v = otf_floats(r);
+        for (float x : v)
+            if (!std::isfinite(x)) fail(ODY_EINVAL, "DenseTensor: non-finite value");
+        ody_tensor* t = new_tensor(r.dims[0], r.dims[1]);
+        std::memcpy(t->data, v.data(), v.size() * 4);
+        *out = t;
+    });
+}
+
+ody_status ody_matmul_f32(const ody_tensor* a, const ody_tensor* b_transposed, ody_tensor** out) {
+    if (!a || !b_transposed || !out) return einval("ody_matmul_f32: null argument");
+    return guarded([&] {
+        if (a->cols != b_transposed->cols)
+            fail(ODY_EINVAL, "matmul_f32: inner dims disagree (" + std::to_string(a->cols) + " vs " +
+                                 std::to_string(b_transposed->cols) + ")");
+        cudaStream_t st = rt().stream;
+        const size_t m = a->rows, n = b_transposed->rows, k = a->cols;
+        DevBuf<float> ad(std::max<size_t>(m * k, 1), st), bd(std::max<size_t>(n * k, 1), st), od(std::max<size_t>(m * n, 1), st);
+        cuda_check(cudaMemcpyAsync(ad.p, a->data, m * k * 4, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(bd.p, b_transposed->data, n * k * 4, cudaMemcpyHostToDevice, st), "H2D");
+        if (m * n > 0)
+            cuda_check(launch_matmul_f32(ad.p, bd.p, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                                         od.p, st),
+                       "matmul_f32 launch");
+        ody_tensor* t = new_tensor(m, n);
+        cuda_check(cudaMemcpyAsync(t->data, od.p, m * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        sync(st, "ody_matmul_f32");
+        *out = t;
+    });
+}
+
+ody_status ody_qtensor_write(const ody_qtensor* q, const char* dir) {
+    if (!q || !dir) return einval("ody_qtensor_write: null argument");
+    return guarded([&] {
+        std::error_code ec;
+        std::filesystem::create_directories(dir, ec);
+        const size_t r = q->rows, c = q->cols;
+        OtfRaw pay, sc;
+        pay.dims = {r, c};
+        std::vector<float> scales(r);
+        if (q->kind == QKind::Act8) {
+            pay.dtype = kOtfI8;
+            pay.payload.resize(r * c);
+        } else {
+            pay.dtype = kOtfPackedI4;
+            pay.payload.resize((r * c + 1) / 2);
+        }
+        const ody_status st = ody_qtensor_export(q, pay.payload.data(), scales.data());
+        if (st != ODY_OK) fail(st, g_last_error);
+        const std::string d(dir);
+        otf_write(pay, d + "/payload.otf");
+        sc.dtype = kOtfF32;
+        sc.dims = {r, 1};
+        sc.payload.resize(r * 4);
+        std::memcpy(sc.payload.data(), scales.data(), r * 4);
+        otf_write(sc, d + "/scales.otf");
+        std::FILE* f = std::fopen((d + "/scheme.txt").c_str(), "w");
+        if (!f) fail(ODY_EIO, "write_tensor: cannot open " + d + "/scheme.txt");
+        std::fprintf(f, "bits=%d\nsymmetric=1\ngranularity=%s\ngroup_size=0\n", q->kind == QKind::Act8 ? 8 : 4,
+                     q->kind == QKind::Act8 ? "per_token" : "per_channel");
+        std::fclose(f);
+    });
+}
+
+ody_status ody_qtensor_read(const char* dir, ody_qtensor** out) {
+    if (!dir || !out) return einval("ody_qtensor_read: null argument");
+    return guarded([&] {
+        const std::string d(dir);
+        std::FILE* f = std::fopen((d + "/scheme.txt").c_str(), "r");  // ref otf.cpp:164-173
+        if (!f) fail(ODY_EIO, "read_tensor: missing scheme.txt in " + d);
+        std::map<std::string, std::string> kv;
+        char line[512];
+        while (std::fgets(line, sizeof(line), f)) {
+            std::string l(line);
+            while (!l.empty() && (l.back() == '\n' || l.back() == '\r')) l.pop_back();
+            const size_t eq = l.find('=');
+            if (eq != std::string::npos) kv[l.substr(0, eq)] = l.substr(eq + 1);
+        }
+        std::fclose(f);
+        for (const char* key : {"bits", "symmetric", "granularity", "group_size"})
+            if (!kv.count(key)) fail(ODY_EINVAL, std::string("read_tensor: scheme.txt lacks ") + key);
+        const int bits = std::stoi(kv["bits"]);
+        const bool sym = kv["symmetric"] == "1";
+        const std::string gran = kv["granularity"];
+        if (bits != 4 && bits != 8) fail(ODY_EINVAL, "QuantScheme: bits must be 4 or 8");
+        OtfRaw pay = otf_read(d + "/payload.otf");  // ref otf.cpp:179-197
+        if (pay.dims.size() != 2) fail(ODY_EPARSE, "quantized payload: expected 2 dims");
+        const size_t r = pay.dims[0], c = pay.dims[1];
+        if (bits == 4 && pay.dtype != kOtfPackedI4) fail(ODY_EPARSE, "4-bit tensor payload must be packed-i4");
+        if (bits == 8 && pay.dtype != kOtfI8) fail(ODY_EPARSE, "8-bit tensor payload must be i8");
+        std::vector<float> scales = otf_floats(otf_read(d + "/scales.otf"));
+        if (!sym) fail(ODY_EINVAL, "read_tensor: asymmetric tensors are not supported on the B200 path");
+        if (scales.size() != r) fail(ODY_EINVAL, "QuantizedTensor: scales size mismatch");
+        if (bits == 4 && gran == "per_channel") {
+            const ody_status st = ody_qtensor_import_w4(r, c, pay.payload.data(), scales.data(), out);
+            if (st != ODY_OK) fail(st, g_last_error);
+        } else if (bits == 8 && gran == "per_token") {
+            const ody_status st = ody_qtensor_import_a8(r, c, reinterpret_cast<const int8_t*>(pay.payload.data()),
+                                                        scales.data(), out);
+            if (st != ODY_OK) fail(st, g_last_error);
+        } else {
+            fail(ODY_EINVAL, "read_tensor: " + std::to_string(bits) + "-bit " + gran +
+                                 " tensors are not supported on the B200 path");
+        }
+    });
+}
+
+// ref clip.cpp:55-103 (LWC grid search) on the GPU, bit-exact: per channel, the
+// (gamma, beta) pair of the candidate grid minimising the quantization MSE.
+ody_status ody_optimize_clipping(const ody_tensor* w, int bits, float grid_min, float grid_step, float* gamma,
+                                 float* beta, float* mse_before, float* mse_after) {
+    if (!w) return einval("ody_optimize_clipping: null tensor");
+    return guarded([&] {
+        if (w->rows * w->cols == 0) fail(ODY_EINVAL, "optimize_clipping: empty weight");
+        if (!(grid_min > 0.0f && grid_min <= 1.0f) || !(grid_step > 0.0f))
+            fail(ODY_EINVAL, "ClipGrid: need 0 < min <= 1 and step > 0");
+        if (bits != 4 && bits != 8) fail(ODY_EINVAL, "QuantScheme: bits must be 4 or 8");
+        if ((1.0f - grid_min) / grid_step > static_cast<float>(lwc_max_candidates() - 2))
+            fail(ODY_EINVAL, "optimize_clipping: candidate grid too fine for the GPU kernel");
+        if (w->cols > 50 * 1024) fail(ODY_EINVAL, "optimize_clipping: rows longer than 51200 elements");
+        cudaStream_t st = rt().stream;
+        const size_t n = w->rows, k = w->cols;
+        DevBuf<float> wd(n * k, st), outd(4 * n, st);
+        cuda_check(cudaMemcpyAsync(wd.p, w->data, n * k * 4, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(launch_lwc_grid(wd.p, static_cast<int>(n), static_cast<int>(k), bits, grid_min, grid_step,
+                                   outd.p, outd.p + n, outd.p + 2 * n, outd.p + 3 * n, st),
+                   "lwc launch");
+        std::vector<float> h(4 * n);
+        cuda_check(cudaMemcpyAsync(h.data(), outd.p, 4 * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        sync(st, "ody_optimize_clipping");
+        if (gamma) std::memcpy(gamma, h.data(), n * 4);
+        if (beta) std::memcpy(beta, h.data() + n, n * 4);
+        if (mse_before) std::memcpy(mse_before, h.data() + 2 * n, n * 4);
+        if (mse_after) std::memcpy(mse_after, h.data() + 3 * n, n * 4);
     });
 }
 

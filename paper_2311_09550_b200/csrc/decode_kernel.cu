@@ -37,9 +37,11 @@
 //          (w<<4)&0xF0F0F0F0 / w&0xF0F0F0F0 int8 lanes (the paper's SINT4->S8 trick) ->
 //          tcgen05.st
 //   8..11  epilogue: tcgen05.ld D -> DSMEM reduce-scatter -> >>4, scale, store
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -121,6 +123,10 @@ struct LinDesc {
 };
 
 struct PParams {
+    // dependent linears (dynamic chain): 2-D TMA maps of their x ({K, M} 16-bit, row
+    // stride ldx, box {256, BN}) -- the producer stages each unit's x slice with ONE
+    // tensor copy; out-of-range rows / columns arrive as zeros
+    alignas(64) CUtensorMap xmap[kMaxLin];
     LinDesc lin[kMaxLin];
     int L;
     int S, C;             // cluster size (split-K factor), clusters
@@ -907,10 +913,11 @@ constexpr int kDynConvGroups = 2;
 constexpr int kDynEpi0 = 12;
 constexpr int kItemSlots = 8;
 // Per-BN configuration of the dynamic kernel (BN = 16/32/64 tokens per MMA N).
-template <int BN>
+template <int BN, bool DEP>
 struct DynCfg {
     static constexpr int kBBlock = BN * 128;                            // one B k-block tile
-    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock;  // weights + B tiles
+    static constexpr int kXBytes = DEP ? BN * 2 * kUnitBlocks * kBlockK : 0;  // staged 16-bit x slice
+    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock + kXBytes;  // weights + B (+ x)
     static constexpr int kStages = (220 * 1024 - 3072) / kStageBytes < 10 ? (220 * 1024 - 3072) / kStageBytes : 10;
     static constexpr int kSmem = kStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
@@ -938,9 +945,9 @@ __device__ __forceinline__ DynItem dyn_item(const PParams& p, int it) {
     return x;
 }
 
-template <int BN>
+template <int BN, bool DEP>
 __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
-    using C = DynCfg<BN>;
+    using C = DynCfg<BN, DEP>;
     constexpr int kDynStages = C::kStages;
     constexpr int kStageBytes = C::kStageBytes;
     constexpr int kBBlockBytes = C::kBBlock;
@@ -957,12 +964,17 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint64_t* d_empty = d_full + kDBufs;
     uint64_t* i_full = d_empty + kDBufs;
     uint64_t* i_empty = i_full + kItemSlots;
-    int* items = reinterpret_cast<int*>(i_empty + kItemSlots);
+    uint64_t* x_full = i_empty + kItemSlots;  // DEP: the unit's x slice landed (every unit: one phase)
+    int* items = reinterpret_cast<int*>(x_full + kDynStages);
     uint32_t* flag = reinterpret_cast<uint32_t*>(items + kItemSlots);
     uint32_t* tmem_slot = flag + 1;
+    float* bsc = reinterpret_cast<float*>(tmem_slot + 1);  // DEP: per-token scale / reciprocal
+    float* brcp = bsc + 64;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
+    // diagnostics: per-unit timeline of the LAST CTA (first 64 units, 8 slots each)
+    unsigned long long* utr = (p.trace && blockIdx.x == gridDim.x - 1) ? p.trace + 148 * kTraceCta : nullptr;
     if (trc && threadIdx.x == 0) trc[0] = globaltimer();
     if (p.pdl) pdl_launch_dependents();
     if (threadIdx.x == 0) {
@@ -979,9 +991,10 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], 4);
         }
+        for (int i = 0; i < kDynStages; ++i) mbar_init(&x_full[i], 1);
         for (int i = 0; i < kItemSlots; ++i) {
             mbar_init(&i_full[i], 1);
-            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4 + 2);  // MMA + converter + epilogue + B warps
+            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4 + (DEP ? 2 : 0));  // MMA, converter, epilogue (+B) warps
         }
         fence_mbar_init();
     }
@@ -1029,10 +1042,82 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 waited = true;
                 for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], dst[i], dkb[i], dnb[i]);
             };
+            // DEP: x-slice copies of dependent units wait until the producer linear is
+            // complete (its `done` reached the item count -- only trusted after
+            // griddepcontrol.wait, the previous launch re-arms the counters); until then
+            // they are deferred and the weight stream keeps going.  Every blocking wait
+            // below polls so that a released dependency's copies go out meanwhile.
+            int xq[DEP ? kDynStages : 1], xst[DEP ? kDynStages : 1], xkb[DEP ? kDynStages : 1], nx = 0;
+            uint32_t rel_mask = 0u;
+            auto released = [&](int l) -> bool {
+                if ((rel_mask >> l) & 1u) return true;
+                if (!waited) return false;
+                const LinDesc& dl = p.lin[l];
+                if (ld_acquire_u32(dl.dep_done) < dl.dep_target) return false;
+                fence_proxy_async_global();  // the producer's generic writes -> our tensor copies
+                rel_mask |= 1u << l;
+                return true;
+            };
+            auto issue_x = [&](int l, int s, int kb) {
+                if (utr) utr[8 * 63 + 7] = globaltimer();  // last x issue
+                mbar_expect_tx(&x_full[s], C::kXBytes);
+                tma_load_2d(ring + s * kStageBytes + kUnitBytes + kUnitBlocks * kBBlockBytes, &p.xmap[l],
+                            kb * kBlockK, 0, &x_full[s]);
+            };
+            auto flush_x = [&]() {
+                int keep = 0;
+                for (int i = 0; i < nx; ++i) {
+                    if (released(xq[i])) {
+                        issue_x(xq[i], xst[i], xkb[i]);
+                    } else {
+                        xq[keep] = xq[i];
+                        xst[keep] = xst[i];
+                        xkb[keep] = xkb[i];
+                        ++keep;
+                    }
+                }
+                nx = keep;
+            };
+            // Both issuing lanes wait TOGETHER (called convergently; `need` false for a lane
+            // with nothing to wait on): each keeps flushing its own deferred copies while the
+            // other waits, so neither can sit at the warp barrier holding a copy the other
+            // lane's ring slot depends on.
+            // The dependency counters are polled by lane 0 ONLY, with back-off: with most
+            // CTAs waiting on one linear, per-role polling at ~100 ns saturated the L2 slice
+            // holding the counter and slowed every CTA still streaming (trace: 2 us/unit).
+            auto wait_poll = [&](uint64_t* bar, uint32_t par, bool need) {
+                if (!DEP) {
+                    if (need) mbar_wait(bar, par);
+                    return;
+                }
+                uint32_t ns = 128;
+                while (true) {
+                    const bool ok = !need || mbar_test(bar, par);
+                    if (__all_sync(0x3u, ok)) break;
+                    const uint32_t want = nx ? (1u << xq[0]) : 0u;
+                    const uint32_t want_all = (want | __shfl_xor_sync(0x3u, want, 1)) & ~rel_mask;
+                    uint32_t newly = 0u;
+                    if (lane == 0 && waited)
+                        for (uint32_t m = want_all; m; m &= m - 1) {
+                            const int l = __ffs(m) - 1;
+                            if (ld_acquire_u32(p.lin[l].dep_done) >= p.lin[l].dep_target) newly |= 1u << l;
+                        }
+                    newly = __shfl_sync(0x3u, newly, 0);
+                    if (newly) {
+                        fence_proxy_async_global();  // the producer linear's writes -> our tensor copies
+                        rel_mask |= newly;
+                        flush_x();
+                        ns = 128;
+                    } else {
+                        __nanosleep(ns);
+                        ns = ns < 1024 ? 2 * ns : 1024;
+                    }
+                }
+            };
             int U = 0;
             for (int j = 0;; ++j) {
                 const int is = j % kItemSlots;
-                if (j >= kItemSlots) mbar_wait(&i_empty[is], ((j / kItemSlots) & 1) ^ 1);
+                wait_poll(&i_empty[is], ((j / kItemSlots) & 1) ^ 1, j >= kItemSlots);
                 // item 0 of every CTA is static (blockIdx.x), so the weight stream starts at
                 // once; the shared counter is only touched after griddepcontrol.wait, i.e.
                 // once the previous launch (which re-arms it) has completed
@@ -1062,17 +1147,31 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
                     if (!waited && U + k0 + 1 >= kDynStages) release_deferred();
                     const int k = k0 + lane;
+                    {
+                        const int Uk = U + k;
+                        wait_poll(&w_empty[Uk % kDynStages], ((Uk / kDynStages) & 1) ^ 1,
+                                  k < nunits && Uk >= kDynStages);
+                    }
                     if (k < nunits) {
                         const int Uk = U + k;
                         const int s = Uk % kDynStages;
                         const int kb = x.kb_lo + kUnitBlocks * k;
                         const int nb = min(kUnitBlocks, x.kb_hi - kb);
-                        if (Uk >= kDynStages) mbar_wait(&w_empty[s], ((Uk / kDynStages) & 1) ^ 1);
                         mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
                         bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol);
-                        if (depi) {
-                            // no B copy: the B-quantizer warps write the tiles and arrive on b_full
+                        if (utr && Uk < 64) utr[8 * Uk + 0] = globaltimer();
+                        if (DEP && !depi) mbar_arrive(&x_full[s]);  // x_full: one phase per unit
+                        if (DEP && depi) {
+                            // no B copy: the B-quantizer warps quantize the staged x slice
+                            if (released(x.l)) {
+                                issue_x(x.l, s, kb);
+                            } else {
+                                xq[nx] = x.l;
+                                xst[nx] = s;
+                                xkb[nx] = kb;
+                                ++nx;
+                            }
                         } else if (waited) {
                             issue_b(d, s, kb, nb);
                         } else {
@@ -1088,6 +1187,13 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 U += nunits;
             }
             if (!waited) release_deferred();
+            for (uint32_t ns = 128; nx;) {
+                flush_x();
+                if (nx) {
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? 2 * ns : 1024;
+                }
+            }
             if (trc && lane == 0) trc[6] = globaltimer();
         }
     } else if (warp == kWarpMma) {
@@ -1111,7 +1217,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 const int as = U % kAStages;
                 const int s = U % kDynStages;
                 mbar_wait(&a_full[as], (U / kAStages) & 1);
+                if (utr && lane == 0 && U < 64) utr[8 * U + 1] = globaltimer();
                 mbar_wait(&b_full[s], (U / kDynStages) & 1);
+                if (utr && lane == 0 && U < 64) utr[8 * U + 6] = globaltimer();
                 tc_fence_after();
                 const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
                 const uint32_t b0 = smem_u32(ring) + s * kStageBytes + kUnitBytes;
@@ -1129,22 +1237,16 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             ++JD;
         }
-    } else if (warp == kWarpAlloc || warp == kWarpAlloc + 1) {
-        // B-quantizer (warps 2-3, idle once TMEM is allocated): for a DEPENDENT linear --
-        // x is an earlier linear's 16-bit output, complete once that linear's `done`
-        // reaches its item count -- quantize each unit's B tiles straight into the ring
-        // stage (quant16: bit-exact with the act-quant kernel), as soon as the stage's
-        // previous unit has been consumed (w_empty), so the x loads' L2 latency overlaps
-        // the weight stream; then arrive on b_full.  The token scale S = max/127 (IEEE;
-        // 0 -> 2^-24, ref quantize.cpp:22-35) comes from the row maxima the producer
-        // linear's epilogues accumulated.
-        constexpr int kTpt = 64 / BN < 1 ? 1 : 64 / BN;       // threads per token
-        constexpr int kCpt = 16 / kTpt;                        // 16-element chunks per thread per unit
-        const int qt = threadIdx.x - kWarpAlloc * 32;          // 0..63
-        const int bt = BN >= 64 ? qt : qt / kTpt;              // token row of this thread
-        const int bj = BN >= 64 ? 0 : qt % kTpt;
+    } else if (DEP && (warp == kWarpAlloc || warp == kWarpAlloc + 1)) {
+        // B-quantizer (warps 2-3, idle once TMEM is allocated).  A DEPENDENT linear's x
+        // is an earlier linear's 16-bit output; the producer stages each unit's slice of it
+        // ([BN tokens][256 k] by one TMA tensor copy, issued once that linear completed).
+        // Quantize it from shared memory into the unit's B tiles (quant16: bit-exact with
+        // the act-quant kernel), then arrive on b_full.  Token scale S = max/127 (IEEE;
+        // 0 -> 2^-24, ref quantize.cpp:22-35) from the row maxima the producer linear's
+        // epilogues accumulated.  Every unit completes one x_full phase (in order).
+        const int qt = threadIdx.x - kWarpAlloc * 32;  // 0..63
         int U = 0;
-        bool pdl_done = false;
         for (int j = 0;; ++j) {
             const int is = j % kItemSlots;
             mbar_wait(&i_full[is], (j / kItemSlots) & 1);
@@ -1155,60 +1257,47 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             const DynItem x = dyn_item(p, it);
             const LinDesc& d = p.lin[x.l];
             const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
-            if (d.dep_done == nullptr) {
-                U += nunits;
-                continue;
-            }
-            if (!pdl_done) {
-                if (p.pdl) pdl_wait();  // the previous launch re-armed the chain counters
-                pdl_done = true;
-            }
-            if (lane == 0)
-                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(20);
-            __syncwarp();
-            (void)ld_acquire_u32(d.dep_done);
-            if (trc && qt == 0 && x.l < 4 && trc[12 + 4 * x.l] == 0) trc[12 + 4 * x.l] = globaltimer();
-            const bool live = bt < d.M;
-            float sc = 1.0f, rcp = 1.0f;
-            if (live) {
-                sc = __uint_as_float(__ldcg(d.amax_src + bt)) / 127.0f;
-                if (!(sc > 0.0f)) sc = kMinScale;
-                rcp = 1.0f / sc;
-            }
-            const unsigned short* xrow = static_cast<const unsigned short*>(d.x) +
-                                         static_cast<size_t>(live ? bt : 0) * d.ldx;
+            const bool depi = d.dep_done != nullptr;
             for (int u = 0; u < nunits; ++u, ++U) {
                 const int s = U % kDynStages;
-                const int kb = x.kb_lo + kUnitBlocks * u;
-                const int nb = min(kUnitBlocks, x.kb_hi - kb);
-                const uint32_t bb = smem_u32(ring) + s * kStageBytes + kUnitBytes;
-                constexpr int kBatch = kCpt < 8 ? kCpt : 8;  // chunk loads in flight per thread
-#pragma unroll
-                for (int cb = 0; cb < kCpt; cb += kBatch) {
-                    uint4 raw[kBatch][2];
-#pragma unroll
-                    for (int c2 = 0; c2 < kBatch; ++c2) {
-                        const int ch = bj * kCpt + cb + c2;
-                        const int b = ch >> 3, c = ch & 7;
-                        if (live && b < nb)
-                            load16_raw(xrow, (kb + b) * kBlockK + c * 16, d.K, true, raw[c2][0], raw[c2][1]);
+                mbar_wait(&x_full[s], (U / kDynStages) & 1);
+                if (utr && qt == 0 && U < 64) utr[8 * U + 2] = globaltimer();
+                if (!depi) continue;
+                if (u == 0) {
+                    // the producer issues x copies only after it acquired the producer
+                    // linear's completion; x_full (its release arrive) passes that on
+                    if (trc && qt == 0 && x.l < 4 && trc[12 + 4 * x.l] == 0) trc[12 + 4 * x.l] = globaltimer();
+                    if (qt < BN) {
+                        float sc = 1.0f;
+                        if (qt < d.M) {
+                            sc = __uint_as_float(__ldcg(d.amax_src + qt)) / 127.0f;
+                            if (!(sc > 0.0f)) sc = kMinScale;
+                        }
+                        bsc[qt] = sc;
+                        brcp[qt] = 1.0f / sc;
                     }
-                    // the stage's B region is free once its previous unit's MMAs completed
-                    if (cb == 0 && U >= kDynStages) mbar_wait(&w_empty[s], ((U / kDynStages) & 1) ^ 1);
+                    named_bar_sync(4, 64);
+                }
+                const int nb = min(kUnitBlocks, x.kb_hi - (x.kb_lo + kUnitBlocks * u));
+                const uint32_t bb = smem_u32(ring) + s * kStageBytes + kUnitBytes;
+                const uint32_t xs = bb + kUnitBlocks * kBBlockBytes;
 #pragma unroll
-                    for (int c2 = 0; c2 < kBatch; ++c2) {
-                        const int ch = bj * kCpt + cb + c2;
-                        const int b = ch >> 3, c = ch & 7;
-                        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                        if (live && b < nb)
-                            v = d.x_bf16 ? quant16<true>(raw[c2][0], raw[c2][1], sc, rcp, 0)
-                                         : quant16<false>(raw[c2][0], raw[c2][1], sc, rcp, 0);
-                        if (b < nb) sts128(bb + b * kBBlockBytes + bt * 128 + ((c ^ (bt & 7)) << 4), v);
+                for (int i = 0; i < BN / 4; ++i) {  // BN rows x 16 sixteen-element chunks
+                    const int task = qt + 64 * i;
+                    const int t = task >> 4, c16 = task & 15;
+                    const int b = c16 >> 3, c = c16 & 7;
+                    if (b < nb) {
+                        const uint4 r0 = lds128(xs + t * 512 + c16 * 32);
+                        const uint4 r1 = lds128(xs + t * 512 + c16 * 32 + 16);
+                        const uint4 v = d.x_bf16 ? quant16<true>(r0, r1, bsc[t], brcp[t], 0)
+                                                 : quant16<false>(r0, r1, bsc[t], brcp[t], 0);
+                        sts128(bb + b * kBBlockBytes + t * 128 + ((c ^ (t & 7)) << 4), v);
                     }
                 }
                 fence_proxy_async_shared();  // generic smem writes -> the MMA's async proxy
                 named_bar_sync(4, 64);
                 if (qt == 0) mbar_arrive(&b_full[s]);
+                if (utr && qt == 0 && U < 64) utr[8 * U + 3] = globaltimer();
             }
         }
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kDynConvGroups) {
@@ -1232,6 +1321,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 const int s = U % kDynStages;
                 const int as = U % kAStages;
                 mbar_wait(&w_full[s], (U / kDynStages) & 1);
+                if (utr && r == 0 && U < 64) utr[8 * U + 4] = globaltimer();
                 const uint32_t src = smem_u32(ring) + s * kStageBytes + r * 16;
                 uint32_t lanes8[kUnitBlocks][32];
 #pragma unroll
@@ -1260,6 +1350,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[as]);
+                if (utr && r == 0 && U < 64) utr[8 * U + 5] = globaltimer();
             }
         }
     } else if (warp >= kDynEpi0) {
@@ -1331,9 +1422,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             const bool depi = d.dep_done != nullptr;
             if (depi) {
                 // in-kernel quantized x: the token scales follow from the producer's row
-                // maxima exactly as the converters derived them (complete by now: the MMAs
-                // consumed B tiles quantized after the producer finished)
-                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(32);
+                // maxima exactly as the B-quantizer derived them (complete by now: the MMAs
+                // consumed B tiles quantized after the producer finished); one acquire
+                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(256);
             }
             const bool own = fin && n < d.N;
             const bool amx = d.amax_dst != nullptr && n >= d.amax_c0 && n < d.amax_c1;
@@ -1478,32 +1569,61 @@ __global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __
         quant_row<false>(b, i, t, red);
 }
 
-template <int BN>
+template <int BN, bool DEP>
 cudaError_t ensure_dyn_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   DynCfg<BN>::kSmem);
+        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel<BN, DEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   DynCfg<BN, DEP>::kSmem);
     });
     return err;
 }
 
-template <int BN>
+template <int BN, bool DEP>
 cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st) {
-    const cudaError_t ed = ensure_dyn_attr<BN>();
+    const cudaError_t ed = ensure_dyn_attr<BN, DEP>();
     if (ed != cudaSuccess) return ed;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.C);
     cfg.blockDim = dim3(kDynThreads);
-    cfg.dynamicSmemBytes = DynCfg<BN>::kSmem;
+    cfg.dynamicSmemBytes = DynCfg<BN, DEP>::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN>, p);
+    return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN, DEP>, p);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// The 2-D map of a dependent linear's 16-bit x: dims {K, M}, row stride ldx elements,
+// box {256 (one pipeline unit of k), BN tokens}, no swizzle, zero fill out of range.
+bool encode_x_map(CUtensorMap* map, const void* x, int x_dtype, size_t ldx, int M, int K, int BN) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kUnitBlocks * kBlockK), static_cast<cuuint32_t>(BN)};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, x_dtype == kDtypeBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+               const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int dyn_bn(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
@@ -1901,10 +2021,14 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
         int mmax = 1;
         for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
-        switch (dyn_bn(mmax)) {
-            case 16: return launch_dyn<16>(p, prog_pdl, st);
-            case 32: return launch_dyn<32>(p, prog_pdl, st);
-            default: return launch_dyn<64>(p, prog_pdl, st);
+        const int bn = dyn_bn(mmax);
+        for (int l = 0; l < L; ++l)
+            if (p.lin[l].dep >= 0 && !encode_x_map(&p.xmap[l], a[l].x, a[l].x_dtype, a[l].ldx, a[l].M, a[l].K, bn))
+                return cudaErrorInvalidValue;
+        switch (bn) {
+            case 16: return launch_dyn<16, true>(p, prog_pdl, st);
+            case 32: return launch_dyn<32, true>(p, prog_pdl, st);
+            default: return launch_dyn<64, true>(p, prog_pdl, st);
         }
     }
     if (dyn) {
@@ -1940,9 +2064,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         int mmax = 1;
         for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
         switch (dyn_bn(mmax)) {
-            case 16: return launch_dyn<16>(p, prog_pdl, st);
-            case 32: return launch_dyn<32>(p, prog_pdl, st);
-            default: return launch_dyn<64>(p, prog_pdl, st);
+            case 16: return launch_dyn<16, false>(p, prog_pdl, st);
+            case 32: return launch_dyn<32, false>(p, prog_pdl, st);
+            default: return launch_dyn<64, false>(p, prog_pdl, st);
         }
     }
     cudaLaunchConfig_t cfg = {};

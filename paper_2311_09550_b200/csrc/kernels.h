@@ -134,4 +134,12 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
 
 int device_sm_count();
 
+// aux_kernels.cu: the reference's offline / float-oracle numerics, bit-exact.
+// LWC grid search (ref clip.cpp:55-103): w is N x K f32 on the device; per-row outputs.
+int lwc_max_candidates();
+cudaError_t launch_lwc_grid(const float* w, int N, int K, int bits, float grid_min, float grid_step, float* gamma,
+                            float* beta, float* mse_before, float* mse_after, cudaStream_t st);
+// matmul_f32 (ref tensor.cpp:176-196): out = a (M x K) . bt (N x K)^T, sequential f32 dots.
+cudaError_t launch_matmul_f32(const float* a, const float* bt, int M, int N, int K, float* out, cudaStream_t st);
+
 }  // namespace odyb200

@@ -73,6 +73,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
         : "memory");
 }
 
+// 2-D TMA tensor load (cp.async.bulk.tensor, tile mode) of the box at (c0 = inner, c1 =
+// outer) of the tensor map `map` (a __grid_constant__ parameter) into shared memory,
+// completing its bytes on `bar`.  Out-of-bound elements are zero-filled.
+__device__ __forceinline__ void tma_load_2d(void* dst_smem, const void* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst_smem)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Shared -> global 1-D bulk store (bulk-group completion).
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),

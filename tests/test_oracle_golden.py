@@ -213,3 +213,47 @@ def test_acceptance_matrix_cases_oracle(oracle):
         acc = oracle.fast_accumulators(codes, packed, m, n, k)
         assert np.all(acc % 16 == 0)
         assert np.array_equal(acc >> 4, codes.astype(np.int64) @ wcodes.astype(np.int64).T)
+
+
+def _engine_inputs(oracle, c):
+    r = oracle.rng(c["seed"])
+    a = oracle.gaussian_fill(r, (c["m"], c["k"]))
+    w = oracle.gaussian_fill(r, (c["n"], c["k"]), 0.1)
+    return a, w
+
+
+def test_comparison_engines_vs_reference(oracle, golden):
+    """gemm.cpp:105-311 restated (W8A8, fine-grained, asymmetric, W4A16) == the
+    reference's outputs bit for bit on its own seeded inputs (gen_golden engine_case)."""
+    cs = [c for c in golden if c["kind"] == "engines"]
+    assert len(cs) >= 3
+    for c in cs:
+        a, w = _engine_inputs(oracle, c)
+        g = c["group"]
+        codes, sa = oracle.quantize_activations(a)
+        w8, _, s8 = oracle.quantize_weights(w, bits=8)
+        assert w8.reshape(-1).tolist() == c["w8_codes"]
+        assert np.array_equal(bits_of(s8), np.asarray(c["w8_scales_bits"], np.uint32))
+        wg, sg = oracle.quantize_weights_per_group(w, g)
+        assert np.array_equal(oracle.pack_int4(wg.reshape(-1)), hex_bytes(c["wg_packed"]))
+        assert np.array_equal(bits_of(sg).reshape(-1), np.asarray(c["wg_scales_bits"], np.uint32))
+        w4, _, s4 = oracle.quantize_weights(w)
+        got = {"w8a8": oracle.gemm_w8a8(codes, sa, w8, s8),
+               "finegrained": oracle.gemm_finegrained(codes, sa, wg, sg, g),
+               "asymmetric": oracle.gemm_asymmetric(codes, sa, w4, s4),
+               "w4a16": oracle.gemm_w4a16(a, wg, sg, g)}
+        for key, out in got.items():
+            assert np.array_equal(bits_of(out).reshape(-1), np.asarray(c[key + "_out_bits"], np.uint32)), (c["name"], key)
+        # FastGEMM == asymmetric bit for bit (test_gemm.cpp:129-149)
+        assert c["fast_out_bits"] == c["asymmetric_out_bits"]
+
+
+def test_lwc_grid_search_vs_reference(oracle, golden):
+    """clip.cpp:55-103 restated == the reference's (gamma, beta, mse) bit for bit."""
+    for c in (x for x in golden if x["kind"] == "lwc"):
+        w = f32_from_bits(c["w_bits"]).reshape(c["n"], c["k"])
+        gmin = float(f32_from_bits([c["gmin_bits"]])[0])
+        gstep = float(f32_from_bits([c["gstep_bits"]])[0])
+        g, b, mb, ma = oracle.optimize_clipping(w, c["bits"], gmin, gstep)
+        for got, key in ((g, "gamma_bits"), (b, "beta_bits"), (mb, "mse_before_bits"), (ma, "mse_after_bits")):
+            assert np.array_equal(bits_of(got), np.asarray(c[key], np.uint32)), (c["name"], key)

@@ -134,3 +134,64 @@ def test_split_rejects_indivisible():
     with pytest.raises(ValueError):
         _split(10, 3, 0)
     assert _split(12, 3, 2) == (8, 12)
+
+
+def _decoder_ref(o, x, ws, h, inter, world):
+    """Unsharded oracle chain with the TP stand-ins (each rank's first width/world
+    columns of its own column block), f32 intermediates like OracleBackend."""
+    def lin(xx, w):
+        codes, sa = o.quantize_activations(np.ascontiguousarray(xx, np.float32))
+        _, packed, sw = o.quantize_weights(w)
+        return o.fast_gemm(codes, sa, packed, sw, xx.shape[0], w.shape[0], xx.shape[1])
+
+    def cols(y, width):
+        blk, wd = y.shape[1] // world, width // world
+        return np.concatenate([y[:, r * blk: r * blk + wd] for r in range(world)], 1)
+    q = lin(x, ws[0])
+    hh = lin(cols(q, h), ws[1])
+    gu = lin(hh, ws[2])
+    return lin(cols(gu, inter), ws[3])
+
+
+def _decoder_worker(rank, world, port, result_q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_09550_b200.tp import TPDecoderLinears
+        be = OracleBackend()
+        r = be.o.rng(77)
+        h, inter, m = 32, 48, 5
+        x = be.o.gaussian_fill(r, (m, h))
+        ws = [be.o.gaussian_fill(r, s, 0.1) for s in ((3 * h, h), (h, h), (2 * inter, h), (h, inter))]
+        layer = TPDecoderLinears(*[torch.from_numpy(w) for w in ws], backend=be)
+        y = layer(torch.from_numpy(x))
+        result_q.put((rank, y.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_tp_decoder_layer_world2():
+    """The four-linear TP decoder layer (column qkv -> row o -> column gate_up -> row
+    down) over gloo, world 2: every rank's output equals the unsharded oracle chain."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_decoder_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=150) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    be = OracleBackend()
+    r = be.o.rng(77)
+    h, inter, m = 32, 48, 5
+    x = be.o.gaussian_fill(r, (m, h))
+    ws = [be.o.gaussian_fill(r, s, 0.1) for s in ((3 * h, h), (h, h), (2 * inter, h), (h, inter))]
+    want = _decoder_ref(be.o, x, ws, h, inter, world)
+    for rank, y in results:
+        assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), rank

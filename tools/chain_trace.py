@@ -54,6 +54,15 @@ def main(m=16):
         print(f"  {nm:14s} {stat(col)}")
     for i, (name, _, _) in enumerate(LAYERS):
         print(f"  {name:8s} first MMA {stat(10 + 4 * i)}  dep released {stat(12 + 4 * i)}  last epilogue {stat(11 + 4 * i)}")
+    ut = buf[148 * 32:].view(64, 8).cpu().numpy()
+    print("last CTA, per unit (us from first CTA entry): W issued, MMA saw a_full, B-quant saw x, B done, "
+          "conv saw W, conv done, MMA saw b_full")
+    for u in range(64):
+        row = ut[u]
+        if row.max() == 0:
+            continue
+        print("  %3d " % u + " ".join("%7.2f" % ((v - base) / 1e3) if v > 0 else "      -" for v in row[:7]))
+    print("  last x issue: %.2f" % ((ut[63, 7] - base) / 1e3 if ut[63, 7] > 0 else -1))
 
 
 if __name__ == "__main__":
