@@ -225,7 +225,8 @@ def optimize_clipping(w, bits: int = 4, grid_min: float = 0.5, grid_step: float 
 
 
 def write_tensor(t, path: str) -> None:
-    check(lib().ody_tensor_write(_as_tensor(t)._h, path.encode()))
+    h = _as_tensor(t)  # held: the handle must outlive the call
+    check(lib().ody_tensor_write(h._h, path.encode()))
 
 
 def read_tensor(path: str) -> np.ndarray:

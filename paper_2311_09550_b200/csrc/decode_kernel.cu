@@ -91,6 +91,7 @@ static_assert(4 * 16 <= 256, "D buffers below the A stages");
 // kind::i8, D=s32, A=B=s8 signed, K-major both, N=16, M=128
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                             (static_cast<uint32_t>(kBN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+constexpr int kAmaxStride = 32;  // u32: per-token row maxima one 128-byte line apart
 constexpr int kTraceCta = 32;  // [entry, setup, -, -, -, exit, producer done, meta, per linear 4 x 6]
 
 struct LinDesc {
@@ -110,6 +111,7 @@ struct LinDesc {
     int rot;              // tile rotation (independent linears spread over the clusters)
     // dynamic schedule (w4a8_decode_dyn_kernel): work items = (tile, k-split) pairs
     int split;            // k-splits per tile
+    int off;              // static chain schedule: CTA of this linear's item 0
     int ibase;            // first work item of this linear
     int tbase;            // first tile of this linear in the program's tile numbering
     // dynamic-schedule dependency chain (w4a8_decode_dyn_kernel)
@@ -120,13 +122,11 @@ struct LinDesc {
     const uint32_t* dep_done;  // dependent linear: its producer's `done`, complete at dep_target
     uint32_t dep_target;
     const uint32_t* amax_src;  // dependent linear: per-token max |x| (its producer's amax_dst)
+    uint32_t* qdone;      // dependent linear: k-blocks of x quantized into qa (grid-wide), or NULL
+    uint32_t qtarget;     //   complete at kblocks
 };
 
 struct PParams {
-    // dependent linears (dynamic chain): 2-D TMA maps of their x ({K, M} 16-bit, row
-    // stride ldx, box {256, BN}) -- the producer stages each unit's x slice with ONE
-    // tensor copy; out-of-range rows / columns arrive as zeros
-    alignas(64) CUtensorMap xmap[kMaxLin];
     LinDesc lin[kMaxLin];
     int L;
     int S, C;             // cluster size (split-K factor), clusters
@@ -135,6 +135,8 @@ struct PParams {
     int32_t* part;        // dynamic schedule: [items][BN][128] split partials (scratch)
     int n_items;          // dynamic schedule: work items of the whole program
     uint32_t* work;       // dynamic schedule: next-item counter (zeroed; reset by the last CTA)
+    int chain_static;     // dependency chain: items dealt round-robin over the CTAs in program
+                          // order (CTA c: items c - off, + C, ... of each linear), no counter
     uint32_t* tile_cnt;   // [program tiles] split arrivals (zeroed)
     int pdl;
     int pf_units;         // L2 prefetch window past the smem ring (units)
@@ -143,6 +145,26 @@ struct PParams {
     int dbg;              // diagnostics (ODY_DBG_DECODE): 1 store raw x (no quant math), 2 no IEEE redo
     unsigned long long* trace;
 };
+
+// A value the compiler must keep in a register (a volatile move cannot be rematerialised
+// from the kernel parameters).
+__device__ __forceinline__ int ld_keep(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ void stg_b16(void* p, unsigned short v) {
+    asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+__device__ __forceinline__ void stg_b32(void* p, uint32_t v) {
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ T* ld_keep_ptr(T* v) {
+    unsigned long long r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(reinterpret_cast<unsigned long long>(v)));
+    return reinterpret_cast<T*>(r);
+}
 
 __device__ __forceinline__ uint64_t b_desc(uint32_t smem_addr) {
     // K-major SWIZZLE_128B: start>>4, SBO = 1024 B (8 rows x 128 B), version 1, swizzle 128B.
@@ -849,7 +871,8 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 #pragma unroll
                         for (int t = 0; t < kBN; ++t) {
                             if (t < d.M) {
-                                const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                                if (p.dbg & 16) continue;  // diagnostics (ODY_DBG_DECODE, diag build only)
+                    const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
                                 const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa[t], sw_n));
                                 const size_t idx = static_cast<size_t>(t) * d.N + n;
                                 if (d.out_dtype == kDtypeF32)
@@ -916,8 +939,7 @@ constexpr int kItemSlots = 8;
 template <int BN, bool DEP>
 struct DynCfg {
     static constexpr int kBBlock = BN * 128;                            // one B k-block tile
-    static constexpr int kXBytes = DEP ? BN * 2 * kUnitBlocks * kBlockK : 0;  // staged 16-bit x slice
-    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock + kXBytes;  // weights + B (+ x)
+    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock;  // weights + B tiles
     static constexpr int kStages = (220 * 1024 - 3072) / kStageBytes < 10 ? (220 * 1024 - 3072) / kStageBytes : 10;
     static constexpr int kSmem = kStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
@@ -931,11 +953,11 @@ struct DynCfg {
 struct DynItem {
     int l, nt, kb_lo, kb_hi, r;
 };
-__device__ __forceinline__ DynItem dyn_item(const PParams& p, int it) {
+__device__ __forceinline__ DynItem dyn_item(const PParams& p, const LinDesc* lin, int it) {
     DynItem x;
     int l = 0;
-    while (l + 1 < p.L && it >= p.lin[l + 1].ibase) ++l;
-    const LinDesc& d = p.lin[l];
+    while (l + 1 < p.L && it >= lin[l + 1].ibase) ++l;
+    const LinDesc& d = lin[l];
     const int rel = it - d.ibase;
     x.l = l;
     x.nt = rel / d.split;
@@ -964,12 +986,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint64_t* d_empty = d_full + kDBufs;
     uint64_t* i_full = d_empty + kDBufs;
     uint64_t* i_empty = i_full + kItemSlots;
-    uint64_t* x_full = i_empty + kItemSlots;  // DEP: the unit's x slice landed (every unit: one phase)
-    int* items = reinterpret_cast<int*>(x_full + kDynStages);
+    int* items = reinterpret_cast<int*>(i_empty + kItemSlots);
     uint32_t* flag = reinterpret_cast<uint32_t*>(items + kItemSlots);
     uint32_t* tmem_slot = flag + 1;
-    float* bsc = reinterpret_cast<float*>(tmem_slot + 1);  // DEP: per-token scale / reciprocal
-    float* brcp = bsc + 64;
+    uint32_t* emax = tmem_slot + 1;  // [BN] the CTA's per-token max |y| of the current item
+    float* ssc = reinterpret_cast<float*>(emax + 64);  // [2][64] token scales of the item (parity)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
@@ -991,10 +1012,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], 4);
         }
-        for (int i = 0; i < kDynStages; ++i) mbar_init(&x_full[i], 1);
         for (int i = 0; i < kItemSlots; ++i) {
             mbar_init(&i_full[i], 1);
-            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4 + (DEP ? 2 : 0));  // MMA, converter, epilogue (+B) warps
+            mbar_init(&i_empty[i], 1 + 4 * kDynConvGroups + 4);  // MMA, converter, epilogue warps
         }
         fence_mbar_init();
     }
@@ -1002,6 +1022,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         tmem_alloc(tmem_slot, kTmemCols);
         tmem_relinquish();
     }
+    if (threadIdx.x < BN) emax[threadIdx.x] = 0u;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1033,7 +1054,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     for (int r2 = 1; r2 <= p.pf_units; ++r2) {
                         const int it2 = static_cast<int>(blockIdx.x + r2 * gridDim.x);
                         if (it2 >= p.n_items) break;
-                        const DynItem y = dyn_item(p, it2);
+                        const DynItem y = dyn_item(p, p.lin, it2);
                         const LinDesc& d2 = p.lin[y.l];
                         bulk_prefetch_l2(d2.wp + (static_cast<size_t>(y.nt) * d2.kblocks + y.kb_lo) * kWBlockBytes,
                                          static_cast<uint32_t>(y.kb_hi - y.kb_lo) * kWBlockBytes);
@@ -1042,37 +1063,35 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 waited = true;
                 for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], dst[i], dkb[i], dnb[i]);
             };
-            // DEP: x-slice copies of dependent units wait until the producer linear is
-            // complete (its `done` reached the item count -- only trusted after
-            // griddepcontrol.wait, the previous launch re-arms the counters); until then
-            // they are deferred and the weight stream keeps going.  Every blocking wait
-            // below polls so that a released dependency's copies go out meanwhile.
-            int xq[DEP ? kDynStages : 1], xst[DEP ? kDynStages : 1], xkb[DEP ? kDynStages : 1], nx = 0;
+            // DEP: the B tiles of a dependent linear come from its a8 buffer, which the
+            // B-quantizer warps of every CTA fill once the producer linear completed (its
+            // `qdone` reaches the k-block count -- only trusted after griddepcontrol.wait,
+            // the previous launch re-arms the counters); until then the copies are deferred
+            // and the weight stream keeps going.  Every blocking wait below polls so that a
+            // released linear's copies go out meanwhile.
+            int xq[DEP ? kDynStages : 1], xst[DEP ? kDynStages : 1], xkb[DEP ? kDynStages : 1],
+                xnb[DEP ? kDynStages : 1], nx = 0;
             uint32_t rel_mask = 0u;
             auto released = [&](int l) -> bool {
                 if ((rel_mask >> l) & 1u) return true;
                 if (!waited) return false;
                 const LinDesc& dl = p.lin[l];
-                if (ld_acquire_u32(dl.dep_done) < dl.dep_target) return false;
-                fence_proxy_async_global();  // the producer's generic writes -> our tensor copies
+                if (ld_acquire_u32(dl.qdone) < dl.qtarget) return false;
+                fence_proxy_async_global();  // the quantizers' generic writes -> our bulk copies
                 rel_mask |= 1u << l;
+                if (trc && l < 4) trc[26 + l] = globaltimer();
                 return true;
-            };
-            auto issue_x = [&](int l, int s, int kb) {
-                if (utr) utr[8 * 63 + 7] = globaltimer();  // last x issue
-                mbar_expect_tx(&x_full[s], C::kXBytes);
-                tma_load_2d(ring + s * kStageBytes + kUnitBytes + kUnitBlocks * kBBlockBytes, &p.xmap[l],
-                            kb * kBlockK, 0, &x_full[s]);
             };
             auto flush_x = [&]() {
                 int keep = 0;
                 for (int i = 0; i < nx; ++i) {
                     if (released(xq[i])) {
-                        issue_x(xq[i], xst[i], xkb[i]);
+                        issue_b(p.lin[xq[i]], xst[i], xkb[i], xnb[i]);
                     } else {
                         xq[keep] = xq[i];
                         xst[keep] = xst[i];
                         xkb[keep] = xkb[i];
+                        xnb[keep] = xnb[i];
                         ++keep;
                     }
                 }
@@ -1100,21 +1119,25 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     if (lane == 0 && waited)
                         for (uint32_t m = want_all; m; m &= m - 1) {
                             const int l = __ffs(m) - 1;
-                            if (ld_acquire_u32(p.lin[l].dep_done) >= p.lin[l].dep_target) newly |= 1u << l;
+                            if (ld_acquire_u32(p.lin[l].qdone) >= p.lin[l].qtarget) newly |= 1u << l;
                         }
                     newly = __shfl_sync(0x3u, newly, 0);
                     if (newly) {
-                        fence_proxy_async_global();  // the producer linear's writes -> our tensor copies
+                        fence_proxy_async_global();  // the quantizers' writes -> our bulk copies
                         rel_mask |= newly;
+                        if (trc)
+                            for (uint32_t m = newly; m; m &= m - 1)
+                                if (__ffs(m) - 1 < 4) trc[26 + __ffs(m) - 1] = globaltimer();
                         flush_x();
                         ns = 128;
                     } else {
                         __nanosleep(ns);
-                        ns = ns < 1024 ? 2 * ns : 1024;
+                        ns = ns < 256 ? 2 * ns : 256;
                     }
                 }
             };
             int U = 0;
+            int cl = 0, ci = -1;  // static chain schedule: current linear, its item index
             for (int j = 0;; ++j) {
                 const int is = j % kItemSlots;
                 wait_poll(&i_empty[is], ((j / kItemSlots) & 1) ^ 1, j >= kItemSlots);
@@ -1122,7 +1145,25 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 // once; the shared counter is only touched after griddepcontrol.wait, i.e.
                 // once the previous launch (which re-arms it) has completed
                 int it = static_cast<int>(blockIdx.x);
-                if (j > 0) {
+                if (p.chain_static) {
+                    // every linear runs alone between grid-wide completions: deal its items
+                    // evenly (a dynamic grab lets idle CTAs hoard the next linear's items)
+                    it = -1;
+                    while (cl < p.L) {
+                        const LinDesc& dl = p.lin[cl];
+                        const int nl = dl.n_tiles * dl.split;
+                        const int C = static_cast<int>(gridDim.x);
+                        const int i = ci < 0 ? ((static_cast<int>(blockIdx.x) - dl.off) % C + C) % C : ci + C;
+                        if (i < nl) {
+                            ci = i;
+                            it = dl.ibase + i;
+                            break;
+                        }
+                        ++cl;
+                        ci = -1;
+                    }
+                    if (j > 0 && !waited) release_deferred();
+                } else if (j > 0) {
                     if (!waited) release_deferred();
                     if (lane == 0) it = static_cast<int>(gridDim.x + atomicAdd(p.work, 1u));
                     it = __shfl_sync(0x3u, it, 0);
@@ -1133,15 +1174,15 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     mbar_arrive(&i_full[is]);  // release: the item id is visible to the consumers
                 }
                 if (it < 0) break;
-                const DynItem x = dyn_item(p, it);
+                const DynItem x = dyn_item(p, p.lin, it);
                 const LinDesc& d = p.lin[x.l];
                 const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
                 const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
                 // A dependent linear's B tiles are quantized in-kernel by the converters once
                 // its producer linear completes.  While it has not, keep HBM streaming: pull
                 // this whole item's weights into L2 (the ring then refills from L2).
-                const bool depi = d.dep_done != nullptr;
-                if (depi && lane == 0 && ld_acquire_u32(d.dep_done) < d.dep_target)
+                const bool depi = d.qdone != nullptr;
+                if (depi && lane == 0 && ld_acquire_u32(d.qdone) < d.qtarget)
                     bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
                                      static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
@@ -1161,15 +1202,14 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol);
                         if (utr && Uk < 64) utr[8 * Uk + 0] = globaltimer();
-                        if (DEP && !depi) mbar_arrive(&x_full[s]);  // x_full: one phase per unit
                         if (DEP && depi) {
-                            // no B copy: the B-quantizer warps quantize the staged x slice
                             if (released(x.l)) {
-                                issue_x(x.l, s, kb);
+                                issue_b(d, s, kb, nb);
                             } else {
                                 xq[nx] = x.l;
                                 xst[nx] = s;
                                 xkb[nx] = kb;
+                                xnb[nx] = nb;
                                 ++nx;
                             }
                         } else if (waited) {
@@ -1205,7 +1245,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             __syncwarp();
             if (lane == 0) mbar_arrive(&i_empty[is]);
             if (it < 0) break;
-            const DynItem x = dyn_item(p, it);
+            const DynItem x = dyn_item(p, p.lin, it);
             if (x.kb_hi <= x.kb_lo) continue;
             if (trc && lane == 0 && x.l < 4 && trc[10 + 4 * x.l] == 0) trc[10 + 4 * x.l] = globaltimer();
             const int db = JD % kDBufs;
@@ -1239,66 +1279,64 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         }
     } else if (DEP && (warp == kWarpAlloc || warp == kWarpAlloc + 1)) {
         // B-quantizer (warps 2-3, idle once TMEM is allocated).  A DEPENDENT linear's x
-        // is an earlier linear's 16-bit output; the producer stages each unit's slice of it
-        // ([BN tokens][256 k] by one TMA tensor copy, issued once that linear completed).
-        // Quantize it from shared memory into the unit's B tiles (quant16: bit-exact with
-        // the act-quant kernel), then arrive on b_full.  Token scale S = max/127 (IEEE;
-        // 0 -> 2^-24, ref quantize.cpp:22-35) from the row maxima the producer linear's
-        // epilogues accumulated.  Every unit completes one x_full phase (in order).
+        // is an earlier linear's 16-bit output.  Once that linear completed, x is
+        // quantized ONCE for the whole grid: CTA c quantizes k-blocks c, c + grid, ... of
+        // it (quant16: bit-exact with the act-quant kernel) into the linear's compact a8
+        // buffer, then bumps its `qdone`; every item of the linear bulk-copies its B tiles
+        // from there like an external linear's.  Token scale S = max/127 (IEEE; 0 -> 2^-24,
+        // ref quantize.cpp:22-35) from the row maxima the producer linear's epilogues
+        // accumulated.
         const int qt = threadIdx.x - kWarpAlloc * 32;  // 0..63
-        int U = 0;
-        for (int j = 0;; ++j) {
-            const int is = j % kItemSlots;
-            mbar_wait(&i_full[is], (j / kItemSlots) & 1);
-            const int it = items[is];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&i_empty[is]);
-            if (it < 0) break;
-            const DynItem x = dyn_item(p, it);
-            const LinDesc& d = p.lin[x.l];
-            const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
-            const bool depi = d.dep_done != nullptr;
-            for (int u = 0; u < nunits; ++u, ++U) {
-                const int s = U % kDynStages;
-                mbar_wait(&x_full[s], (U / kDynStages) & 1);
-                if (utr && qt == 0 && U < 64) utr[8 * U + 2] = globaltimer();
-                if (!depi) continue;
-                if (u == 0) {
-                    // the producer issues x copies only after it acquired the producer
-                    // linear's completion; x_full (its release arrive) passes that on
-                    if (trc && qt == 0 && x.l < 4 && trc[12 + 4 * x.l] == 0) trc[12 + 4 * x.l] = globaltimer();
-                    if (qt < BN) {
-                        float sc = 1.0f;
-                        if (qt < d.M) {
-                            sc = __uint_as_float(__ldcg(d.amax_src + qt)) / 127.0f;
-                            if (!(sc > 0.0f)) sc = kMinScale;
-                        }
-                        bsc[qt] = sc;
-                        brcp[qt] = 1.0f / sc;
-                    }
-                    named_bar_sync(4, 64);
+        if (p.pdl) pdl_wait();  // the counters are re-armed by the previous launch
+        for (int l = 0; l < p.L; ++l) {
+            const LinDesc& d = p.lin[l];
+            if (d.qdone == nullptr) continue;
+            if (qt == 0) {
+                uint32_t ns = 64;
+                while (ld_acquire_u32(d.dep_done) < d.dep_target) {
+                    __nanosleep(ns);
+                    ns = ns < 256 ? 2 * ns : 256;
                 }
-                const int nb = min(kUnitBlocks, x.kb_hi - (x.kb_lo + kUnitBlocks * u));
-                const uint32_t bb = smem_u32(ring) + s * kStageBytes + kUnitBytes;
-                const uint32_t xs = bb + kUnitBlocks * kBBlockBytes;
-#pragma unroll
-                for (int i = 0; i < BN / 4; ++i) {  // BN rows x 16 sixteen-element chunks
-                    const int task = qt + 64 * i;
-                    const int t = task >> 4, c16 = task & 15;
-                    const int b = c16 >> 3, c = c16 & 7;
-                    if (b < nb) {
-                        const uint4 r0 = lds128(xs + t * 512 + c16 * 32);
-                        const uint4 r1 = lds128(xs + t * 512 + c16 * 32 + 16);
-                        const uint4 v = d.x_bf16 ? quant16<true>(r0, r1, bsc[t], brcp[t], 0)
-                                                 : quant16<false>(r0, r1, bsc[t], brcp[t], 0);
-                        sts128(bb + b * kBBlockBytes + t * 128 + ((c ^ (t & 7)) << 4), v);
-                    }
-                }
-                fence_proxy_async_shared();  // generic smem writes -> the MMA's async proxy
-                named_bar_sync(4, 64);
-                if (qt == 0) mbar_arrive(&b_full[s]);
-                if (utr && qt == 0 && U < 64) utr[8 * U + 3] = globaltimer();
+                if (trc && l < 4) trc[12 + 4 * l] = globaltimer();
             }
+            named_bar_sync(4, 64);
+            int nq = 0;
+            for (int kb = static_cast<int>(blockIdx.x); kb < d.kblocks; kb += static_cast<int>(gridDim.x), ++nq) {
+                // BN rows x 8 sixteen-element chunks of k-block kb
+#pragma unroll 1
+                for (int task = qt; task < BN * 8; task += 64) {
+                    const int t = task >> 3, c = task & 7;
+                    const int k0 = kb * kBlockK + c * 16;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if (t < d.M && k0 < d.K) {
+                        float sc = __uint_as_float(__ldcg(d.amax_src + t * kAmaxStride)) / 127.0f;
+                        if (!(sc > 0.0f)) sc = kMinScale;
+                        const unsigned short* row = static_cast<const unsigned short*>(d.x) + static_cast<size_t>(t) * d.ldx;
+                        uint4 r0, r1;
+                        if (k0 + 16 <= d.K) {
+                            r0 = __ldcg(reinterpret_cast<const uint4*>(row + k0));
+                            r1 = __ldcg(reinterpret_cast<const uint4*>(row + k0 + 8));
+                        } else {
+                            uint32_t w[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const uint32_t lo = k0 + 2 * e < d.K ? __ldcg(row + k0 + 2 * e) : 0u;
+                                const uint32_t hi = k0 + 2 * e + 1 < d.K ? __ldcg(row + k0 + 2 * e + 1) : 0u;
+                                w[e] = lo | (hi << 16);
+                            }
+                            r0 = make_uint4(w[0], w[1], w[2], w[3]);
+                            r1 = make_uint4(w[4], w[5], w[6], w[7]);
+                        }
+                        v = d.x_bf16 ? quant16<true>(r0, r1, sc, 1.0f / sc, 0) : quant16<false>(r0, r1, sc, 1.0f / sc, 0);
+                    }
+                    *reinterpret_cast<uint4*>(const_cast<int8_t*>(d.qa) + static_cast<size_t>(kb) * BN * 128 + t * 128 +
+                                              ((c ^ (t & 7)) << 4)) = v;
+                }
+            }
+            fence_proxy_async_global();  // generic writes -> the consumers' bulk copies
+            named_bar_sync(4, 64);
+            if (qt == 0 && nq > 0) red_release_add_u32(d.qdone, static_cast<uint32_t>(nq));
+            if (trc && qt == 0 && l < 4) trc[13 + 4 * l] = globaltimer();
         }
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kDynConvGroups) {
         const int q = warp & 3;
@@ -1312,7 +1350,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             __syncwarp();
             if (lane == 0) mbar_arrive(&i_empty[is]);
             if (it < 0) break;
-            const DynItem x = dyn_item(p, it);
+            const DynItem x = dyn_item(p, p.lin, it);
             for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
                 // the group owning ring stage U % kDynStages widens this unit (stage
                 // ownership keeps every w_full waiter in phase order on odd-length rings)
@@ -1358,6 +1396,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         const int r = 32 * q + lane;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * q) << 16);
         int JD = 0, cur_l = -1;
+        // diagnostics: per-item epilogue timeline of the LAST CTA (first 32 items, 8 slots)
+        unsigned long long* etr = utr ? utr + 64 * 8 : nullptr;
+        auto emark = [&](int j2, int slot) {
+            if (etr && r == 0 && j2 < 32) etr[16 * j2 + slot] = globaltimer();
+        };
         for (int j = 0;; ++j) {
             const int is = j % kItemSlots;
             mbar_wait(&i_full[is], (j / kItemSlots) & 1);
@@ -1365,7 +1408,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             __syncwarp();
             if (lane == 0) mbar_arrive(&i_empty[is]);
             if (it < 0) break;
-            const DynItem x = dyn_item(p, it);
+            const DynItem x = dyn_item(p, p.lin, it);
             const LinDesc& d = p.lin[x.l];
             if (cur_l < 0 && p.pdl) pdl_wait();  // token scales come from the act-quant kernel
             cur_l = x.l;
@@ -1375,6 +1418,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             if (x.kb_hi > x.kb_lo) {
                 const int db = JD % kDBufs;
                 mbar_wait(&d_full[db], (JD / kDBufs) & 1);
+                emark(j, 0);
                 tc_fence_after();
 #pragma unroll
                 for (int tc = 0; tc < BN; tc += 16) {
@@ -1392,6 +1436,28 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
 #pragma unroll
                 for (int t = 0; t < BN; ++t) v[t] = 0u;
             }
+            // Token scales, staged once per item in smem (a per-token global load inside the
+            // store loop below cannot be hoisted past the output stores: 16 serial L2 round
+            // trips).  A dependent linear's scales follow from its producer's row maxima exactly
+            // as the B-quantizers derived them (complete by now: the MMAs consumed B tiles
+            // quantized after the producer finished; one acquire).
+            emark(j, 1);
+            const bool depi = d.qdone != nullptr;
+            float* tsc = ssc + (j & 1) * 64;
+            if (depi) {
+                // no acquire needed here: the producer linear's row-max atomics precede its
+                // `done` release, which the B-quantizers acquired before releasing `qdone`,
+                // which the producer warp acquired before the B copies this item's MMAs
+                // consumed (mbarrier chain to d_full): the maxima are final in L2
+                if (r < d.M) {
+                    float sc = __uint_as_float(__ldcg(d.amax_src + r * kAmaxStride)) / 127.0f;
+                    if (!(sc > 0.0f)) sc = kMinScale;
+                    tsc[r] = sc;
+                }
+            } else if (r < d.M) {
+                tsc[r] = __ldg(d.sa + r);
+            }
+            emark(j, 2);
             bool fin = true;
             if (d.split > 1) {
                 // Per-ROW last-arriver reduction, no barrier and no waiting: thread r stores
@@ -1408,73 +1474,96 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 uint32_t* rc = reinterpret_cast<uint32_t*>(p.acc) + static_cast<size_t>(d.tbase + x.nt) * kTileN + r;
                 const uint32_t old = atom_add_acq_rel_u32(rc, 1u);
                 fin = old == static_cast<uint32_t>(d.split - 1);
+                emark(j, 3);
                 if (fin) {
+                    // the other splits' rows, kPer splits' loads in flight per round trip
+                    constexpr int kPer = BN >= 32 ? 1 : 32 / BN;
                     const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * BN * kTileN;
-                    for (int s2 = 0; s2 < d.split; ++s2) {
-                        if (s2 == x.r) continue;
+#pragma unroll 1
+                    for (int s0 = 0; s0 < d.split; s0 += kPer) {
+                        uint32_t add[kPer][BN];
 #pragma unroll
-                        for (int t = 0; t < BN; ++t)
-                            if (t < d.M) v[t] += static_cast<uint32_t>(__ldcg(p0 + (s2 * BN + t) * kTileN + r));
+                        for (int j2 = 0; j2 < kPer; ++j2) {
+                            const int s2 = s0 + j2;
+                            const bool use = s2 < d.split && s2 != x.r;
+#pragma unroll
+                            for (int t = 0; t < BN; ++t)
+                                add[j2][t] = (use && t < d.M)
+                                                 ? static_cast<uint32_t>(__ldcg(p0 + (s2 * BN + t) * kTileN + r))
+                                                 : 0u;
+                        }
+#pragma unroll
+                        for (int j2 = 0; j2 < kPer; ++j2)
+#pragma unroll
+                            for (int t = 0; t < BN; ++t) v[t] += add[j2][t];
                     }
                     *rc = 0u;  // every split of this row arrived: re-armed for the next launch
                 }
             }
-            const bool depi = d.dep_done != nullptr;
-            if (depi) {
-                // in-kernel quantized x: the token scales follow from the producer's row
-                // maxima exactly as the B-quantizer derived them (complete by now: the MMAs
-                // consumed B tiles quantized after the producer finished); one acquire
-                while (ld_acquire_u32(d.dep_done) < d.dep_target) __nanosleep(256);
-            }
-            const bool own = fin && n < d.N;
-            const bool amx = d.amax_dst != nullptr && n >= d.amax_c0 && n < d.amax_c1;
+            emark(j, 4);
+            named_bar_sync(3, 128);  // tsc complete (the other parity buffer is still in use)
+            emark(j, 8);
+            // The descriptor fields used per token, hoisted into registers once: read through a
+            // run-time linear index they compile to indexed LDC, re-issued for every token
+            // (rematerialised rather than kept live) at ~0.3 us per token on this path.
+            const int m_rows = ld_keep(d.M);
+            const int n_cols = ld_keep(d.N);
+            const int odt = ld_keep(d.out_dtype);
+            uint8_t* const outp = ld_keep_ptr(static_cast<uint8_t*>(d.out));
+            int32_t* const accp = ld_keep_ptr(d.acc_out);
+            float* const sa_outp = (depi && x.nt == 0 && r == 0) ? ld_keep_ptr(d.sa_out) : nullptr;
+            const bool amx_on = d.amax_dst != nullptr;
+            const bool own = fin && n < n_cols;
+            const bool amx = amx_on && n >= d.amax_c0 && n < d.amax_c1;
 #pragma unroll
             for (int t = 0; t < BN; ++t) {
-                if (t < d.M) {
-                    const size_t idx = static_cast<size_t>(t) * d.N + n;
-                    if (d.acc_out) {
-                        if (own) d.acc_out[idx] = static_cast<int32_t>(v[t]);  // pre-shift (TP all-reduce)
+                if (t < m_rows) {
+                    const size_t idx = static_cast<size_t>(t) * n_cols + n;
+                    if (accp) {
+                        if (own) stg_b32(accp + idx, v[t]);  // pre-shift (TP all-reduce)
                         continue;
                     }
-                    float sa_t;
-                    if (depi) {
-                        sa_t = __uint_as_float(__ldcg(d.amax_src + t)) / 127.0f;
-                        if (!(sa_t > 0.0f)) sa_t = kMinScale;
-                        if (d.sa_out && own && x.nt == 0 && r == 0) d.sa_out[t] = sa_t;
-                    } else {
-                        sa_t = __ldg(d.sa + t);
-                    }
+                    // explicit ld.shared: a generic load here (tsc is a generic pointer) is
+                    // ordered behind the previous token's global stores
+                    const float sa_t = __uint_as_float(lds32(smem_u32(tsc + t)));
+                    if (sa_outp && own) stg_b32(sa_outp + t, __float_as_uint(sa_t));
                     const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
                     const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa_t, sw_n));
                     uint32_t mag = 0u;  // |stored value| as f32 bits (the dependent linear's x)
-                    if (d.out_dtype == kDtypeF32) {
-                        if (own) static_cast<float*>(d.out)[idx] = y;
-                    } else if (d.out_dtype == kDtypeF16) {
+                    if (odt == kDtypeF32) {
+                        if (own) stg_b32(outp + 4 * idx, __float_as_uint(y));
+                    } else if (odt == kDtypeF16) {
                         const __half h = __float2half_rn(y);
-                        if (own) static_cast<__half*>(d.out)[idx] = h;
+                        if (own) stg_b16(outp + 2 * idx, __half_as_ushort(h));
                         mag = __float_as_uint(fabsf(__half2float(h)));
                     } else {
                         const __nv_bfloat16 h = __float2bfloat16_rn(y);
-                        if (own) static_cast<__nv_bfloat16*>(d.out)[idx] = h;
+                        if (own) stg_b16(outp + 2 * idx, __bfloat16_as_ushort(h));
                         mag = __float_as_uint(fabsf(__bfloat162float(h)));
                     }
-                    if (d.amax_dst != nullptr) {  // warp-uniform: every lane joins the reduction
-                        mag = (own && amx) ? mag : 0u;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, o));
-                        if (lane == 0 && mag != 0u) atomicMax(d.amax_dst + t, mag);
+                    if (amx_on) {  // warp-uniform: every lane joins the reduction
+                        mag = __reduce_max_sync(0xffffffffu, (own && amx) ? mag : 0u);
+                        if (lane == 0 && mag != 0u) atom_max_shared_u32(smem_u32(emax + t), mag);
                     }
                 }
             }
+            emark(j, 5);
             if (trc && r == 0 && x.l < 4) trc[11 + 4 * x.l] = globaltimer();
             if (d.done != nullptr) {
                 // publish: every store (and row-max contribution) of this item happens
-                // before the release increment the dependent linear acquires
+                // before the release increment the dependent linear acquires.  One global
+                // atomicMax per token per item, each token on its own 128-byte line (the
+                // whole grid's items hit these few addresses: same-line atomics serialise).
                 named_bar_sync(3, 128);
-                if (r == 0) {
-                    __threadfence();
-                    red_release_add_u32(d.done, 1u);
+                if (d.amax_dst != nullptr && r < d.M) {
+                    const uint32_t m = emax[r];
+                    emax[r] = 0u;
+                    if (m != 0u) atomicMax(d.amax_dst + r * kAmaxStride, m);
                 }
+                if (d.amax_dst != nullptr) named_bar_sync(3, 128);
+                emark(j, 6);
+                if (r == 0) red_release_add_u32(d.done, 1u);  // cumulative over the CTA barrier
+                emark(j, 7);
             }
         }
         if (trc && r == 0) trc[4] = globaltimer();
@@ -1491,8 +1580,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             p.ctr[kMaxLin] = 0u;
             for (int l = 0; l < p.L; ++l) {  // chain state of this launch (zero region)
                 if (p.lin[l].done) *p.lin[l].done = 0u;
+                if (p.lin[l].qdone) *p.lin[l].qdone = 0u;
                 if (p.lin[l].amax_dst)
-                    for (int t = 0; t < p.lin[l].M; ++t) p.lin[l].amax_dst[t] = 0u;
+                    for (int t = 0; t < p.lin[l].M; ++t) p.lin[l].amax_dst[t * kAmaxStride] = 0u;
             }
             __threadfence();
         }
@@ -1597,35 +1687,6 @@ cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN, DEP>, p);
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    });
-    return fn;
-}
-
-// The 2-D map of a dependent linear's 16-bit x: dims {K, M}, row stride ldx elements,
-// box {256 (one pipeline unit of k), BN tokens}, no swizzle, zero fill out of range.
-bool encode_x_map(CUtensorMap* map, const void* x, int x_dtype, size_t ldx, int M, int K, int BN) {
-    auto enc = tensor_map_encoder();
-    if (!enc) return false;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kUnitBlocks * kBlockK), static_cast<cuuint32_t>(BN)};
-    const cuuint32_t estr[2] = {1, 1};
-    return enc(map, x_dtype == kDtypeBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-               const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 int dyn_bn(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
 
 cudaError_t ensure_decode_attr() {
@@ -1689,9 +1750,9 @@ static size_t program_tiles(const LinearArgs* a, int L) {
 constexpr size_t kAccOffset = kProgramCounterRegion + kProgramMaxTiles * 4;
 // chain state inside the counter region: done[kMaxLin] at u32 64, row maxima [kMaxLin][64]
 constexpr int kChainDoneU32 = 64;
-constexpr size_t kChainAmaxOffset = 1024;
+constexpr size_t kChainAmaxOffset = 4096;
 constexpr int kChainMaxM = 64;
-static_assert(kChainAmaxOffset + kMaxLin * kChainMaxM * 4 <= kProgramCounterRegion, "counter region");
+static_assert(kChainAmaxOffset + kMaxLin * kChainMaxM * kAmaxStride * 4 <= kProgramCounterRegion, "counter region");
 // the last 4 KiB of the zero region are the two-kernel GEMM's stream-K counters when the
 // same scratch serves ody_dev_w4a8_linear's fallback (kLinearGemmCounters)
 constexpr size_t kZeroRegion = kAccOffset + kProgramMaxTiles * kBN * kTileN * 4 + kLinearGemmCounters;
@@ -1795,12 +1856,36 @@ static int dyn_split(int kblocks) {
     static const int target = env ? std::max(1, std::atoi(env)) : 56;
     return std::max(1, (kblocks + target - 1) / target);
 }
+// Dependency chain: every linear runs alone between two grid-wide completions, so its
+// split is chosen for that linear's own critical path: items per CTA (waves w) x
+// max(mainloop, epilogue) + the last epilogue, with a measured ~0.15 us per k-block of
+// mainloop and ~1 us (whole-K item: the completion release) / ~2.5 us (split item: plus
+// the partial-sum round trips) of epilogue latency per item (tools/chain_trace.py).
+static int chain_split(int n_tiles, int kblocks, int sms) {
+    static const char* env = ODY_DIAG_ENV("ODY_CHAIN_SPLIT");  // diagnostics: fixed split
+    if (env) return std::max(1, std::min(std::atoi(env), kblocks));
+    int best = 1;
+    double best_t = 1e30;
+    for (int sp = 1; sp <= 8 && sp <= kblocks; ++sp) {
+        const int waves = (n_tiles * sp + sms - 1) / sms;
+        const double ml = 0.15 * ((kblocks + sp - 1) / sp);
+        const double ep = sp > 1 ? 2.5 : 1.0;
+        const double t = waves * std::max(ml, ep) + ep;
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = sp;
+        }
+    }
+    return best;
+}
 static size_t dyn_items(const LinearArgs* a, int L) {
-    // upper bound over the tail refinement (any linear may be the tail one, <= 12-block items)
+    // upper bound over the tail refinement (any linear may be the tail one, <= 12-block
+    // items) and the chain split (<= 8)
     size_t n = 0;
     for (int l = 0; l < L; ++l) {
         const int kb = static_cast<int>(pad_k(a[l].K) / kBlockK);
-        n += (pad_n(a[l].N) / kTileN) * std::max(dyn_split(kb), (kb + 11) / 12);
+        const int nt = static_cast<int>(pad_n(a[l].N) / kTileN);
+        n += static_cast<size_t>(nt) * std::max(std::max(dyn_split(kb), (kb + 11) / 12), std::min(8, kb));
     }
     return n;
 }
@@ -1989,11 +2074,16 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         // are all handed out before its dependent's), per-linear completion counters and
         // per-token row maxima in the zero region (re-armed by the launch's last CTA).
         uint32_t* done = counters + kChainDoneU32;
+        uint32_t* qdone = done + kMaxLin;
         uint32_t* amax = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kChainAmaxOffset);
+        int mmax_c = 1;
+        for (int l = 0; l < L; ++l) mmax_c = std::max(mmax_c, a[l].M);
+        const int bn = dyn_bn(mmax_c);
         int ib = 0, tb = 0;
         for (int l = 0; l < L; ++l) {
             LinDesc& d = p.lin[l];
-            d.split = dyn_split(d.kblocks);
+            d.split = chain_split(d.n_tiles, d.kblocks, std::min(sms, device_sm_count()));
+            d.off = ib;  // round-robin continues across linears (reduced mod C in the kernel)
             d.ibase = ib;
             d.tbase = tb;
             ib += d.n_tiles * d.split;
@@ -2006,25 +2096,29 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             dyn_chain_slice(a, deps, L, l, &c0);
             LinDesc& y = p.lin[d.dep];
             y.done = done + d.dep;
-            y.amax_dst = amax + d.dep * kChainMaxM;
+            y.amax_dst = amax + d.dep * kChainMaxM * kAmaxStride;
             y.amax_c0 = c0;
             y.amax_c1 = c0 + d.K;
             d.dep_done = y.done;
             d.dep_target = static_cast<uint32_t>(y.n_tiles * y.split);
             d.amax_src = y.amax_dst;
+            // the grid-wide quantized x (compact a8: BN rows per k-block), after the
+            // external linears' buffers in the scratch
+            d.qa = reinterpret_cast<const int8_t*>(cursor);
+            cursor += round_up(static_cast<size_t>(bn) * pad_k(d.K), 256);
+            d.Mp = bn;
+            d.qdone = qdone + l;
+            d.qtarget = static_cast<uint32_t>(d.kblocks);
         }
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
         p.pf_units = 0;
         p.S = 1;
         p.C = std::min(sms, ib);
+        static const char* st_env = ODY_DIAG_ENV("ODY_CHAIN_DYNAMIC");  // diagnostics: 1 = counter
+        p.chain_static = (st_env && st_env[0] == '1') ? 0 : 1;
+        for (int l = 0; l < L; ++l) p.lin[l].off %= p.C;
         if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
-        int mmax = 1;
-        for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
-        const int bn = dyn_bn(mmax);
-        for (int l = 0; l < L; ++l)
-            if (p.lin[l].dep >= 0 && !encode_x_map(&p.xmap[l], a[l].x, a[l].x_dtype, a[l].ldx, a[l].M, a[l].K, bn))
-                return cudaErrorInvalidValue;
         switch (bn) {
             case 16: return launch_dyn<16, true>(p, prog_pdl, st);
             case 32: return launch_dyn<32, true>(p, prog_pdl, st);

@@ -120,7 +120,7 @@ cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st);
 // program_scratch_bytes(), its first kProgramCounterRegion bytes zeroed once (the launch
 // leaves them zeroed).  Of a[]'s launch fields only a[0].max_ctas and a[0].trace are used.
 constexpr int kProgramMaxLinears = 8;
-constexpr size_t kProgramCounterRegion = 4096;  // counters + chain done/absmax (decode_kernel.cu)
+constexpr size_t kProgramCounterRegion = 4096 + 65536;  // counters + chain done/absmax (decode_kernel.cu)
 constexpr size_t kProgramMaxTiles = 1024;  // 128-row weight tiles per program (8 MiB of split-K sums)
 constexpr size_t kLinearGemmCounters = 4096;  // == the GEMM workspace's counter region
 // Bytes at the start of a program scratch that must stay zero (counters, accumulators);

@@ -8,6 +8,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+if os.environ.get("ODY_USE_DIAG"):
+    from paper_2311_09550_b200 import _lib as _l  # noqa: E402
+    _l.use_diag_library()
 from paper_2311_09550_b200 import device as dev  # noqa: E402
 from paper_2311_09550_b200._lib import lib  # noqa: E402
 
@@ -26,7 +30,7 @@ def main(m=16):
     for _ in range(3):
         prog.run()
     torch.cuda.synchronize()
-    buf = torch.zeros(148 * 32 + 512, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(148 * 32 + 512 + 512, dtype=torch.int64, device="cuda")
     lib().ody_dev_set_trace(buf.data_ptr())
     prog.run()
     lib().ody_dev_set_trace(None)
@@ -54,7 +58,15 @@ def main(m=16):
         print(f"  {nm:14s} {stat(col)}")
     for i, (name, _, _) in enumerate(LAYERS):
         print(f"  {name:8s} first MMA {stat(10 + 4 * i)}  dep released {stat(12 + 4 * i)}  last epilogue {stat(11 + 4 * i)}")
-    ut = buf[148 * 32:].view(64, 8).cpu().numpy()
+        print(f"  {'':8s} x quantized {stat(13 + 4 * i)}  producer saw qdone {stat(26 + i)}")
+    et = buf[148 * 32 + 512:].view(32, 16).cpu().numpy()[:, :11]
+    print("last CTA, per item epilogue (us): d_full, tmem ld, scales, atom, reduced, stored, amax, done, after-bar")
+    for j2 in range(32):
+        row = et[j2]
+        if row.max() == 0:
+            continue
+        print("  %3d " % j2 + " ".join("%7.2f" % ((v - base) / 1e3) if v > 0 else "      -" for v in row))
+    ut = buf[148 * 32:148 * 32 + 512].view(64, 8).cpu().numpy()
     print("last CTA, per unit (us from first CTA entry): W issued, MMA saw a_full, B-quant saw x, B done, "
           "conv saw W, conv done, MMA saw b_full")
     for u in range(64):
