@@ -47,8 +47,9 @@ typedef enum ody_granularity {
     ODY_PER_GROUP = 3,
 } ody_granularity;
 
-/* ref odyssey.h:36-42.  Only ODY_ENGINE_FAST runs here; the comparison engines
- * return ODY_EINVAL ("not implemented on the B200 path"), never a CPU fallback. */
+/* ref odyssey.h:36-42.  Every engine runs on the GPU (FAST: the FastGEMM kernels; the
+ * comparison engines W8A8 / ASYMMETRIC / FINEGRAINED / W4A16: engine_kernel.cu), bit-exact
+ * with the reference's gemm.cpp; there is never a CPU fallback. */
 typedef enum ody_engine {
     ODY_ENGINE_W4A16 = 0,
     ODY_ENGINE_FINEGRAINED = 1,
@@ -81,9 +82,10 @@ ody_status ody_tensor_data(const ody_tensor* t, const float** data);        /* :
 void ody_qtensor_free(ody_qtensor* q);                                        /* :79 */
 ody_status ody_qtensor_dims(const ody_qtensor* q, size_t* rows, size_t* cols); /* :82 */
 
-/* ref odyssey.h:87-89.  Hot path: bits == 4, ODY_PER_CHANNEL (group_size ignored),
- * optional per-row clip_gamma / clip_beta in (0,1].  Quantizes on the GPU straight
- * into the kernel's prepacked tile layout. */
+/* ref odyssey.h:87-89.  Hot path: bits == 4, ODY_PER_CHANNEL; also bits == 4
+ * ODY_PER_GROUP (group_size | cols; the FINEGRAINED / W4A16 engines) and bits == 8
+ * ODY_PER_CHANNEL (the W8A8 engine).  Optional per-row clip_gamma / clip_beta in (0,1].
+ * Quantizes on the GPU straight into the kernels' layouts. */
 ody_status ody_quantize_weights(const ody_tensor* w, int bits, ody_granularity granularity,
                                 size_t group_size, const float* clip_gamma,
                                 const float* clip_beta, ody_qtensor** out);
@@ -94,7 +96,8 @@ ody_status ody_quantize_activations(const ody_tensor* a, ody_qtensor** out);
 /* ref odyssey.h:94 */
 ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out);
 
-/* ref odyssey.h:120-121 -- ODY_ENGINE_FAST only; returns a new host f32 tensor. */
+/* ref odyssey.h:120-121 -- any engine (ref gemm.cpp:313-333 run_engine, same validation
+ * order and counter formulas); returns a new host f32 tensor. */
 ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q,
                     const ody_qtensor* w_q, ody_gemm_counters* counters, ody_tensor** out);
 
@@ -245,8 +248,9 @@ ody_status ody_dev_a8_unpack(const void* q, const float* s, size_t m, size_t k, 
 
 /* ================================================================ part 3 */
 
-/* Host copies of a qtensor's content in the REFERENCE layouts: activations ->
- * m*k int8 codes; weights -> (n*k+1)/2 flat PackedInt4Buffer bytes; plus scales. */
+/* Host copies of a qtensor's content in the REFERENCE layouts: activations and 8-bit
+ * weights -> rows*cols int8 codes; 4-bit weights -> (n*k+1)/2 flat PackedInt4Buffer
+ * bytes; plus scales (rows x groups per row). */
 ody_status ody_qtensor_export(const ody_qtensor* q, void* codes_or_nibbles, float* scales);
 /* Build a weight qtensor from reference-layout packed nibbles + scales (e.g. an OTF
  * payload.otf / scales.otf pair, ref otf.cpp:121-153). */
@@ -256,6 +260,9 @@ ody_status ody_qtensor_import_w4(size_t n, size_t k, const void* flat_nibbles,
 ody_status ody_qtensor_import_a8(size_t m, size_t k, const int8_t* codes, const float* scales,
                                  ody_qtensor** out);
 /* ref gemm.cpp:229-249: int32 accumulators before the >>4, m*n row-major. */
+/* The scheme of a qtensor (the reference keeps it in QuantizedTensor::scheme, tensor.hpp:76-109):
+ * bits 4/8, granularity (PER_TOKEN activations, PER_CHANNEL / PER_GROUP weights), group_size. */
+ody_status ody_qtensor_scheme(const ody_qtensor* q, int* bits, ody_granularity* granularity, size_t* group_size);
 ody_status ody_gemm_accumulators(const ody_qtensor* a_q, const ody_qtensor* w_q, int32_t* acc);
 /* Library/device identification, e.g. "libodyssey_b200 sm_100a NVIDIA B200 (148 SMs)". */
 const char* ody_b200_version(void);

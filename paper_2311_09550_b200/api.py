@@ -15,12 +15,13 @@ raise :class:`OdyError` with the same status the reference ABI returns.
 """
 from __future__ import annotations
 
-from ctypes import POINTER, byref, c_float, c_size_t, c_void_p, cast
+from ctypes import POINTER, byref, c_float, c_int, c_size_t, c_void_p, cast
 
 import numpy as np
 
-from ._lib import (ODY_ENGINE_FAST, ODY_PER_CHANNEL, OdyError, check, lib,  # noqa: F401
-                   ody_gemm_counters)
+from ._lib import (ODY_ENGINE_ASYMMETRIC, ODY_ENGINE_FAST, ODY_ENGINE_FINEGRAINED,  # noqa: F401
+                   ODY_ENGINE_W4A16, ODY_ENGINE_W8A8, ODY_PER_CHANNEL, ODY_PER_GROUP, ODY_PER_TOKEN, OdyError,
+                   check, lib, ody_gemm_counters)
 
 __all__ = ["Tensor", "QTensor", "quantize_activations_per_token", "quantize_weights",
            "gemm_w4a8_fast", "gemm_w4a8_fast_accumulators", "run_engine", "dequantize",
@@ -77,9 +78,9 @@ class Tensor:
 class QTensor:
     """ody_qtensor: device-resident codes + scales in the kernel layouts."""
 
-    def __init__(self, handle, kind: str):
+    def __init__(self, handle, kind: str = ""):
         self._h = handle
-        self.kind = kind  # "a8" or "w4"
+        self.kind = kind  # informational; the scheme is read from the handle
 
     @property
     def shape(self):
@@ -87,12 +88,22 @@ class QTensor:
         check(lib().ody_qtensor_dims(self._h, byref(r), byref(c)))
         return (r.value, c.value)
 
+    @property
+    def scheme(self):
+        """(bits, granularity, group_size) -- ref QuantScheme (tensor.hpp:76-90)."""
+        b, g, gs = c_int(), c_int(), c_size_t()
+        check(lib().ody_qtensor_scheme(self._h, byref(b), byref(g), byref(gs)))
+        return b.value, g.value, gs.value
+
     def export(self):
-        """(codes, scales) in the REFERENCE layouts: a8 -> int8 [rows, cols];
-        w4 -> flat PackedInt4Buffer bytes ((rows*cols+1)//2,) (ref tensor.hpp:43-64)."""
+        """(codes, scales) in the REFERENCE layouts: 8-bit -> int8 [rows, cols];
+        4-bit -> flat PackedInt4Buffer bytes ((rows*cols+1)//2,) (ref tensor.hpp:43-64);
+        scales f32 [rows * groups_per_row]."""
         rows, cols = self.shape
-        scales = np.empty(rows, np.float32)
-        if self.kind == "a8":
+        bits, gran, gs = self.scheme
+        groups = cols // gs if gran == ODY_PER_GROUP else 1
+        scales = np.empty(rows * groups, np.float32)
+        if bits == 8:
             codes = np.empty((rows, cols), np.int8)
         else:
             codes = np.empty((rows * cols + 1) // 2, np.uint8)
@@ -138,7 +149,7 @@ def quantize_weights(w, bits: int = 4, granularity: int = ODY_PER_CHANNEL, group
     check(lib().ody_quantize_weights(t._h, bits, granularity, group_size,
                                      _fptr(g) if g is not None else None,
                                      _fptr(b) if b is not None else None, byref(h)))
-    return QTensor(h, "w4")
+    return QTensor(h, "w8" if bits == 8 else ("w4g" if granularity == ODY_PER_GROUP else "w4"))
 
 
 def run_engine(engine: int, a_dense, a_q: QTensor | None, w_q: QTensor, with_counters=False):
@@ -241,15 +252,11 @@ def write_qtensor(q: QTensor, directory: str) -> None:
 
 def read_qtensor(directory: str) -> QTensor:
     """ody_qtensor_read: an `odyssey quantize` output directory straight into the device
-    layout (per-channel INT4 weights -> prepacked tiles; per-token INT8 -> a8)."""
-    import os
+    layouts (ref otf.cpp:164-202): per-channel / per-group INT4 and per-channel INT8
+    weights, per-token INT8 activations."""
     h = c_void_p()
     check(lib().ody_qtensor_read(directory.encode(), byref(h)))
-    kind = "w4"
-    try:
-        with open(os.path.join(directory, "scheme.txt")) as f:
-            if "bits=8" in f.read():
-                kind = "a8"
-    except OSError:
-        pass
-    return QTensor(h, kind)
+    q = QTensor(h)
+    bits, gran, _ = q.scheme
+    q.kind = "a8" if gran == ODY_PER_TOKEN else ("w8" if bits == 8 else ("w4g" if gran == ODY_PER_GROUP else "w4"))
+    return q

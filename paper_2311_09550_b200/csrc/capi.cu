@@ -165,6 +165,17 @@ struct DevBuf {  // stream-ordered device temporary
     ~DevBuf() {
         if (p) cudaFreeAsync(p, st);
     }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFreeAsync(p, st);
+            p = o.p;
+            st = o.st;
+            o.p = nullptr;
+        }
+        return *this;
+    }
     T* release() {
         T* q = p;
         p = nullptr;
@@ -181,11 +192,20 @@ struct ody_tensor {
     ~ody_tensor() { pinned().put(data); }
 };
 
-enum class QKind { Act8, Weight4 };
+// Act8: per-token INT8 (a8 layout); Weight4: per-channel INT4 (W4 tile layout);
+// Weight4G: per-group INT4 (W4 tile layout, scales [rows][cols/group]); Weight8:
+// per-channel INT8 (W8 layout).
+enum class QKind { Act8, Weight4, Weight4G, Weight8 };
 
 struct ody_qtensor {
     QKind kind;
     size_t rows = 0, cols = 0;
+    size_t group_size = 128;  // the scheme's group_size (ref tensor.hpp:80), written to scheme.txt
+    size_t groups() const { return kind == QKind::Weight4G ? cols / group_size : 1; }
+    int bits() const { return kind == QKind::Act8 || kind == QKind::Weight8 ? 8 : 4; }
+    const char* granularity() const {
+        return kind == QKind::Act8 ? "per_token" : (kind == QKind::Weight4G ? "per_group" : "per_channel");
+    }
     void* codes = nullptr;  // device, kernel layout
     float* scales = nullptr;  // device
     ~ody_qtensor() {
@@ -254,6 +274,123 @@ void run_gemm(const ody_qtensor* a_q, const ody_qtensor* w_q, float* out_dev, in
     g.max_ctas = r.sms;
     g.pdl = false;
     cuda_check(launch_w4a8_gemm(g, st), "w4a8_gemm launch");
+}
+
+void require_per_token_i8(const ody_qtensor* a_q) {  // ref gemm.cpp:26-30
+    if (a_q->kind != QKind::Act8) fail(ODY_EINVAL, "GEMM: activations must be symmetric per-token INT8");
+}
+void check_k(size_t k) {  // ref gemm.cpp:14-20
+    if (k > kMaxK) fail(ODY_EINVAL, "GEMM: K exceeds the 32-bit accumulator safety bound 2^17");
+}
+
+// The comparison engines (ref gemm.cpp:313-333 run_engine), each in the reference's
+// validation order, on the GPU (engine_kernel.cu); counters are the reference's formulas.
+void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q, const ody_qtensor* w_q,
+                    ody_gemm_counters* counters, ody_tensor** out) {
+    Runtime& r = rt();
+    std::lock_guard<std::mutex> lock(r.mu);
+    cudaStream_t st = r.stream;
+    const bool w4 = w_q->kind == QKind::Weight4 || w_q->kind == QKind::Weight4G;
+    ody_gemm_counters c = {};
+    size_t m = 0, n = w_q->rows, k = w_q->cols;
+    DevBuf<float> od(0, st);
+    if (engine == ODY_ENGINE_W4A16) {  // ref gemm.cpp:100-104
+        if (a_dense->cols != w_q->cols) fail(ODY_EINVAL, "gemm_w4a16_grouped: inner dims disagree");
+        if (!w4) fail(ODY_EINVAL, "gemm_w4a16_grouped: weights must be 4-bit");
+        m = a_dense->rows;
+        if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff) fail(ODY_EINVAL, "GEMM: dimension exceeds int32 range");
+        DevBuf<float> ad(m * k, st);
+        cuda_check(cudaMemcpyAsync(ad.p, a_dense->data, m * k * 4, cudaMemcpyHostToDevice, st), "H2D a");
+        od = DevBuf<float>(m * n, st);
+        cuda_check(launch_w4a16(ad.p, static_cast<const uint8_t*>(w_q->codes), w_q->scales, static_cast<int>(m),
+                                static_cast<int>(n), static_cast<int>(k),
+                                static_cast<int>(w_q->kind == QKind::Weight4G ? w_q->group_size : k), od.p, st),
+                   "w4a16 launch");
+        c.dequant_events = static_cast<uint64_t>(m) * n * k;
+    } else {
+        EngineArgs e = {};
+        DevBuf<uint8_t> offset(0, st), regroup_w(0, st);
+        DevBuf<int8_t> regroup_a(0, st);
+        m = a_q->rows;
+        e.qa = static_cast<const int8_t*>(a_q->codes);
+        e.K = static_cast<int>(k);
+        if (engine == ODY_ENGINE_FINEGRAINED) {  // ref gemm.cpp:125-133
+            require_per_token_i8(a_q);
+            if (a_q->cols != w_q->cols) fail(ODY_EINVAL, "gemm_w4a8_finegrained: inner dims disagree");
+            if (!w4) fail(ODY_EINVAL, "gemm_w4a8_finegrained: weights must be 4-bit");
+            const size_t g = w_q->kind == QKind::Weight4G ? w_q->group_size : k;
+            if (g == 0 || k % g != 0) fail(ODY_EINVAL, "gemm_w4a8_finegrained: g does not divide K");
+            check_k(g);
+            e.mode = kEngineFine;
+            e.group = static_cast<int>(g);
+            e.w = static_cast<const uint8_t*>(w_q->codes);
+            e.qa = static_cast<const int8_t*>(a_q->codes);
+            e.K = static_cast<int>(k);
+            if (g % 32 != 0) {  // whole MMA k-steps per group: both operands re-laid out
+                const size_t g32 = (g + 31) / 32 * 32, kq = (k / g) * g32;
+                regroup_w = DevBuf<uint8_t>(w4_packed_bytes(n, kq), st);
+                regroup_a = DevBuf<int8_t>(a8_bytes(m, kq), st);
+                cuda_check(launch_regroup(e.w, e.qa, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                                          static_cast<int>(g), regroup_w.p, regroup_a.p, st),
+                           "finegrained regroup");
+                e.w = regroup_w.p;
+                e.qa = regroup_a.p;
+                e.K = static_cast<int>(kq);
+                e.group = static_cast<int>(g32);
+            }
+            c.int8_mac_ops = static_cast<uint64_t>(m) * n * k;
+            c.dequant_events = static_cast<uint64_t>(m) * n * (k / g);
+        } else if (engine == ODY_ENGINE_ASYMMETRIC) {  // ref gemm.cpp:320-325, 163-172
+            if (w_q->kind != QKind::Weight4) fail(ODY_EINVAL, "asymmetric engine: weights must be per-channel 4-bit");
+            require_per_token_i8(a_q);
+            if (a_q->cols != k) fail(ODY_EINVAL, "gemm_w4a8_asymmetric: inner dims disagree");
+            check_k(k);
+            // the reference re-packs to UINT4 + 8 on every call (run_engine): so does this engine
+            offset = DevBuf<uint8_t>(w4_packed_bytes(n, k), st);
+            cuda_check(launch_w4_offset(static_cast<const uint8_t*>(w_q->codes), static_cast<int>(n),
+                                        static_cast<int>(k), offset.p, st),
+                       "w4 offset repack");
+            e.mode = kEngineAsym;
+            e.w = offset.p;
+            c.zero_point_sub_ops = static_cast<uint64_t>(n) * k;
+            c.int8_mac_ops = static_cast<uint64_t>(m) * n * k;
+            c.dequant_events = static_cast<uint64_t>(m) * n;
+            c.final_scale_ops = static_cast<uint64_t>(m) * n;
+        } else {  // ODY_ENGINE_W8A8, ref gemm.cpp:281-287
+            require_per_token_i8(a_q);
+            if (w_q->kind != QKind::Weight8) fail(ODY_EINVAL, "gemm_w8a8: weights must be per-channel 8-bit");
+            if (a_q->cols != w_q->cols) fail(ODY_EINVAL, "gemm_w8a8: inner dims disagree");
+            check_k(k);
+            e.mode = kEngineW8A8;
+            e.w = static_cast<const uint8_t*>(w_q->codes);
+            c.int8_mac_ops = static_cast<uint64_t>(m) * n * k;
+            c.dequant_events = static_cast<uint64_t>(m) * n;
+            c.final_scale_ops = static_cast<uint64_t>(m) * n;
+        }
+        if (m > 0x7fffffff || n > 0x7fffffff) fail(ODY_EINVAL, "GEMM: dimension exceeds int32 range");
+        od = DevBuf<float>(m * n, st);
+        e.sw = w_q->scales;
+        e.sa = a_q->scales;
+        e.out = od.p;
+        e.M = static_cast<int>(m);
+        e.N = static_cast<int>(n);
+        const size_t wsb = engine_workspace_bytes(e.mode, e.M, e.N, e.K);
+        DevBuf<uint8_t> ws(wsb, st);
+        if (wsb) cuda_check(cudaMemsetAsync(ws.p, 0, wsb, st), "memset engine workspace");
+        e.workspace = ws.p;
+        e.workspace_bytes = wsb;
+        cuda_check(launch_engine_gemm(e, st), "engine gemm launch");
+    }
+    ody_tensor* t = new_tensor(m, n);
+    cudaError_t err = cudaMemcpyAsync(t->data, od.p, m * n * 4, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) {
+        delete t;
+        cuda_check(err, "ody_gemm");
+    }
+    if (counters) *counters = c;
+    *out = t;
 }
 
 }  // namespace
@@ -330,34 +467,46 @@ ody_status ody_quantize_weights(const ody_tensor* w, int bits, ody_granularity g
                                          (arr == clip_gamma ? "clip_gamma" : "clip_beta") +
                                          " outside (0,1]");
         }
-        if (bits != 4 || granularity != ODY_PER_CHANNEL)
-            fail(ODY_EINVAL,
-                 "quantize_weights: the B200 FastGEMM path takes bits=4, per_channel weights");
+        if (bits == 8 && granularity == ODY_PER_GROUP)
+            fail(ODY_EINVAL, "quantize_weights: 8-bit per_group weights feed no engine of the B200 path");
         if (w->rows > 0x7fffffff || w->cols > 0x7fffffff) fail(ODY_EINVAL, "quantize_weights: too large");
         Runtime& r = rt();
         cudaStream_t st = r.stream;
         const size_t n = w->rows, k = w->cols;
+        const QKind kind = bits == 8 ? QKind::Weight8 : (granularity == ODY_PER_GROUP ? QKind::Weight4G : QKind::Weight4);
+        const size_t groups = kind == QKind::Weight4G ? k / group_size : 1;
         DevBuf<float> wd(n * k, st);
         cuda_check(cudaMemcpyAsync(wd.p, w->data, n * k * 4, cudaMemcpyHostToDevice, st), "H2D w");
         DevBuf<float> gd(clip_gamma ? n : 0, st), bd(clip_beta ? n : 0, st);
         if (clip_gamma) cuda_check(cudaMemcpyAsync(gd.p, clip_gamma, n * 4, cudaMemcpyHostToDevice, st), "H2D");
         if (clip_beta) cuda_check(cudaMemcpyAsync(bd.p, clip_beta, n * 4, cudaMemcpyHostToDevice, st), "H2D");
-        DevBuf<uint8_t> packed(w4_packed_bytes(n, k), st);
-        DevBuf<float> scales(n, st);
+        DevBuf<uint8_t> packed(kind == QKind::Weight8 ? w8_bytes(n, k) : w4_packed_bytes(n, k), st);
+        DevBuf<float> scales(n * groups, st);
         DevBuf<int> err(1, st);
         cuda_check(cudaMemsetAsync(err.p, 0, sizeof(int), st), "memset");
-        cuda_check(launch_w4_quant_prepack(wd.p, static_cast<int>(n), static_cast<int>(k), 4,
-                                           clip_gamma ? gd.p : nullptr, clip_beta ? bd.p : nullptr,
-                                           packed.p, scales.p, err.p, st),
-                   "w4 quantize launch");
+        const float* g = clip_gamma ? gd.p : nullptr;
+        const float* b = clip_beta ? bd.p : nullptr;
+        if (kind == QKind::Weight4)
+            cuda_check(launch_w4_quant_prepack(wd.p, static_cast<int>(n), static_cast<int>(k), 4, g, b, packed.p,
+                                               scales.p, err.p, st),
+                       "w4 quantize launch");
+        else if (kind == QKind::Weight4G)  // gamma/beta validated on the host above
+            cuda_check(launch_wg_quant_prepack(wd.p, static_cast<int>(n), static_cast<int>(k),
+                                               static_cast<int>(group_size), 4, g, b, packed.p, scales.p, st),
+                       "w4 per-group quantize launch");
+        else
+            cuda_check(launch_w8_quant(wd.p, static_cast<int>(n), static_cast<int>(k), g, b,
+                                       reinterpret_cast<int8_t*>(packed.p), scales.p, err.p, st),
+                       "w8 quantize launch");
         int herr = 0;
         cuda_check(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         sync(st, "ody_quantize_weights");
         if (herr) fail(ODY_EINVAL, "compute_scale_symmetric: gamma/beta outside (0,1]");
         auto* q = new ody_qtensor();
-        q->kind = QKind::Weight4;
+        q->kind = kind;
         q->rows = n;
         q->cols = k;
+        q->group_size = group_size;
         q->codes = packed.release();
         q->scales = scales.release();
         *out = q;
@@ -397,9 +546,13 @@ ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out) {
         cudaStream_t st = rt().stream;
         const size_t r = q->rows, c = q->cols;
         DevBuf<float> d(r * c, st);
-        if (q->kind == QKind::Act8)
+        if (q->kind == QKind::Act8 || q->kind == QKind::Weight8)  // W8 is the a8 layout over the rows
             cuda_check(launch_a8_unpack(static_cast<const int8_t*>(q->codes), q->scales,
                                         static_cast<int>(r), static_cast<int>(c), nullptr, d.p, st),
+                       "dequant launch");
+        else if (q->kind == QKind::Weight4G)
+            cuda_check(launch_wg_dequant(static_cast<const uint8_t*>(q->codes), q->scales, static_cast<int>(r),
+                                         static_cast<int>(c), static_cast<int>(q->group_size), d.p, st),
                        "dequant launch");
         else
             cuda_check(launch_w4_dequant(static_cast<const uint8_t*>(q->codes), q->scales,
@@ -427,8 +580,10 @@ ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qten
             fail(ODY_EINVAL, "ody_gemm: w4a16 engine needs a_dense");
         if (engine != ODY_ENGINE_W4A16 && !a_q)
             fail(ODY_EINVAL, "ody_gemm: engine needs quantized activations");
-        if (engine != ODY_ENGINE_FAST)
-            fail(ODY_EINVAL, "ody_gemm: only ODY_ENGINE_FAST is implemented on the B200 path");
+        if (engine != ODY_ENGINE_FAST) {
+            run_engine_abi(engine, a_dense, a_q, w_q, counters, out);
+            return;
+        }
         check_fast_inputs(a_q, w_q);
         Runtime& r = rt();
         std::lock_guard<std::mutex> lock(r.mu);
@@ -756,7 +911,7 @@ ody_status ody_qtensor_export(const ody_qtensor* q, void* codes_or_nibbles, floa
         cudaStream_t st = rt().stream;
         const size_t r = q->rows, c = q->cols;
         if (codes_or_nibbles) {
-            if (q->kind == QKind::Act8) {
+            if (q->kind == QKind::Act8 || q->kind == QKind::Weight8) {
                 DevBuf<int8_t> d(r * c, st);
                 cuda_check(launch_a8_unpack(static_cast<const int8_t*>(q->codes), q->scales,
                                             static_cast<int>(r), static_cast<int>(c), d.p, nullptr, st),
@@ -774,10 +929,18 @@ ody_status ody_qtensor_export(const ody_qtensor* q, void* codes_or_nibbles, floa
             }
         }
         if (scales) {
-            cuda_check(cudaMemcpyAsync(scales, q->scales, r * 4, cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaMemcpyAsync(scales, q->scales, r * q->groups() * 4, cudaMemcpyDeviceToHost, st), "D2H");
             sync(st, "ody_qtensor_export");
         }
     });
+}
+
+ody_status ody_qtensor_scheme(const ody_qtensor* q, int* bits, ody_granularity* granularity, size_t* group_size) {
+    if (!q || !bits || !granularity || !group_size) return einval("ody_qtensor_scheme: null argument");
+    *bits = q->bits();
+    *granularity = q->kind == QKind::Act8 ? ODY_PER_TOKEN : (q->kind == QKind::Weight4G ? ODY_PER_GROUP : ODY_PER_CHANNEL);
+    *group_size = q->group_size;
+    return ODY_OK;
 }
 
 ody_status ody_qtensor_import_w4(size_t n, size_t k, const void* flat, const float* scales,
@@ -992,11 +1155,11 @@ ody_status ody_qtensor_write(const ody_qtensor* q, const char* dir) {
     return guarded([&] {
         std::error_code ec;
         std::filesystem::create_directories(dir, ec);
-        const size_t r = q->rows, c = q->cols;
+        const size_t r = q->rows, c = q->cols, groups = q->groups();
         OtfRaw pay, sc;
         pay.dims = {r, c};
-        std::vector<float> scales(r);
-        if (q->kind == QKind::Act8) {
+        std::vector<float> scales(r * groups);
+        if (q->bits() == 8) {
             pay.dtype = kOtfI8;
             pay.payload.resize(r * c);
         } else {
@@ -1008,14 +1171,14 @@ ody_status ody_qtensor_write(const ody_qtensor* q, const char* dir) {
         const std::string d(dir);
         otf_write(pay, d + "/payload.otf");
         sc.dtype = kOtfF32;
-        sc.dims = {r, 1};
-        sc.payload.resize(r * 4);
-        std::memcpy(sc.payload.data(), scales.data(), r * 4);
+        sc.dims = {r, groups};  // ref otf.cpp:138-140: rows x groups_per_row
+        sc.payload.resize(r * groups * 4);
+        std::memcpy(sc.payload.data(), scales.data(), r * groups * 4);
         otf_write(sc, d + "/scales.otf");
         std::FILE* f = std::fopen((d + "/scheme.txt").c_str(), "w");
         if (!f) fail(ODY_EIO, "write_tensor: cannot open " + d + "/scheme.txt");
-        std::fprintf(f, "bits=%d\nsymmetric=1\ngranularity=%s\ngroup_size=0\n", q->kind == QKind::Act8 ? 8 : 4,
-                     q->kind == QKind::Act8 ? "per_token" : "per_channel");
+        std::fprintf(f, "bits=%d\nsymmetric=1\ngranularity=%s\ngroup_size=%zu\n", q->bits(), q->granularity(),
+                     q->group_size);
         std::fclose(f);
     });
 }
@@ -1048,14 +1211,35 @@ ody_status ody_qtensor_read(const char* dir, ody_qtensor** out) {
         if (bits == 8 && pay.dtype != kOtfI8) fail(ODY_EPARSE, "8-bit tensor payload must be i8");
         std::vector<float> scales = otf_floats(otf_read(d + "/scales.otf"));
         if (!sym) fail(ODY_EINVAL, "read_tensor: asymmetric tensors are not supported on the B200 path");
-        if (scales.size() != r) fail(ODY_EINVAL, "QuantizedTensor: scales size mismatch");
-        if (bits == 4 && gran == "per_channel") {
+        const size_t group_size = static_cast<size_t>(std::stoull(kv["group_size"]));
+        const bool per_group = gran == "per_group";
+        if (per_group && (group_size == 0 || c % group_size != 0))
+            fail(ODY_EINVAL, "QuantScheme: group size does not divide axis length");
+        const size_t groups = per_group ? c / group_size : 1;
+        if (scales.size() != r * groups) fail(ODY_EINVAL, "QuantizedTensor: scales size mismatch");
+        for (float v : scales)  // ref tensor.cpp:161-165
+            if (!(v > 0.0f) || !std::isfinite(v)) fail(ODY_EINVAL, "QuantizedTensor: non-positive scale");
+        if (bits == 4 && (gran == "per_channel" || per_group)) {
             const ody_status st = ody_qtensor_import_w4(r, c, pay.payload.data(), scales.data(), out);
             if (st != ODY_OK) fail(st, g_last_error);
-        } else if (bits == 8 && gran == "per_token") {
+            if (per_group) {  // the same codes layout, scales [rows][groups]
+                ody_qtensor* q = *out;
+                cudaStream_t s2 = rt().stream;
+                DevBuf<float> sd(r * groups, s2);
+                cuda_check(cudaMemcpyAsync(sd.p, scales.data(), r * groups * 4, cudaMemcpyHostToDevice, s2), "H2D");
+                sync(s2, "ody_qtensor_read");
+                cudaFreeAsync(q->scales, s2);
+                q->scales = sd.release();
+                q->kind = QKind::Weight4G;
+            }
+            (*out)->group_size = group_size;
+        } else if (bits == 8 && (gran == "per_token" || gran == "per_channel")) {
+            // per-token activations and per-channel INT8 weights share the a8 layout
             const ody_status st = ody_qtensor_import_a8(r, c, reinterpret_cast<const int8_t*>(pay.payload.data()),
                                                         scales.data(), out);
             if (st != ODY_OK) fail(st, g_last_error);
+            if (gran == "per_channel") (*out)->kind = QKind::Weight8;
+            (*out)->group_size = group_size;
         } else {
             fail(ODY_EINVAL, "read_tensor: " + std::to_string(bits) + "-bit " + gran +
                                  " tensors are not supported on the B200 path");

@@ -134,6 +134,42 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
 
 int device_sm_count();
 
+// engine_kernel.cu: the reference's comparison engines (ref gemm.cpp:100-311) on tcgen05.
+enum : int { kEngineFast = 0, kEngineAsym = 1, kEngineW8A8 = 2, kEngineFine = 3 };
+struct EngineArgs {
+    int mode;
+    const uint8_t* w;     // W4 tile layout (FAST/FINE), its UINT4+8 twin (ASYM), W8 layout (W8A8)
+    const float* sw;      // [N], or [N][K/group] (FINE)
+    const int8_t* qa;     // a8 k-block layout
+    const float* sa;
+    float* out;           // M x N f32 row-major
+    int M, N, K;
+    int group;            // FINE: group size (multiple of 32, divides K)
+    void* workspace;      // engine_workspace_bytes, zeroed once (left zeroed)
+    size_t workspace_bytes;
+};
+int engine_splits(int mode, int M, int N, int K);
+size_t engine_workspace_bytes(int mode, int M, int N, int K);
+cudaError_t launch_engine_gemm(const EngineArgs& a, cudaStream_t st);
+// per-row symmetric scale (ref quantize.cpp:22-35), bits 4 or 8; err set on bad gamma/beta
+cudaError_t launch_w_scale(const float* w, int N, int K, int bits, const float* gamma, const float* beta,
+                           float* s, int* err, cudaStream_t st);
+// per-group INT4 weights (scales [N][K/g]) into the W4 tile layout
+cudaError_t launch_wg_quant_prepack(const float* w, int N, int K, int g, int bits, const float* gamma,
+                                    const float* beta, uint8_t* packed, float* s, cudaStream_t st);
+// per-channel INT8 weights into the W8 layout (a8 k-block layout over the padded rows)
+size_t w8_bytes(size_t n, size_t k);
+cudaError_t launch_w8_quant(const float* w, int N, int K, const float* gamma, const float* beta, int8_t* codes,
+                            float* s, int* err, cudaStream_t st);
+cudaError_t launch_w4_offset(const uint8_t* packed, int N, int K, uint8_t* out, cudaStream_t st);
+// FINEGRAINED with g % 32 != 0: W4 tiles and a8 codes re-laid out over K' = (K/g)*ceil32(g)
+cudaError_t launch_regroup(const uint8_t* w4, const int8_t* qa, int M, int N, int K, int g, uint8_t* w4_out,
+                           int8_t* qa_out, cudaStream_t st);
+cudaError_t launch_wg_dequant(const uint8_t* packed, const float* s, int N, int K, int g, float* out,
+                              cudaStream_t st);
+cudaError_t launch_w4a16(const float* a, const uint8_t* packed, const float* s, int M, int N, int K, int g,
+                         float* out, cudaStream_t st);
+
 // aux_kernels.cu: the reference's offline / float-oracle numerics, bit-exact.
 // LWC grid search (ref clip.cpp:55-103): w is N x K f32 on the device; per-row outputs.
 int lwc_max_candidates();

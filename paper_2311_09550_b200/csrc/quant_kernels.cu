@@ -470,6 +470,14 @@ cudaError_t launch_w4_quant_prepack(const float* w, int N, int K, int bits, cons
     return cudaGetLastError();
 }
 
+cudaError_t launch_w_scale(const float* w, int N, int K, int bits, const float* gamma, const float* beta,
+                           float* s, int* err, cudaStream_t st) {
+    w_scale_kernel<<<(N + 7) / 8, 256, 0, st>>>(w, N, K, bits, gamma, beta, s, err);
+    return cudaGetLastError();
+}
+
+size_t w8_bytes(size_t n, size_t k) { return pad_n(n) * pad_k(k); }
+
 cudaError_t launch_w4_prepack_flat(const uint8_t* flat, int N, int K, uint8_t* packed,
                                    cudaStream_t st) {
     const int Np = static_cast<int>(pad_n(N)), Kp = static_cast<int>(pad_k(K));

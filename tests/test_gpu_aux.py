@@ -56,7 +56,7 @@ def test_otf_write_is_byte_identical(golden, tmp_path):
     from paper_2311_09550_b200 import api
     c = cases(golden, "otf")[0]
     w = f32_from_bits(c["w_bits"]).reshape(3, 5)
-    q = api.quantize_weights(w)
+    q = api.quantize_weights(w, 4, 1, 128)  # the reference's per_channel(4): group_size 128 in scheme.txt
     d = str(tmp_path / "w.q")
     q.write(d)
     for fname, key in (("payload.otf", "payload_otf"), ("scales.otf", "scales_otf"), ("scheme.txt", "scheme_txt")):
