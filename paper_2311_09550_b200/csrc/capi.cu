@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -74,11 +75,15 @@ ody_status einval(const char* msg) {
 // ---------------------------------------------------------------- runtime
 // One library stream for the host-handle API; device memory from the stream-ordered
 // pool (cudaMallocAsync) so per-call temporaries cost no driver round trip.
+std::atomic<cudaStream_t> g_lib_stream{nullptr};  // the library stream (PinnedPool events)
+
 struct Runtime {
     std::mutex mu;          // serialises host-API GEMMs (shared workspace)
     cudaStream_t stream = nullptr;
     void* workspace = nullptr;
     size_t workspace_bytes = 0;
+    void* pscratch = nullptr;  // decode-width ody_gemm: dynamic decode kernel scratch
+    size_t pscratch_bytes = 0;
     int sms = 0;
     std::string version;
 };
@@ -96,6 +101,7 @@ Runtime& rt() {
         }
         x->sms = prop.multiProcessorCount;
         cuda_check(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking), "stream");
+        g_lib_stream.store(x->stream);
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
@@ -112,16 +118,33 @@ Runtime& rt() {
 
 // Pooled pinned host buffers back ody_tensor so H2D/D2H run at full PCIe rate and
 // repeated calls do not pay cudaHostAlloc.
+// Page-locked host buffers for ody_tensor data, pooled.  A buffer returned while a
+// stream-ordered copy from it may still be pending (ody_quantize_activations does not
+// synchronize) carries an event recorded on the library stream at return time; it is
+// handed out again only once that event completed.  Pooled bytes are capped: past the
+// cap a returned buffer is released (after its event).
 struct PinnedPool {
+    struct Entry {
+        void* p;
+        cudaEvent_t ev;  // completes when the library stream passed the buffer's last use
+    };
+    static constexpr size_t kCapBytes = size_t(1) << 30;
     std::mutex mu;
-    std::multimap<size_t, void*> free_list;
+    std::multimap<size_t, Entry> free_list;
+    std::map<void*, size_t> sizes;
+    size_t pooled = 0;
     void* get(size_t bytes) {
         bytes = std::max<size_t>(bytes, 256);
         {
             std::lock_guard<std::mutex> l(mu);
-            auto it = free_list.lower_bound(bytes);
-            if (it != free_list.end() && it->first <= 2 * bytes) {
-                void* p = it->second;
+            for (auto it = free_list.lower_bound(bytes); it != free_list.end() && it->first <= 2 * bytes; ++it) {
+                if (it->second.ev && cudaEventQuery(it->second.ev) != cudaSuccess) {
+                    cudaGetLastError();  // cudaErrorNotReady is not an error here
+                    continue;
+                }
+                void* p = it->second.p;
+                if (it->second.ev) cudaEventDestroy(it->second.ev);
+                pooled -= it->first;
                 free_list.erase(it);
                 return p;
             }
@@ -145,9 +168,28 @@ struct PinnedPool {
             std::free(p);
             return;
         }
-        free_list.emplace(it->second, p);
+        cudaEvent_t ev = nullptr;
+        cudaStream_t st = g_lib_stream.load();
+        if (st && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+            if (cudaEventRecord(ev, st) != cudaSuccess) {
+                cudaEventDestroy(ev);
+                ev = nullptr;
+                cudaStreamSynchronize(st);
+            }
+        }
+        cudaGetLastError();
+        if (pooled + it->second > kCapBytes) {  // over the cap: release it instead
+            if (ev) {
+                cudaEventSynchronize(ev);
+                cudaEventDestroy(ev);
+            }
+            cudaFreeHost(p);
+            sizes.erase(it);
+            return;
+        }
+        pooled += it->second;
+        free_list.emplace(it->second, Entry{p, ev});
     }
-    std::map<void*, size_t> sizes;
 };
 PinnedPool& pinned() {
     static PinnedPool* p = new PinnedPool();
@@ -248,6 +290,31 @@ void check_fast_inputs(const ody_qtensor* a_q, const ody_qtensor* w_q) {
 void run_gemm(const ody_qtensor* a_q, const ody_qtensor* w_q, float* out_dev, int32_t* acc_dev,
               cudaStream_t st) {
     Runtime& r = rt();
+    const int M = static_cast<int>(a_q->rows), N = static_cast<int>(w_q->rows), K = static_cast<int>(w_q->cols);
+    if (gemm_prequant_eligible(M, N, K)) {  // decode widths: the dynamic decode kernel
+        const size_t need = gemm_prequant_scratch_bytes(M, N, K);
+        if (r.pscratch_bytes < need) {
+            if (r.pscratch) cuda_check(cudaFreeAsync(r.pscratch, st), "cudaFreeAsync");
+            r.pscratch = nullptr;
+            cuda_check(cudaMallocAsync(&r.pscratch, need, st), "cudaMallocAsync scratch");
+            cuda_check(cudaMemsetAsync(r.pscratch, 0, program_zero_bytes(), st), "cudaMemsetAsync scratch");
+            r.pscratch_bytes = need;
+        }
+        GemmArgs g = {};
+        g.qa = static_cast<const int8_t*>(a_q->codes);
+        g.sa = a_q->scales;
+        g.wp = static_cast<const uint8_t*>(w_q->codes);
+        g.sw = w_q->scales;
+        g.out = out_dev;
+        g.out_dtype = kDtypeF32;
+        g.acc_out = acc_dev;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.max_ctas = r.sms;
+        cuda_check(launch_w4a8_gemm_prequant(g, r.pscratch, r.pscratch_bytes, st), "w4a8 decode gemm launch");
+        return;
+    }
     const size_t need = gemm_workspace_bytes(static_cast<int>(a_q->rows), static_cast<int>(w_q->rows),
                                              static_cast<int>(w_q->cols), r.sms);
     if (r.workspace_bytes < need) {
@@ -407,11 +474,22 @@ void ody_set_threads(int n) { (void)n; }  // no host worker threads on the GPU p
 ody_status ody_tensor_create(size_t rows, size_t cols, const float* data, ody_tensor** out) {
     if (!data || !out) return einval("ody_tensor_create: null argument");
     return guarded([&] {
-        for (size_t i = 0; i < rows * cols; ++i) {  // ref tensor.cpp:21-27
-            if (!std::isfinite(data[i])) fail(ODY_EINVAL, "DenseTensor: non-finite value");
-        }
+        // ref tensor.cpp:21-27 (reject NaN/Inf), fused with the copy into pinned memory:
+        // one vectorizable pass over the exponent bits
         ody_tensor* t = new_tensor(rows, cols);
-        std::memcpy(t->data, data, rows * cols * sizeof(float));
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(data);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(t->data);
+        uint32_t bad = 0;
+        const size_t nel = rows * cols;
+        for (size_t i = 0; i < nel; ++i) {
+            const uint32_t b = src[i];
+            dst[i] = b;
+            bad |= static_cast<uint32_t>((b & 0x7f800000u) == 0x7f800000u);
+        }
+        if (bad) {
+            delete t;
+            fail(ODY_EINVAL, "DenseTensor: non-finite value");
+        }
         *out = t;
     });
 }
@@ -529,7 +607,9 @@ ody_status ody_quantize_activations(const ody_tensor* a, ody_qtensor** out) {
         cuda_check(launch_act_quant(xd.p, kDtypeF32, k, static_cast<int>(m), static_cast<int>(k),
                                     q.p, s.p, nullptr, nullptr, false, st),
                    "act_quant launch");
-        sync(st, "ody_quantize_activations");
+        // no synchronize: the qtensor lives on the library stream (every later use is
+        // ordered after this launch) and the source tensor's pinned buffer is only reused
+        // after the stream passed this copy (PinnedPool)
         auto* qt = new ody_qtensor();
         qt->kind = QKind::Act8;
         qt->rows = m;

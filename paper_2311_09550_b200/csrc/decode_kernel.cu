@@ -990,7 +990,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint32_t* flag = reinterpret_cast<uint32_t*>(items + kItemSlots);
     uint32_t* tmem_slot = flag + 1;
     uint32_t* emax = tmem_slot + 1;  // [BN] the CTA's per-token max |y| of the current item
-    float* ssc = reinterpret_cast<float*>(emax + 64);  // [2][64] token scales of the item (parity)
+    // [2][64] token scales of the item (parity), 16-byte aligned for ld.shared.v4
+    float* ssc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(emax + 64) + 15) & ~uintptr_t(15));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
@@ -1043,8 +1044,14 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             // tiles of a unit are one contiguous run
             auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
                 mbar_expect_tx(&b_full[s], nb * kBBlockBytes);
-                bulk_g2s(ring + s * kStageBytes + kUnitBytes, d.qa + static_cast<size_t>(kb) * d.Mp * 128,
-                         nb * kBBlockBytes, &b_full[s], pol_b);
+                if (d.Mp == BN) {  // compact a8 (BN rows per k-block): one contiguous run
+                    bulk_g2s(ring + s * kStageBytes + kUnitBytes, d.qa + static_cast<size_t>(kb) * d.Mp * 128,
+                             nb * kBBlockBytes, &b_full[s], pol_b);
+                } else {           // 128-row padded a8 (an ody_qtensor): rows 0..BN-1 per k-block
+                    for (int b = 0; b < nb; ++b)
+                        bulk_g2s(ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
+                                 d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
+                }
             };
             auto release_deferred = [&]() {
                 // The ring is full and the B tiles wait for the act quant (i.e. for the
@@ -1513,19 +1520,28 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             int32_t* const accp = ld_keep_ptr(d.acc_out);
             float* const sa_outp = (depi && x.nt == 0 && r == 0) ? ld_keep_ptr(d.sa_out) : nullptr;
             const bool amx_on = d.amax_dst != nullptr;
-            const bool own = fin && n < n_cols;
+            const bool own = fin && n < n_cols && !(p.dbg & 16);  // dbg 16 (diag build): no stores
             const bool amx = amx_on && n >= d.amax_c0 && n < d.amax_c1;
+            float sat[16];  // the token scales of 16 tokens at a time, loaded ahead of the stores
 #pragma unroll
             for (int t = 0; t < BN; ++t) {
+                if ((t & 15) == 0) {
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const uint4 s4 = lds128(smem_u32(tsc + t + 4 * q4));
+                        sat[4 * q4] = __uint_as_float(s4.x);
+                        sat[4 * q4 + 1] = __uint_as_float(s4.y);
+                        sat[4 * q4 + 2] = __uint_as_float(s4.z);
+                        sat[4 * q4 + 3] = __uint_as_float(s4.w);
+                    }
+                }
                 if (t < m_rows) {
                     const size_t idx = static_cast<size_t>(t) * n_cols + n;
                     if (accp) {
                         if (own) stg_b32(accp + idx, v[t]);  // pre-shift (TP all-reduce)
                         continue;
                     }
-                    // explicit ld.shared: a generic load here (tsc is a generic pointer) is
-                    // ordered behind the previous token's global stores
-                    const float sa_t = __uint_as_float(lds32(smem_u32(tsc + t)));
+                    const float sa_t = sat[t & 15];
                     if (sa_outp && own) stg_b32(sa_outp + t, __float_as_uint(sa_t));
                     const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
                     const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa_t, sw_n));
@@ -1923,8 +1939,12 @@ size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L) {
     int mmax = 1;
     for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
     size_t b = kZeroRegion + dyn_items(a, L) * dyn_bn(mmax) * kTileN * 4;  // + split partials
-    for (int l = 0; l < L; ++l)
-        if (!deps || deps[l] < 0) b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
+    for (int l = 0; l < L; ++l) {
+        if (!deps || deps[l] < 0)
+            b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
+        else  // dependency chain: the grid-wide quantized x (compact a8, BN rows)
+            b += round_up(static_cast<size_t>(dyn_bn(mmax)) * pad_k(a[l].K), 256);
+    }
     return b;
 }
 
@@ -2140,7 +2160,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         int ib = 0, tb = 0;
         for (int l = 0; l < L; ++l) {
             LinDesc& d = sorted[l];
-            d.split = dyn_split(d.kblocks);
+            // a lone linear is split like a chain link (all SMs, short last wave); in a
+            // program the other linears' items fill the machine
+            d.split = L == 1 ? chain_split(d.n_tiles, d.kblocks, std::min(sms, device_sm_count())) : dyn_split(d.kblocks);
             if (l == L - 1 && L > 1 && tail_kb > 0) d.split = std::max(d.split, (d.kblocks + tail_kb - 1) / tail_kb);
             d.ibase = ib;
             d.tbase = tb;
@@ -2188,6 +2210,60 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
 cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st) {
     return launch_w4a8_program(&a, nullptr, 1, a.workspace, a.workspace_bytes, a.pdl, a.next_wp, a.next_bytes,
                                st);
+}
+
+
+// ody_gemm's decode widths (M <= 64) on pre-quantized activations (an ody_qtensor: the
+// 128-row padded a8 layout): the dynamic decode kernel as a program of ONE linear, its
+// k-split chosen like a chain link's so every SM streams weights.
+size_t gemm_prequant_scratch_bytes(int M, int N, int K) {
+    const int sms = device_sm_count();
+    const int kb = static_cast<int>(pad_k(K) / kBlockK), nt = static_cast<int>(pad_n(N) / kTileN);
+    return kZeroRegion + static_cast<size_t>(nt) * chain_split(nt, kb, sms) * dyn_bn(M) * kTileN * 4;
+}
+
+bool gemm_prequant_eligible(int M, int N, int K) {
+    return M >= 1 && M <= 64 && N >= 1 && K >= 1 && pad_n(N) / kTileN <= kProgramMaxTiles;
+}
+
+cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& g, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+    if (!gemm_prequant_eligible(g.M, g.N, g.K)) return cudaErrorInvalidValue;
+    if (!scratch || scratch_bytes < gemm_prequant_scratch_bytes(g.M, g.N, g.K)) return cudaErrorInvalidValue;
+    const int sms = std::min(g.max_ctas > 0 ? g.max_ctas : device_sm_count(), device_sm_count());
+    PParams p = {};
+    p.L = 1;
+    LinDesc& d = p.lin[0];
+    d.wp = g.wp;
+    d.sw = g.sw;
+    d.out = g.out;
+    d.out_dtype = g.out_dtype;
+    d.acc_out = g.acc_out;
+    d.M = g.M;
+    d.N = g.N;
+    d.K = g.K;
+    d.kblocks = static_cast<int>(pad_k(g.K) / kBlockK);
+    d.n_tiles = static_cast<int>(pad_n(g.N) / kTileN);
+    d.qa = g.qa;
+    d.sa = g.sa;
+    d.Mp = static_cast<int>(pad_m(g.M));
+    d.dep = -1;
+    d.split = chain_split(d.n_tiles, d.kblocks, sms);
+    p.n_items = d.n_tiles * d.split;
+    uint32_t* counters = static_cast<uint32_t*>(scratch);
+    p.ctr = counters;
+    p.work = counters + kMaxLin + 1;
+    p.tile_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kProgramCounterRegion);
+    p.acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kAccOffset);
+    p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
+    p.S = 1;
+    p.C = std::min(sms, p.n_items);
+    p.pdl = g.pdl ? 1 : 0;
+    p.trace = g.trace;
+    switch (dyn_bn(g.M)) {
+        case 16: return launch_dyn<16, false>(p, g.pdl, st);
+        case 32: return launch_dyn<32, false>(p, g.pdl, st);
+        default: return launch_dyn<64, false>(p, g.pdl, st);
+    }
 }
 
 }  // namespace odyb200

@@ -74,6 +74,12 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, cudaStream_t st);
 bool prefill_eligible(int M, int N, int K);
 void set_prefill_min_m(int m);  // 0 disables
 cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st);
+// Decode widths (M <= 64) on pre-quantized 128-row a8 activations: the dynamic decode
+// kernel as a one-linear program (decode_kernel.cu).  scratch: gemm_prequant_scratch_bytes,
+// its first program_zero_bytes() zeroed once (left zeroed).
+bool gemm_prequant_eligible(int M, int N, int K);
+size_t gemm_prequant_scratch_bytes(int M, int N, int K);
+cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& a, void* scratch, size_t scratch_bytes, cudaStream_t st);
 
 // The W4A8 linear y = x W^T end to end from unquantized activations: K1 fused into the
 // GEMM (decode widths, one kernel) or act_quant + GEMM.  workspace: linear_scratch_bytes.

@@ -203,12 +203,13 @@ def test_program_independent_layer(m, torch_cuda, dev):
             assert torch.equal(c.out, ref), name
 
 
-def test_program_dependency_chain(torch_cuda, dev):
+@pytest.mark.parametrize("m", [1, 16, 17, 32, 48, 64])
+def test_program_dependency_chain(torch_cuda, dev, m):
     """x of each linear is (a column slice of) an earlier linear's output inside the same
     launch: grid-wide completion counters order them; bit-identical to sequential runs,
-    eagerly, back to back and from a CUDA graph."""
+    eagerly, back to back and from a CUDA graph.  Every decode width (BN = 16/32/64), in
+    a workspace of exactly the queried size."""
     torch = torch_cuda
-    m = 16
     dims = [(3072, 1024), (1024, 2048), (2048, 1024), (1024, 2048)]  # (n, k); x1 = out0[:, :2048]
     ws = [_weights(torch, dev, n, k, seed=200 + i, scale=0.03)[0] for i, (n, k) in enumerate(dims)]
     x0 = torch.randn((m, 1024), device="cuda").half()

@@ -19,14 +19,20 @@ H, I = 5120, 13824
 LAYERS = [("qkv", 3 * H, H), ("o", H, H), ("gate_up", 2 * I, H), ("down", H, I)]
 
 
-def main(m=16):
-    ws = [dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1) for _, n, k in LAYERS]
-    x = (torch.randn((m, H), device="cuda") * 2).half()
-    outs = [torch.empty((m, n), dtype=torch.float16, device="cuda") for _, n, _ in LAYERS]
-    prog = dev.Program([dev.LinearCall(x, ws[0], outs[0]),
-                        dev.LinearCall(outs[0][:, :H], ws[1], outs[1], dep=0),
-                        dev.LinearCall(outs[1], ws[2], outs[2], dep=1),
-                        dev.LinearCall(outs[2][:, :I], ws[3], outs[3], dep=2)])
+def main(m=16, single=None):
+    if single:  # one linear (n, k) as a program of one
+        n, k = single
+        w = dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1)
+        x = (torch.randn((m, k), device="cuda") * 2).half()
+        prog = dev.Program([dev.LinearCall(x, w, torch.empty((m, n), dtype=torch.float16, device="cuda"))])
+    else:
+        ws = [dev.W4Weight.quantize(torch.randn((n, k), device="cuda") * 0.1) for _, n, k in LAYERS]
+        x = (torch.randn((m, H), device="cuda") * 2).half()
+        outs = [torch.empty((m, n), dtype=torch.float16, device="cuda") for _, n, _ in LAYERS]
+        prog = dev.Program([dev.LinearCall(x, ws[0], outs[0]),
+                            dev.LinearCall(outs[0][:, :H], ws[1], outs[1], dep=0),
+                            dev.LinearCall(outs[1], ws[2], outs[2], dep=1),
+                            dev.LinearCall(outs[2][:, :I], ws[3], outs[3], dep=2)])
     for _ in range(3):
         prog.run()
     torch.cuda.synchronize()
@@ -78,5 +84,8 @@ def main(m=16):
 
 
 if __name__ == "__main__":
-    for m in (1, 16):
-        main(m)
+    if len(sys.argv) > 2:  # chain_trace.py N K [M]: one linear
+        main(int(sys.argv[3]) if len(sys.argv) > 3 else 16, (int(sys.argv[1]), int(sys.argv[2])))
+    else:
+        for m in (1, 16):
+            main(m)
