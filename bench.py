@@ -384,6 +384,69 @@ def config1(args, dev, stream):
             "kernel": "act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (program of one linear)"}
 
 
+def engines_ablation(args, stream):
+    """The paper's dequantization-scheme ablation (Fig. 7) on B200: the
+    reference's engines (ref gemm.cpp:100-311) through ody_gemm_dev on pre-quantized
+    activations, one 13B o-proj-sized GEMM (N = K = 5120) at decode M = 16 and prefill
+    M = 1024.  FAST = the FastGEMM kernels; ASYMMETRIC / FINEGRAINED (g = 128) / W8A8 =
+    engine_kernel.cu (ASYMMETRIC re-packs to UINT4+8 every call, as the reference does);
+    W4A16 = the reference's sequential-f32 engine (decode only).  Rotating weight copies
+    (> L2 at decode); CUDA-event time per call on the stream."""
+    import numpy as np
+    import torch
+
+    from paper_2311_09550_b200 import api
+    from paper_2311_09550_b200._lib import lib
+    hbm, _ = peaks()
+    res = {}
+    rs = np.random.default_rng(11)
+    n = k = 5120
+    for m, copies in ((16, 8), (1024, 2)):
+        a = (rs.standard_normal((m, k), dtype=np.float32) * 2).astype(np.float32)
+        aq = api.quantize_activations_per_token(a)
+        a_dev = torch.from_numpy(a).cuda()
+        wf = [(rs.standard_normal((n, k), dtype=np.float32) * 0.1).astype(np.float32) for _ in range(copies)]
+        ws = {"fast": (3, [api.quantize_weights(w) for w in wf]),
+              "asymmetric": (2, [api.quantize_weights(w) for w in wf]),
+              "finegrained_g128": (1, [api.quantize_weights(w, 4, 3, 128) for w in wf]),
+              "w8a8": (4, [api.quantize_weights(w, 8, 1, 128) for w in wf])}
+        if m == 16:
+            ws["w4a16_g128"] = (0, ws["finegrained_g128"][1])
+        del wf
+        out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+        row = {}
+        for name, (eng, wl) in ws.items():
+            def call(w, eng=eng):
+                rc = lib().ody_gemm_dev(eng, a_dev.data_ptr() if eng == 0 else None, m, None if eng == 0 else aq._h,
+                                        w._h, out.data_ptr(), None, stream.cuda_stream)
+                if rc:
+                    raise RuntimeError(f"ody_gemm_dev({name}) failed: {lib().ody_last_error()}")
+            with torch.cuda.stream(stream):
+                for w in wl:
+                    call(w)
+            torch.cuda.synchronize()
+            reps = 10 if (m == 1024 or eng == 0) else 40
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                s0.record(stream)
+                for _ in range(reps):
+                    for w in wl:
+                        call(w)
+                e0.record(stream)
+            torch.cuda.synchronize()
+            us = s0.elapsed_time(e0) * 1e3 / (reps * len(wl))
+            wbytes = n * k if name == "w8a8" else n * k // 2
+            byts = wbytes + m * k + 4 * n + 4 * m + 4 * m * n
+            row[name] = {"us": round(us, 2), "GB/s": round(byts / (us * 1e-6) / 1e9, 1),
+                         "frac_hbm": round(byts / (us * 1e-6) / 1e9 / hbm, 3),
+                         "TOPS": round(2.0 * m * n * k / (us * 1e-6) / 1e12, 1)}
+        res[f"M{m}"] = row
+        del ws, aq
+        torch.cuda.empty_cache()
+    return {"shape": {"N": n, "K": k}, "per_M": res, "out": "f32 (the reference's engines return f32)",
+            "note": "ody_gemm_dev per call incl. launch; ASYMMETRIC includes its per-call UINT4+8 repack"}
+
+
 def decode_sweep(args, dev, h, stream):
     """configs[1] sweep: the chain step at M = 1..64 (one program launch per step)."""
     import torch
@@ -658,6 +721,7 @@ def run_b200(args):
         result["config1"] = config1(args, dev, stream)
         result["sweep_M"] = decode_sweep(args, dev, h, stream)
         result["prefill"] = prefill_roofline(args, dev, h, stream)
+        result["engines"] = engines_ablation(args, stream)
     h = None
     torch.cuda.empty_cache()
     if not args.quick:

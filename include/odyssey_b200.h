@@ -100,6 +100,12 @@ ody_status ody_dequantize(const ody_qtensor* q, ody_tensor** out);
  * order and counter formulas); returns a new host f32 tensor. */
 ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q,
                     const ody_qtensor* w_q, ody_gemm_counters* counters, ody_tensor** out);
+/* ody_gemm on device memory, stream-ordered (no host copies, no synchronization): out_dev
+ * (m x n f32, device) <- engine(a_q, w_q).  W4A16 takes device f32 activations a_dev
+ * (a_rows x w cols) instead of a_q.  stream NULL = the library stream.  Calls share the
+ * library's workspaces: order them on one stream. */
+ody_status ody_gemm_dev(ody_engine engine, const float* a_dev, size_t a_rows, const ody_qtensor* a_q,
+                        const ody_qtensor* w_q, float* out_dev, ody_gemm_counters* counters, void* stream);
 
 /* Reference OTF files and float oracles (ref odyssey.h:71-75, 80-81, 100-101).
  * ody_qtensor_read builds the DEVICE qtensor straight from an `odyssey quantize` output

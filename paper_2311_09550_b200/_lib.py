@@ -95,6 +95,8 @@ SIGNATURES = {
     "ody_qtensor_export": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ody_qtensor_import_w4": (c_int, [c_size_t, c_size_t, c_void_p, c_void_p, POINTER(c_void_p)]),
     "ody_qtensor_import_a8": (c_int, [c_size_t, c_size_t, c_void_p, c_void_p, POINTER(c_void_p)]),
+    "ody_gemm_dev": (c_int, [c_int, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p, POINTER(ody_gemm_counters),
+                             c_void_p]),
     "ody_qtensor_scheme": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_size_t)]),
     "ody_gemm_accumulators": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ody_b200_version": (c_char_p, []),

@@ -84,6 +84,8 @@ struct Runtime {
     size_t workspace_bytes = 0;
     void* pscratch = nullptr;  // decode-width ody_gemm: dynamic decode kernel scratch
     size_t pscratch_bytes = 0;
+    void* escratch = nullptr;  // comparison engines: split-K sums + tile counters
+    size_t escratch_bytes = 0;
     int sms = 0;
     std::string version;
 };
@@ -352,26 +354,21 @@ void check_k(size_t k) {  // ref gemm.cpp:14-20
 
 // The comparison engines (ref gemm.cpp:313-333 run_engine), each in the reference's
 // validation order, on the GPU (engine_kernel.cu); counters are the reference's formulas.
-void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q, const ody_qtensor* w_q,
-                    ody_gemm_counters* counters, ody_tensor** out) {
-    Runtime& r = rt();
-    std::lock_guard<std::mutex> lock(r.mu);
-    cudaStream_t st = r.stream;
+// Stream-ordered: out_dev (m x n f32) is written on `st`; a_dev is W4A16's f32
+// activations on the device (m rows).
+void engine_core(ody_engine engine, const float* a_dev, size_t a_rows, size_t a_cols, const ody_qtensor* a_q,
+                 const ody_qtensor* w_q, float* out_dev, ody_gemm_counters* counters, cudaStream_t st) {
     const bool w4 = w_q->kind == QKind::Weight4 || w_q->kind == QKind::Weight4G;
     ody_gemm_counters c = {};
     size_t m = 0, n = w_q->rows, k = w_q->cols;
-    DevBuf<float> od(0, st);
     if (engine == ODY_ENGINE_W4A16) {  // ref gemm.cpp:100-104
-        if (a_dense->cols != w_q->cols) fail(ODY_EINVAL, "gemm_w4a16_grouped: inner dims disagree");
+        if (a_cols != w_q->cols) fail(ODY_EINVAL, "gemm_w4a16_grouped: inner dims disagree");
         if (!w4) fail(ODY_EINVAL, "gemm_w4a16_grouped: weights must be 4-bit");
-        m = a_dense->rows;
+        m = a_rows;
         if (m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff) fail(ODY_EINVAL, "GEMM: dimension exceeds int32 range");
-        DevBuf<float> ad(m * k, st);
-        cuda_check(cudaMemcpyAsync(ad.p, a_dense->data, m * k * 4, cudaMemcpyHostToDevice, st), "H2D a");
-        od = DevBuf<float>(m * n, st);
-        cuda_check(launch_w4a16(ad.p, static_cast<const uint8_t*>(w_q->codes), w_q->scales, static_cast<int>(m),
+        cuda_check(launch_w4a16(a_dev, static_cast<const uint8_t*>(w_q->codes), w_q->scales, static_cast<int>(m),
                                 static_cast<int>(n), static_cast<int>(k),
-                                static_cast<int>(w_q->kind == QKind::Weight4G ? w_q->group_size : k), od.p, st),
+                                static_cast<int>(w_q->kind == QKind::Weight4G ? w_q->group_size : k), out_dev, st),
                    "w4a16 launch");
         c.dequant_events = static_cast<uint64_t>(m) * n * k;
     } else {
@@ -391,8 +388,6 @@ void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qten
             e.mode = kEngineFine;
             e.group = static_cast<int>(g);
             e.w = static_cast<const uint8_t*>(w_q->codes);
-            e.qa = static_cast<const int8_t*>(a_q->codes);
-            e.K = static_cast<int>(k);
             if (g % 32 != 0) {  // whole MMA k-steps per group: both operands re-laid out
                 const size_t g32 = (g + 31) / 32 * 32, kq = (k / g) * g32;
                 regroup_w = DevBuf<uint8_t>(w4_packed_bytes(n, kq), st);
@@ -435,19 +430,41 @@ void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qten
             c.final_scale_ops = static_cast<uint64_t>(m) * n;
         }
         if (m > 0x7fffffff || n > 0x7fffffff) fail(ODY_EINVAL, "GEMM: dimension exceeds int32 range");
-        od = DevBuf<float>(m * n, st);
         e.sw = w_q->scales;
         e.sa = a_q->scales;
-        e.out = od.p;
+        e.out = out_dev;
         e.M = static_cast<int>(m);
         e.N = static_cast<int>(n);
+        // split-K sums + tile counters: runtime-owned, zeroed once (the kernel leaves them zeroed)
         const size_t wsb = engine_workspace_bytes(e.mode, e.M, e.N, e.K);
-        DevBuf<uint8_t> ws(wsb, st);
-        if (wsb) cuda_check(cudaMemsetAsync(ws.p, 0, wsb, st), "memset engine workspace");
-        e.workspace = ws.p;
-        e.workspace_bytes = wsb;
+        Runtime& r = rt();
+        if (wsb > r.escratch_bytes) {
+            if (r.escratch) cuda_check(cudaFreeAsync(r.escratch, st), "cudaFreeAsync");
+            r.escratch = nullptr;
+            cuda_check(cudaMallocAsync(&r.escratch, wsb, st), "cudaMallocAsync engine workspace");
+            cuda_check(cudaMemsetAsync(r.escratch, 0, wsb, st), "memset engine workspace");
+            r.escratch_bytes = wsb;
+        }
+        e.workspace = r.escratch;
+        e.workspace_bytes = r.escratch_bytes;
         cuda_check(launch_engine_gemm(e, st), "engine gemm launch");
     }
+    if (counters) *counters = c;
+}
+
+void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qtensor* a_q, const ody_qtensor* w_q,
+                    ody_gemm_counters* counters, ody_tensor** out) {
+    Runtime& r = rt();
+    std::lock_guard<std::mutex> lock(r.mu);
+    cudaStream_t st = r.stream;
+    const size_t m = engine == ODY_ENGINE_W4A16 ? a_dense->rows : a_q->rows, n = w_q->rows;
+    DevBuf<float> od(m * n, st);
+    DevBuf<float> ad(engine == ODY_ENGINE_W4A16 ? a_dense->rows * a_dense->cols : 0, st);
+    if (engine == ODY_ENGINE_W4A16)
+        cuda_check(cudaMemcpyAsync(ad.p, a_dense->data, a_dense->rows * a_dense->cols * 4, cudaMemcpyHostToDevice, st),
+                   "H2D a");
+    engine_core(engine, ad.p, engine == ODY_ENGINE_W4A16 ? a_dense->rows : 0,
+                engine == ODY_ENGINE_W4A16 ? a_dense->cols : 0, a_q, w_q, od.p, counters, st);
     ody_tensor* t = new_tensor(m, n);
     cudaError_t err = cudaMemcpyAsync(t->data, od.p, m * n * 4, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess) err = cudaGetLastError();
@@ -456,7 +473,6 @@ void run_engine_abi(ody_engine engine, const ody_tensor* a_dense, const ody_qten
         delete t;
         cuda_check(err, "ody_gemm");
     }
-    if (counters) *counters = c;
     *out = t;
 }
 
@@ -686,6 +702,28 @@ ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qten
             counters->final_scale_ops = static_cast<uint64_t>(m) * n;
         }
         *out = t;
+    });
+}
+
+ody_status ody_gemm_dev(ody_engine engine, const float* a_dev, size_t a_rows, const ody_qtensor* a_q,
+                        const ody_qtensor* w_q, float* out_dev, ody_gemm_counters* counters, void* stream) {
+    if (!w_q || !out_dev) return einval("ody_gemm_dev: null argument");
+    return guarded([&] {
+        if (engine < ODY_ENGINE_W4A16 || engine > ODY_ENGINE_W8A8) fail(ODY_EINVAL, "bad engine enum");
+        if (engine == ODY_ENGINE_W4A16 && !a_dev) fail(ODY_EINVAL, "ody_gemm_dev: w4a16 engine needs a_dev");
+        if (engine != ODY_ENGINE_W4A16 && !a_q) fail(ODY_EINVAL, "ody_gemm_dev: engine needs quantized activations");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt().stream;
+        if (engine == ODY_ENGINE_FAST) {
+            check_fast_inputs(a_q, w_q);
+            run_gemm(a_q, w_q, out_dev, nullptr, st);
+            if (counters) {
+                const uint64_t m = a_q->rows, n = w_q->rows, k = w_q->cols;
+                *counters = {m * n * k, m * n, 0, m * n};
+            }
+        } else {
+            engine_core(engine, a_dev, a_rows, w_q->cols, a_q, w_q, out_dev, counters, st);
+        }
+        cuda_check(cudaGetLastError(), "ody_gemm_dev");
     });
 }
 
