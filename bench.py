@@ -83,6 +83,15 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def i8_peak():
+    """Measured whole-GPU dense INT8 peak (tools/i8_peak.cu; profiles/i8_peak.json)."""
+    p = os.path.join(ROOT, "profiles", "i8_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("i8_dense_tops_measured")
+    return None
+
+
 def bf16_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -487,8 +496,14 @@ def prefill_roofline(args, dev, h, stream, m=1024):
         tot_ops += ops
         tot_ms += ms
     tops = tot_ops / (tot_ms * 1e-3) / 1e12
+    i8m = i8_peak()
+    if i8m:
+        for v in res.values():
+            v["frac_measured"] = round(v["TOPS"] / i8m, 3)
     return {"bound": "tensor", "M": m, "achieved": round(tops, 1), "peak": INT8_PEAK_TOPS, "unit": "TOP/s",
             "frac": round(tops / INT8_PEAK_TOPS, 3),
+            "peak_measured": i8m, "frac_measured": round(tops / i8m, 3) if i8m else None,
+            "peak_measured_source": "tools/i8_peak.cu (profiles/r2_i8_peak.md): sustained, power-capped ~1.59 GHz",
             "frac_of_2x_measured_bf16": round(tops / (2 * bf16), 3) if bf16 else None,
             "kernel": "w4a8_prefill_kernel (2-SM tcgen05 kind::i8, 256 weight rows x BT tokens per CTA pair)",
             "layer_us": round(tot_ms * 1e3, 1), "per_shape": res, "traffic": "profiles/r2_prefill_ncu.md"}
