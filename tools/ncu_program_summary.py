@@ -83,13 +83,18 @@ def main():
     ap.add_argument("--rep", required=True)
     ap.add_argument("--launches", required=True)
     ap.add_argument("--tag", default="r1")
+    ap.add_argument("--chain", action="store_true", help="the capture is the dependent chain (prof_program.py --chain)")
     args = ap.parse_args()
+    what = "chain" if args.chain else "program"
     hdr, units, vals = raw(args.rep)
-    lines = [f"# Decode linear program, ncu --set full ({args.tag})", "",
+    desc = ("the DEPENDENT chain qkv -> o(qkv[:, :5120]) -> gate_up -> down(gate_up[:, :13824]) (bench.py's "
+            "headline step: dependent linears' x quantized in-kernel grid-wide)" if args.chain else
+            "the 4 linears as INDEPENDENT inputs")
+    lines = [f"# Decode linear {what}, ncu --set full ({args.tag})", "",
              "Command: `ncu --set full --clock-control none --import-source on -k regex:w4a8_decode_dyn -s 2 "
-             "-c 1 python tools/prof_program.py` -- ONE launch of w4a8_decode_dyn_kernel running the "
-             "LLaMA-13B decoder layer's 4 linears (qkv, o, gate_up, down) at M=16 on pre-quantized "
-             "activations; cold L2, serialised, unlocked clocks (compare bytes and shares, not absolutes).",
+             f"-c 1 python tools/prof_program.py{' --chain' if args.chain else ''}` -- ONE launch of "
+             "w4a8_decode_dyn_kernel running the LLaMA-13B decoder layer's 4 linears (qkv, o, gate_up, down) at "
+             f"M=16: {desc}; cold L2, serialised, unlocked clocks (compare bytes and shares, not absolutes).",
              "", "| metric | value |", "|---|---|"]
     traffic = 0.0
     for key, label in WANT:
@@ -98,7 +103,11 @@ def main():
             lines.append(f"| {label} (`{key}`) | {vals[i]} {units[i]} |")
             if key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 traffic += float(vals[i].replace(",", "")) * SCALE.get(units[i], 1)
-    alg = 158597120 + 4 * (15360 + 5120 + 27648 + 5120) + 16 * (5120 * 3 + 13824) + 2 * 16 * (15360 + 5120 + 27648 + 5120)
+    if args.chain:  # bench.py linear_bytes: INT4 W + scales + fp16 x + fp16 y + token scales
+        alg = sum(n * k // 2 + 4 * n + 2 * 16 * k + 2 * 16 * n + 4 * 16
+                  for n, k in ((15360, 5120), (5120, 5120), (27648, 5120), (5120, 13824)))
+    else:
+        alg = 158597120 + 4 * (15360 + 5120 + 27648 + 5120) + 16 * (5120 * 3 + 13824) + 2 * 16 * (15360 + 5120 + 27648 + 5120)
     lines += ["", f"DRAM traffic {traffic / 1e6:.2f} MB vs algorithmic {alg / 1e6:.2f} MB "
               f"(INT4 weights + scales + int8 activation tiles + fp16 outputs): ratio {traffic / alg:.3f} -- "
               "every weight byte is fetched from HBM once.", ""]
@@ -106,7 +115,7 @@ def main():
     if st:
         lines += ["Warp-state samples (source page), top reasons:", "", "| reason | samples | share |", "|---|---|---|"]
         lines += [f"| {k} | {v} | {f:.1%} |" for k, v, f in st]
-    open(os.path.join(ROOT, "profiles", f"{args.tag}_program_ncu.md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(ROOT, "profiles", f"{args.tag}_{what}_ncu.md"), "w").write("\n".join(lines) + "\n")
 
     d, meta = launches(args.launches)
     fam = collections.defaultdict(list)
@@ -115,7 +124,7 @@ def main():
     total = sum(x.get("gpu__time_duration.sum", 0) for v in fam.values() for x in v)
     out = [f"# Launch list inside bench.py's timed region ({args.tag})", "",
            "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
-           "-k \"regex:w4a8|act_quant\" -s 20 -c 24 python bench.py --steps 20 --warmup 3 --no-cpu` -- "
+           "-k \"regex:w4a8|act_quant\" -s 20 -c 24 python bench.py --steps 20 --warmup 3 --no-cpu --quick` -- "
            "serialised, cold-cache per-launch device times: only the SHARE of each kernel is meaningful.", "",
            "| kernel | grid | launches | mean us | mean DRAM read MB | share of device time |", "|---|---|---|---|---|---|"]
     for (name, grid), v in sorted(fam.items(), key=lambda kv: -sum(x.get("gpu__time_duration.sum", 0) for x in kv[1])):
@@ -123,11 +132,11 @@ def main():
         rd = [x.get("dram__bytes_read.sum", 0) for x in v]
         out.append(f"| `{name}` | {grid} | {len(v)} | {sum(t) / len(t):.2f} | {sum(rd) / len(rd) / 1e6:.2f} | "
                    f"{sum(t) / total:.1%} |")
-    open(os.path.join(ROOT, "profiles", f"{args.tag}_program_launches.md"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(ROOT, "profiles", f"{args.tag}_{what}_launches.md"), "w").write("\n".join(out) + "\n")
     tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     js = json.load(open(tp)) if os.path.exists(tp) else {}
-    js["program_M16"] = int(traffic)
-    js["program_M16_source"] = f"profiles/{args.tag}_program_ncu.md"
+    js[f"{what}_M16"] = int(traffic)
+    js[f"{what}_M16_source"] = f"profiles/{args.tag}_{what}_ncu.md"
     json.dump(js, open(tp, "w"), indent=1)
     print("\n".join(lines))
     print("\n".join(out))
