@@ -936,12 +936,27 @@ constexpr int kDynConvGroups = 2;
 constexpr int kDynEpi0 = 12;
 constexpr int kItemSlots = 8;
 // Per-BN configuration of the dynamic kernel (BN = 16/32/64 tokens per MMA N).
-template <int BN, bool DEP>
+template <int BN, bool DEP, int UB = 2>
 struct DynCfg {
+    // Pipeline unit: UB k-blocks (UB * 8 KiB of packed weights, a UB*32-column TMEM A stage).
+    // The MMA warp's per-unit fixed cost (two mbarrier waits ~100 cycles each even when
+    // already complete, commits, loop: ~350 cycles, tools/mma_loop_bench.cu) is amortised
+    // over UB k-blocks: UB = 4 for a lone linear (config 1: 18.2 -> 12.1 us), UB = 2 for
+    // multi-linear programs, whose deeper rings and A-stage count measured faster (37.5 vs
+    // 41.3 us for the layer's 4 linears).
+    static constexpr int kUB = UB;
+    static constexpr int kUBytes = kUB * kWBlockBytes;
+    static constexpr int kAStageColsD = kUB * kBlockK / 4;
     static constexpr int kBBlock = BN * 128;                            // one B k-block tile
-    static constexpr int kStageBytes = kUnitBytes + kUnitBlocks * kBBlock;  // weights + B tiles
+    static constexpr int kStageBytes = kUBytes + kUB * kBBlock;         // weights + B tiles
     static constexpr int kStages = (220 * 1024 - 3072) / kStageBytes < 10 ? (220 * 1024 - 3072) / kStageBytes : 10;
     static constexpr int kSmem = kStages * kStageBytes + 2048 /*barriers, items*/ + 1024 /*alignment*/;
+    // TMEM: kDBufs accumulator buffers (BN columns each) at column 0, then as many 64-column
+    // A stages as fit.  The converter -> MMA -> commit -> converter handshake has ~1 us of
+    // round-trip latency, so the unit rate is A stages / that latency (measured: 0.32 us per
+    // unit with 4 stages, unchanged with the MMAs and TMEM stores removed).
+    static constexpr int kAColBase = kDBufs * BN;
+    static constexpr int kAStages = (kTmemCols - kAColBase) / kAStageColsD;
     // kind::i8, D=s32, A=B=s8 signed, K-major both, N=BN, M=128
     static constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                        (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
@@ -967,9 +982,9 @@ __device__ __forceinline__ DynItem dyn_item(const PParams& p, const LinDesc* lin
     return x;
 }
 
-template <int BN, bool DEP>
+template <int BN, bool DEP, int UB>
 __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const __grid_constant__ PParams p) {
-    using C = DynCfg<BN, DEP>;
+    using C = DynCfg<BN, DEP, UB>;
     constexpr int kDynStages = C::kStages;
     constexpr int kStageBytes = C::kStageBytes;
     constexpr int kBBlockBytes = C::kBBlock;
@@ -981,8 +996,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint64_t* w_empty = w_full + kDynStages;
     uint64_t* b_full = w_empty + kDynStages;
     uint64_t* a_full = b_full + kDynStages;
-    uint64_t* a_empty = a_full + kAStages;
-    uint64_t* d_full = a_empty + kAStages;
+    uint64_t* a_empty = a_full + C::kAStages;
+    uint64_t* d_full = a_empty + C::kAStages;
     uint64_t* d_empty = d_full + kDBufs;
     uint64_t* i_full = d_empty + kDBufs;
     uint64_t* i_empty = i_full + kItemSlots;
@@ -1005,7 +1020,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             mbar_init(&w_empty[i], 5);  // 4 converter warps read W, the MMA consumed B
             mbar_init(&b_full[i], 1);
         }
-        for (int i = 0; i < kAStages; ++i) {
+        for (int i = 0; i < C::kAStages; ++i) {
             mbar_init(&a_full[i], 4);
             mbar_init(&a_empty[i], 1);
         }
@@ -1045,11 +1060,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             auto issue_b = [&](const LinDesc& d, int s, int kb, int nb) {
                 mbar_expect_tx(&b_full[s], nb * kBBlockBytes);
                 if (d.Mp == BN) {  // compact a8 (BN rows per k-block): one contiguous run
-                    bulk_g2s(ring + s * kStageBytes + kUnitBytes, d.qa + static_cast<size_t>(kb) * d.Mp * 128,
+                    bulk_g2s(ring + s * kStageBytes + C::kUBytes, d.qa + static_cast<size_t>(kb) * d.Mp * 128,
                              nb * kBBlockBytes, &b_full[s], pol_b);
                 } else {           // 128-row padded a8 (an ody_qtensor): rows 0..BN-1 per k-block
                     for (int b = 0; b < nb; ++b)
-                        bulk_g2s(ring + s * kStageBytes + kUnitBytes + b * kBBlockBytes,
+                        bulk_g2s(ring + s * kStageBytes + C::kUBytes + b * kBBlockBytes,
                                  d.qa + static_cast<size_t>(kb + b) * d.Mp * 128, kBBlockBytes, &b_full[s], pol_b);
                 }
             };
@@ -1184,12 +1199,12 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 const DynItem x = dyn_item(p, p.lin, it);
                 const LinDesc& d = p.lin[x.l];
                 const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
-                const int nunits = (x.kb_hi - x.kb_lo + kUnitBlocks - 1) / kUnitBlocks;
+                const int nunits = (x.kb_hi - x.kb_lo + C::kUB - 1) / C::kUB;
                 // A dependent linear's B tiles are quantized in-kernel by the converters once
                 // its producer linear completes.  While it has not, keep HBM streaming: pull
                 // this whole item's weights into L2 (the ring then refills from L2).
                 const bool depi = d.qdone != nullptr;
-                if (depi && lane == 0 && ld_acquire_u32(d.qdone) < d.qtarget)
+                if (depi && lane == 0 && !(p.dbg & 64) && ld_acquire_u32(d.qdone) < d.qtarget)
                     bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
                                      static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
@@ -1203,8 +1218,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     if (k < nunits) {
                         const int Uk = U + k;
                         const int s = Uk % kDynStages;
-                        const int kb = x.kb_lo + kUnitBlocks * k;
-                        const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                        const int kb = x.kb_lo + C::kUB * k;
+                        const int nb = min(C::kUB, x.kb_hi - kb);
                         mbar_expect_tx(&w_full[s], nb * kWBlockBytes);
                         bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol);
@@ -1259,24 +1274,24 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             const uint32_t d_tmem = tmem + db * BN;
             mbar_wait(&d_empty[db], ((JD / kDBufs) & 1) ^ 1);
             tc_fence_after();
-            for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
-                const int nb = min(kUnitBlocks, x.kb_hi - kb);
-                const int as = U % kAStages;
+            for (int kb = x.kb_lo; kb < x.kb_hi; kb += C::kUB, ++U) {
+                const int nb = min(C::kUB, x.kb_hi - kb);
+                const int as = U % C::kAStages;
                 const int s = U % kDynStages;
-                mbar_wait(&a_full[as], (U / kAStages) & 1);
+                mbar_wait(&a_full[as], (U / C::kAStages) & 1);
                 if (utr && lane == 0 && U < 64) utr[8 * U + 1] = globaltimer();
                 mbar_wait(&b_full[s], (U / kDynStages) & 1);
                 if (utr && lane == 0 && U < 64) utr[8 * U + 6] = globaltimer();
                 tc_fence_after();
-                const uint32_t a_tmem = tmem + kAColBase + as * kAStageCols;
-                const uint32_t b0 = smem_u32(ring) + s * kStageBytes + kUnitBytes;
+                const uint32_t a_tmem = tmem + C::kAColBase + as * C::kAStageColsD;
+                const uint32_t b0 = smem_u32(ring) + s * kStageBytes + C::kUBytes;
                 if (elect_one()) {
 #pragma unroll
-                    for (int c = 0; c < 4 * kUnitBlocks; ++c)
-                        if (c < 4 * nb)
+                    for (int c = 0; c < 4 * C::kUB; ++c)
+                        if (c < 4 * nb && !((p.dbg & 128) && (kb > x.kb_lo || c > 0)))  // dbg 128: first MMA only
                             mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b0 + (c / 4) * kBBlockBytes + 32 * (c % 4)),
                                       C::kIdesc, (kb > x.kb_lo || c > 0) ? 1u : 0u);
-                    mma_commit(&a_empty[as]);
+                    if (!(p.dbg & 1024)) mma_commit(&a_empty[as]);  // dbg 1024 (diag, unsafe): no A-stage handshake
                     mma_commit(&w_empty[s]);
                     if (kb + nb >= x.kb_hi) mma_commit(&d_full[db]);
                 }
@@ -1309,8 +1324,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             named_bar_sync(4, 64);
             int nq = 0;
             for (int kb = static_cast<int>(blockIdx.x); kb < d.kblocks; kb += static_cast<int>(gridDim.x), ++nq) {
-                // BN rows x 8 sixteen-element chunks of k-block kb
-#pragma unroll 1
+                // BN rows x 8 sixteen-element chunks of k-block kb (unrolled: every load of
+                // a thread is in flight at once, one L2 round trip)
+#pragma unroll
                 for (int task = qt; task < BN * 8; task += 64) {
                     const int t = task >> 3, c = task & 7;
                     const int k0 = kb * kBlockK + c * 16;
@@ -1340,7 +1356,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                                               ((c ^ (t & 7)) << 4)) = v;
                 }
             }
-            fence_proxy_async_global();  // generic writes -> the consumers' bulk copies
+            // no writer-side proxy fence: each consumer orders its bulk copies (async proxy)
+            // after its acquire of qdone with fence.proxy.async (the `released` check); the
+            // release below publishes these generic stores at gpu scope
             named_bar_sync(4, 64);
             if (qt == 0 && nq > 0) red_release_add_u32(d.qdone, static_cast<uint32_t>(nq));
             if (trc && qt == 0 && l < 4) trc[13 + 4 * l] = globaltimer();
@@ -1358,44 +1376,52 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             if (lane == 0) mbar_arrive(&i_empty[is]);
             if (it < 0) break;
             const DynItem x = dyn_item(p, p.lin, it);
-            for (int kb = x.kb_lo; kb < x.kb_hi; kb += kUnitBlocks, ++U) {
+            for (int kb = x.kb_lo; kb < x.kb_hi; kb += C::kUB, ++U) {
                 // the group owning ring stage U % kDynStages widens this unit (stage
                 // ownership keeps every w_full waiter in phase order on odd-length rings)
                 if ((U % kDynStages) % kDynConvGroups != grp) continue;
-                const int nb = min(kUnitBlocks, x.kb_hi - kb);
+                const int nb = min(C::kUB, x.kb_hi - kb);
                 const int s = U % kDynStages;
-                const int as = U % kAStages;
+                const int as = U % C::kAStages;
                 mbar_wait(&w_full[s], (U / kDynStages) & 1);
                 if (utr && r == 0 && U < 64) utr[8 * U + 4] = globaltimer();
                 const uint32_t src = smem_u32(ring) + s * kStageBytes + r * 16;
-                uint32_t lanes8[kUnitBlocks][32];
+                if (!(p.dbg & 1024)) mbar_wait(&a_empty[as], ((U / C::kAStages) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dst = tmem + (static_cast<uint32_t>(32 * q) << 16) + C::kAColBase + as * C::kAStageColsD;
+                // two k-blocks at a time (64 words in registers), each straight to TMEM
 #pragma unroll
-                for (int b = 0; b < kUnitBlocks; ++b) {
-                    if (b < nb) {
+                for (int h = 0; h < C::kUB; h += 2) {
+                    if (h < nb) {
+                        uint32_t lanes8[2][32];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const uint4 v = lds128(src + b * kWBlockBytes + c * 2048);
-                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                        for (int b2 = 0; b2 < 2; ++b2) {
+                            const int b = h + b2;
 #pragma unroll
-                            for (int jj = 0; jj < 4; ++jj) {
-                                lanes8[b][c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k 8jj+0..3
-                                lanes8[b][c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k 8jj+4..7
+                            for (int c = 0; c < 4; ++c) {
+                                const uint4 v = (b < nb && !(p.dbg & 512)) ? lds128(src + b * kWBlockBytes + c * 2048)
+                                                                           : make_uint4(0u, 0u, 0u, 0u);
+                                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj) {
+                                    lanes8[b2][c * 8 + 2 * jj] = (w[jj] << 4) & 0xF0F0F0F0u;  // k 8jj+0..3
+                                    lanes8[b2][c * 8 + 2 * jj + 1] = w[jj] & 0xF0F0F0F0u;     // k 8jj+4..7
+                                }
                             }
+                        }
+                        if (!(p.dbg & 256)) {  // dbg 256 (diag build): no TMEM stores
+                            tmem_st_32x32b_x32(dst + 32 * h, lanes8[0]);
+                            if (h + 1 < nb) tmem_st_32x32b_x32(dst + 32 * h + 32, lanes8[1]);
                         }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&w_empty[s]);
-                mbar_wait(&a_empty[as], ((U / kAStages) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t dst = tmem + (static_cast<uint32_t>(32 * q) << 16) + kAColBase + as * kAStageCols;
-                tmem_st_32x32b_x32(dst, lanes8[0]);
-                if (nb > 1) tmem_st_32x32b_x32(dst + 32, lanes8[1]);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[as]);
-                if (utr && r == 0 && U < 64) utr[8 * U + 5] = globaltimer();
+                if (utr && lane == 0 && U < 64) utr[8 * U + (q == 0 ? 5 : (q == 1 ? 2 : (q == 2 ? 3 : 7)))] = globaltimer();
             }
         }
     } else if (warp >= kDynEpi0) {
@@ -1675,32 +1701,32 @@ __global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __
         quant_row<false>(b, i, t, red);
 }
 
-template <int BN, bool DEP>
+template <int BN, bool DEP, int UB>
 cudaError_t ensure_dyn_attr() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel<BN, DEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   DynCfg<BN, DEP>::kSmem);
+        err = cudaFuncSetAttribute(w4a8_decode_dyn_kernel<BN, DEP, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   DynCfg<BN, DEP, UB>::kSmem);
     });
     return err;
 }
 
-template <int BN, bool DEP>
+template <int BN, bool DEP, int UB>
 cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st) {
-    const cudaError_t ed = ensure_dyn_attr<BN, DEP>();
+    const cudaError_t ed = ensure_dyn_attr<BN, DEP, UB>();
     if (ed != cudaSuccess) return ed;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.C);
     cfg.blockDim = dim3(kDynThreads);
-    cfg.dynamicSmemBytes = DynCfg<BN, DEP>::kSmem;
+    cfg.dynamicSmemBytes = DynCfg<BN, DEP, UB>::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN, DEP>, p);
+    return cudaLaunchKernelEx(&cfg, w4a8_decode_dyn_kernel<BN, DEP, UB>, p);
 }
 
 int dyn_bn(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
@@ -2140,9 +2166,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) p.lin[l].off %= p.C;
         if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
         switch (bn) {
-            case 16: return launch_dyn<16, true>(p, prog_pdl, st);
-            case 32: return launch_dyn<32, true>(p, prog_pdl, st);
-            default: return launch_dyn<64, true>(p, prog_pdl, st);
+            case 16: return launch_dyn<16, true, 2>(p, prog_pdl, st);
+            case 32: return launch_dyn<32, true, 2>(p, prog_pdl, st);
+            default: return launch_dyn<64, true, 2>(p, prog_pdl, st);
         }
     }
     if (dyn) {
@@ -2180,9 +2206,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         int mmax = 1;
         for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
         switch (dyn_bn(mmax)) {
-            case 16: return launch_dyn<16, false>(p, prog_pdl, st);
-            case 32: return launch_dyn<32, false>(p, prog_pdl, st);
-            default: return launch_dyn<64, false>(p, prog_pdl, st);
+            case 16: return (L == 1 ? launch_dyn<16, false, 4>(p, prog_pdl, st) : launch_dyn<16, false, 2>(p, prog_pdl, st));
+            case 32: return (L == 1 ? launch_dyn<32, false, 4>(p, prog_pdl, st) : launch_dyn<32, false, 2>(p, prog_pdl, st));
+            default: return (L == 1 ? launch_dyn<64, false, 4>(p, prog_pdl, st) : launch_dyn<64, false, 2>(p, prog_pdl, st));
         }
     }
     cudaLaunchConfig_t cfg = {};
@@ -2260,9 +2286,9 @@ cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& g, void* scratch, size_t s
     p.pdl = g.pdl ? 1 : 0;
     p.trace = g.trace;
     switch (dyn_bn(g.M)) {
-        case 16: return launch_dyn<16, false>(p, g.pdl, st);
-        case 32: return launch_dyn<32, false>(p, g.pdl, st);
-        default: return launch_dyn<64, false>(p, g.pdl, st);
+        case 16: return launch_dyn<16, false, 4>(p, g.pdl, st);
+        case 32: return launch_dyn<32, false, 4>(p, g.pdl, st);
+        default: return launch_dyn<64, false, 4>(p, g.pdl, st);
     }
 }
 

@@ -65,6 +65,21 @@ def main(m=16, single=None):
     for i, (name, _, _) in enumerate(LAYERS):
         print(f"  {name:8s} first MMA {stat(10 + 4 * i)}  dep released {stat(12 + 4 * i)}  last epilogue {stat(11 + 4 * i)}")
         print(f"  {'':8s} x quantized {stat(13 + 4 * i)}  producer saw qdone {stat(26 + i)}")
+    if not single:
+        tt = buf[:148 * 32].view(148, 32).cpu().numpy()
+        for i, (name, _, k) in enumerate(LAYERS):
+            if i == 0:
+                continue
+            kb = (k + 127) // 128
+            q = (tt[:, 13 + 4 * i] - base) / 1e3
+            r = (tt[:, 12 + 4 * i] - base) / 1e3
+            quant = np.arange(148) < kb
+            d = q - r
+            order = np.argsort(-d)
+            print(f"  {name}: quantizing CTAs {quant.sum()}: release->quantized us median {np.median(d[quant]):.2f} "
+                  f"max {d[quant].max():.2f}; slowest CTAs " +
+                  ", ".join(f"{c}({d[c]:.2f})" for c in order[:5]) +
+                  f"; non-quantizing max {d[~quant].max() if (~quant).any() else 0:.2f}")
     et = buf[148 * 32 + 512:].view(32, 16).cpu().numpy()[:, :11]
     print("last CTA, per item epilogue (us): d_full, tmem ld, scales, atom, reduced, stored, amax, done, after-bar")
     for j2 in range(32):
@@ -79,7 +94,7 @@ def main(m=16, single=None):
         row = ut[u]
         if row.max() == 0:
             continue
-        print("  %3d " % u + " ".join("%7.2f" % ((v - base) / 1e3) if v > 0 else "      -" for v in row[:7]))
+        print("  %3d " % u + " ".join("%7.2f" % ((v - base) / 1e3) if v > 0 else "      -" for v in row[:8]))
     print("  last x issue: %.2f" % ((ut[63, 7] - base) / 1e3 if ut[63, 7] > 0 else -1))
 
 
