@@ -104,3 +104,21 @@ def test_gpu_entry_points_fail_loudly_without_device(L):
     with pytest.raises(OdyError) as e:
         quantize_activations_per_token(Tensor(np.ones((2, 8), np.float32)))
     assert e.value.status == _lib.ODY_EDEVICE
+
+
+def test_tensor_create_large_copy_and_finite_check():
+    """ody_tensor_create (ref tensor.cpp:21-27 + capi.cpp:149): a multi-MB tensor is
+    copied exactly (fused copy + finite scan), and a NaN/Inf anywhere -- first, middle,
+    last element -- is rejected with EINVAL."""
+    import numpy as np
+
+    from paper_2311_09550_b200 import api
+    from paper_2311_09550_b200._lib import OdyError
+    x = np.random.default_rng(0).standard_normal((1024, 1000), dtype=np.float32)
+    assert np.array_equal(api.Tensor(x).numpy(), x)
+    for pos, bad in ((0, np.inf), (512_000, np.nan), (1_023_999, -np.inf)):
+        y = x.copy().reshape(-1)
+        y[pos] = bad
+        with pytest.raises(OdyError) as e:
+            api.Tensor(y.reshape(1024, 1000))
+        assert e.value.status == 1
