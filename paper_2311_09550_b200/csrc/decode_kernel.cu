@@ -871,8 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) w4a8_decode_kernel(const __grid_c
 #pragma unroll
                         for (int t = 0; t < kBN; ++t) {
                             if (t < d.M) {
-                                if (p.dbg & 16) continue;  // diagnostics (ODY_DBG_DECODE, diag build only)
-                    const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                                const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
                                 const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa[t], sw_n));
                                 const size_t idx = static_cast<size_t>(t) * d.N + n;
                                 if (d.out_dtype == kDtypeF32)
@@ -1204,7 +1203,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 // its producer linear completes.  While it has not, keep HBM streaming: pull
                 // this whole item's weights into L2 (the ring then refills from L2).
                 const bool depi = d.qdone != nullptr;
-                if (depi && lane == 0 && !(p.dbg & 64) && ld_acquire_u32(d.qdone) < d.qtarget)
+                if (depi && lane == 0 && ld_acquire_u32(d.qdone) < d.qtarget)
                     bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
                                      static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
@@ -1291,7 +1290,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         if (c < 4 * nb && !((p.dbg & 128) && (kb > x.kb_lo || c > 0)))  // dbg 128: first MMA only
                             mma_i8_ts(d_tmem, a_tmem + 8 * c, b_desc(b0 + (c / 4) * kBBlockBytes + 32 * (c % 4)),
                                       C::kIdesc, (kb > x.kb_lo || c > 0) ? 1u : 0u);
-                    if (!(p.dbg & 1024)) mma_commit(&a_empty[as]);  // dbg 1024 (diag, unsafe): no A-stage handshake
+                    mma_commit(&a_empty[as]);
                     mma_commit(&w_empty[s]);
                     if (kb + nb >= x.kb_hi) mma_commit(&d_full[db]);
                 }
@@ -1386,7 +1385,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 mbar_wait(&w_full[s], (U / kDynStages) & 1);
                 if (utr && r == 0 && U < 64) utr[8 * U + 4] = globaltimer();
                 const uint32_t src = smem_u32(ring) + s * kStageBytes + r * 16;
-                if (!(p.dbg & 1024)) mbar_wait(&a_empty[as], ((U / C::kAStages) & 1) ^ 1);
+                mbar_wait(&a_empty[as], ((U / C::kAStages) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t dst = tmem + (static_cast<uint32_t>(32 * q) << 16) + C::kAColBase + as * C::kAStageColsD;
                 // two k-blocks at a time (64 words in registers), each straight to TMEM
@@ -1546,7 +1545,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             int32_t* const accp = ld_keep_ptr(d.acc_out);
             float* const sa_outp = (depi && x.nt == 0 && r == 0) ? ld_keep_ptr(d.sa_out) : nullptr;
             const bool amx_on = d.amax_dst != nullptr;
-            const bool own = fin && n < n_cols && !(p.dbg & 16);  // dbg 16 (diag build): no stores
+            const bool own = fin && n < n_cols;
             const bool amx = amx_on && n >= d.amax_c0 && n < d.amax_c1;
             float sat[16];  // the token scales of 16 tokens at a time, loaded ahead of the stores
 #pragma unroll
