@@ -6,9 +6,10 @@ DEPENDENT chain a real layer executes (not four independent linears):
     x[M,5120] -> qkv (15360x5120) -> o (5120x5120) on qkv[:, :5120]   (attention stand-in)
               -> gate_up (27648x5120) -> down (5120x13824) on gate_up[:, :13824] (SiLU stand-in)
 Each linear quantizes its input per token (K1), runs the W4A8 FastGEMM (K3) and the
-dequantizing epilogue (K4), fp16 in / fp16 out.  At N = 1 the step is ONE linear program
-(the batched act-quant kernel + one persistent w4a8_decode_dyn_kernel launch: each
-dependent linear's input is quantized in-kernel once its producer finished).  At N > 1
+dequantizing epilogue (K4), fp16 in / fp16 out.  At N = 1 the step is FOUR dependent
+launches in stream order (per linear: the batched act-quant kernel + a one-linear program
+on the persistent w4a8_decode_dyn_kernel, PDL between them) -- measured faster than the
+same layer as one chain program, which is reported beside it (roofline.chain_program).  At N > 1
 the same layer runs Megatron-TP over N GPUs through ody_tp_linear (column qkv/gate_up,
 row o/down with the MAX + exact int32 SUM NCCL all-reduces), one CUDA graph per step;
 strong scaling (the layer is fixed, its shards shrink).
@@ -241,6 +242,33 @@ class ChainLayer:
         return self.y
 
 
+class SeqLayer:
+    """One decoder layer's linears as FOUR dependent launches in stream order (each: the
+    batched act quant of its input + a one-linear program on the dynamic kernel, PDL
+    between launches): qkv -> o(qkv[:, :5120]) -> gate_up -> down(gate_up[:, :13824]),
+    the slices read in place.  The headline step at N = 1: measured faster than the
+    one-launch chain program (tools/layer_launch_ab.py).  Shares one
+    workspace across its programs (stream-ordered)."""
+
+    def __init__(self, dev, ws, x, workspace=None):
+        import torch
+        m = x.shape[0]
+        self.outs = [torch.empty((m, w.n), dtype=torch.float16, device=x.device) for w in ws]
+        o, d = ws[1], ws[3]
+        ins = [x, self.outs[0][:, :o.k], self.outs[1], self.outs[2][:, :d.k]]
+        self.progs = []
+        for i, w, y in zip(ins, ws, self.outs):
+            self.progs.append(dev.Program([dev.LinearCall(i, w, y)], workspace=workspace))
+            workspace = self.progs[-1].workspace
+        self.workspace = workspace
+        self.y = self.outs[3]
+
+    def run(self, pdl=True, stream=None):
+        for p in self.progs:
+            p.run(pdl=pdl, stream=stream)
+        return self.y
+
+
 class TPLayer:
     """The same layer under Megatron TP over an ody_comm (ody_tp_linear per shard)."""
 
@@ -271,10 +299,10 @@ def headline(args, dev, world, rank, comm, stream):
         ws_shared = None
         layers = []
         for c in range(args.copies):
-            layers.append(ChainLayer(dev, copies[c], x, workspace=ws_shared))
-            ws_shared = layers[-1].prog.workspace
+            layers.append(SeqLayer(dev, copies[c], x, workspace=ws_shared))
+            ws_shared = layers[-1].workspace
         step = lambda c: layers[c].run(pdl=True, stream=stream)  # noqa: E731
-        launches = 2
+        launches = 8  # 4 x (batched act quant + one-linear decode program)
         local_b = step_bytes(m)
     else:
         copies = None
@@ -325,26 +353,32 @@ def headline(args, dev, world, rank, comm, stream):
 
 
 def roofline(args, dev, h, stream):
-    """Dominant kernel at N = 1: the chain program launch (act_quant_rows_kernel +
-    w4a8_decode_dyn_kernel<16>), timed alone over graph replays of the weight copies back
-    to back (no PDL: each launch starts on an idle GPU); achieved = the layer's
-    algorithmic bytes / that launch time.  Also the same four linears as INDEPENDENT
-    inputs in one launch, and each linear alone (one ody_dev_w4a8_linear each)."""
+    """Dominant kernel at N = 1: the one-linear decode program (act_quant_rows_kernel +
+    w4a8_decode_dyn_kernel<16, 0, 4>), four dependent launches per step, timed alone over
+    graph replays of the weight copies back to back (no PDL: each launch starts on an
+    idle GPU); achieved = the layer's algorithmic bytes / the step's launch time.  Also:
+    the same dependent layer as ONE chain program, the four linears as INDEPENDENT inputs
+    in one launch, and each linear alone."""
     import torch
     hbm, kind = peaks()
     m = args.m
     layers = h["layers"]
 
-    def chain():
+    def seq():
         for l in layers:
             l.run(pdl=False, stream=stream)
 
-    ms = _graph_time(chain, stream, reps=50) / len(layers)
+    ms = _graph_time(seq, stream, reps=50) / len(layers)
     achieved = step_bytes(m) / (ms * 1e-3) / 1e9
     xs = {k: (torch.randn((m, k), device="cuda") * 2).half() for k in (HIDDEN, INTER)}
     ind = [dev.Program([dev.LinearCall(xs[w.k], w, torch.empty((m, w.n), dtype=torch.float16, device="cuda"))
                         for w in cw]) for cw in h["copies"]]
     ms_ind = _graph_time(lambda: [p.run(pdl=True, stream=stream) for p in ind], stream, reps=50) / len(ind)
+    del ind
+    chains = [ChainLayer(dev, cw, h["x"]) for cw in h["copies"]]
+    ms_chain = _graph_time(lambda: [c.run(pdl=True, stream=stream) for c in chains], stream, reps=50) / len(chains)
+    del chains
+    torch.cuda.empty_cache()
     per = {}
     wsl = dev.Workspace.get_linear(m, 27648, 13824, "cuda")
     for li, (name, n, k) in enumerate(LAYERS):
@@ -361,13 +395,19 @@ def roofline(args, dev, h, stream):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(f"chain_M{m}")
+                traffic = json.load(f).get(f"seq_M{m}")
         except Exception:
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": kind,
-            "kernel": "act_quant_rows_kernel + w4a8_decode_dyn_kernel<16> (the layer chain: ONE program launch)",
+            "kernel": "act_quant_rows_kernel + w4a8_decode_dyn_kernel<16, 0, 4> per linear (4 dependent launches "
+                      "per step; bytes and time per step)",
             "launch_us": round(ms * 1e3, 3), "algorithmic_bytes_per_launch": step_bytes(m),
+            "chain_program": {"us": round(ms_chain * 1e3, 3),
+                              "GB/s": round(step_bytes(m) / (ms_chain * 1e-3) / 1e9, 1),
+                              "frac": round(step_bytes(m) / (ms_chain * 1e-3) / 1e9 / hbm, 4),
+                              "note": "the same dependent layer as ONE program launch (in-kernel grid-wide "
+                                      "quantization of each dependent x), PDL"},
             "independent_linears_program": {"us": round(ms_ind * 1e3, 3),
                                             "GB/s": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9, 1),
                                             "frac": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9 / hbm, 4),
@@ -457,17 +497,17 @@ def engines_ablation(args, stream):
 
 
 def decode_sweep(args, dev, h, stream):
-    """configs[1] sweep: the chain step at M = 1..64 (one program launch per step)."""
+    """configs[1] sweep: the headline step (the dependent layer, 4 launches) at M = 1..64."""
     import torch
     hbm, _ = peaks()
     res = {}
     for m in (1, 2, 4, 8, 16, 32, 64):
         x = (torch.randn((m, HIDDEN), device="cuda") * 2).half()
-        ls = [ChainLayer(dev, cw, x) for cw in h["copies"]]
+        ls = [SeqLayer(dev, cw, x) for cw in h["copies"]]
         ms = _graph_time(lambda ls=ls: [l.run(pdl=True, stream=stream) for l in ls], stream, reps=20) / len(ls)
         gbs = step_bytes(m) / (ms * 1e-3) / 1e9
         res[f"M{m}"] = {"us_per_step": round(ms * 1e3, 2), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 3),
-                        "fused": ls[0].prog.fused}
+                        "fused": all(p.fused for p in ls[0].progs)}
         del ls
     return res
 
@@ -512,7 +552,7 @@ def prefill_roofline(args, dev, h, stream, m=1024):
 def tp70b(args, dev, world, comm, stream):
     """configs[3]: LLaMA-2-70B decoder-layer linears (hidden 8192, inter 28672, GQA kv
     1024) at TP = N: column qkv/gate_up, row o/down (MAX + int32 SUM all-reduces).  At
-    N = 1 the unsharded layer runs as one chain program.  Decode M in {1, 16, 64} (2
+    N = 1 the unsharded layer runs as the headline step (4 dependent launches).  Decode M in {1, 16, 64} (2
     rotating weight copies, 856 MB); prefill M = 1024 once."""
     import torch
     hbm, _ = peaks()
@@ -527,7 +567,7 @@ def tp70b(args, dev, world, comm, stream):
         x = (torch.randn((m, H70), device="cuda", generator=torch.Generator(device="cuda").manual_seed(m)) *
              2).half()
         if comm is None:
-            ls = [ChainLayer(dev, cw, x) for cw in cws]
+            ls = [SeqLayer(dev, cw, x) for cw in cws]
             fn = lambda ls=ls: [l.run(pdl=True, stream=stream) for l in ls]  # noqa: E731
             local = step_bytes(m, LAYERS70)
         else:
@@ -540,15 +580,15 @@ def tp70b(args, dev, world, comm, stream):
                         "TOPS": round(ops / (ms * 1e-3) / 1e12, 1),
                         "per_rank_frac_hbm": round(local / (ms * 1e-3) / 1e9 / hbm, 3)}
     return {"tp": world, "dims": {nm: [n, k] for nm, n, k in LAYERS70},
-            "path": "one chain program" if comm is None else "ody_tp_linear x4 (NCCL), one CUDA graph per layer",
+            "path": "4 dependent one-linear launches" if comm is None else "ody_tp_linear x4 (NCCL), one CUDA graph per layer",
             "per_M": res}
 
 
 def stack13b(args, dev, world, comm, stream, n_layers=40, prompt=1024, gen=128):
     """configs[4]: 40 LLaMA-13B layers' linear stacks: a 1024-token prefill, then 128
     decode steps at batch args.stack_m (default 1), each decode step = ONE CUDA graph of
-    the 40 layer chains (N = 1: 40 program launches + 40 batched act quants, PDL-chained;
-    N > 1: ody_tp_linear shards).  The layer output feeds the next layer; the last
+    the 40 layers (N = 1: 160 one-linear decode programs + their batched act quants, the
+    headline step's launch form, PDL-chained; N > 1: ody_tp_linear shards).  The layer output feeds the next layer; the last
     layer's output feeds the next step (synthetic stand-in for the LM head + sampling)."""
     import torch
     hbm, _ = peaks()
@@ -566,8 +606,8 @@ def stack13b(args, dev, world, comm, stream, n_layers=40, prompt=1024, gen=128):
         if comm is None:
             chain, x, wsp = [], x0, None
             for L in range(n_layers):
-                chain.append(ChainLayer(dev, ws[L], x, workspace=wsp))
-                wsp = chain[-1].prog.workspace
+                chain.append(SeqLayer(dev, ws[L], x, workspace=wsp))
+                wsp = chain[-1].workspace
                 x = chain[-1].y
             def run():
                 for c in chain:
@@ -714,6 +754,7 @@ def run_b200(args):
         "config": {"workload": "llama13b_decoder_layer_linear_chain_decode", "M": m,
                    "layers": {nm: [n, k] for nm, n, k in LAYERS}, "hidden": HIDDEN, "intermediate": INTER,
                    "chain": "qkv -> o(qkv[:, :5120]) -> gate_up -> down(gate_up[:, :13824])",
+                   "step": "4 dependent launches (act quant + one-linear decode program each), PDL",
                    "parallelism": f"tp{world}" if (world > 1 or comm is not None) else "single",
                    "weight_bytes_per_step": sum(n * k // 2 for _, n, k in LAYERS),
                    "l2": "inputs larger than L2 (158.6 MB weights/step, 4 rotating copies)",

@@ -135,6 +135,8 @@ struct PParams {
     int32_t* part;        // dynamic schedule: [items][BN][128] split partials (scratch)
     int n_items;          // dynamic schedule: work items of the whole program
     uint32_t* work;       // dynamic schedule: next-item counter (zeroed; reset by the last CTA)
+    int reset_at_exit;    // the last CTA out re-arms the work counter / chain state (else
+                          // nothing to re-arm: static deal, no chain state)
     int chain_static;     // dependency chain: items dealt round-robin over the CTAs in program
                           // order (CTA c: items c - off, + C, ... of each linear), no counter
     uint32_t* tile_cnt;   // [program tiles] split arrivals (zeroed)
@@ -1613,8 +1615,10 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     __syncthreads();
     tc_fence_after();
     if (warp == kWarpAlloc) tmem_dealloc(tmem, kTmemCols);
-    if (threadIdx.x == 0) {
-        // the last CTA out re-arms the item counter for the next launch
+    if (threadIdx.x == 0 && p.reset_at_exit) {
+        // the last CTA out re-arms the item counter for the next launch (a lone linear is
+        // dealt statically and skips this: the exit atomic is an L2 round trip every CTA
+        // pays before the grid can complete)
         __threadfence();
         if (atomicAdd(p.ctr + kMaxLin, 1u) == gridDim.x - 1) {
             *p.work = 0u;
@@ -1627,8 +1631,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             __threadfence();
         }
-        if (trc) trc[5] = globaltimer();
     }
+    if (trc && threadIdx.x == 0) trc[5] = globaltimer();
 }
 
 // K1 for the external activations of a program: one 128-thread CTA per token row,
@@ -2162,6 +2166,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         p.C = std::min(sms, ib);
         static const char* st_env = ODY_DIAG_ENV("ODY_CHAIN_DYNAMIC");  // diagnostics: 1 = counter
         p.chain_static = (st_env && st_env[0] == '1') ? 0 : 1;
+        p.reset_at_exit = 1;  // done / qdone / row maxima (and the counter when dynamic)
         for (int l = 0; l < L; ++l) p.lin[l].off %= p.C;
         if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
         switch (bn) {
@@ -2197,6 +2202,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) p.lin[l] = sorted[l];
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
+        // a lone linear: static deal (items <= ~2 per CTA, balanced), nothing to re-arm
+        p.chain_static = L == 1 ? 1 : 0;
+        p.reset_at_exit = L == 1 ? 0 : 1;
         static const char* pfi_env = ODY_DIAG_ENV("ODY_DYN_PF_ITEMS");  // second-round items to L2
         p.pf_units = pfi_env ? std::atoi(pfi_env) : 0;  // measured: guessing next items costs more
         p.S = 1;
@@ -2282,6 +2290,8 @@ cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& g, void* scratch, size_t s
     p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
     p.S = 1;
     p.C = std::min(sms, p.n_items);
+    p.chain_static = 1;  // static deal of the lone linear's items: no counter to re-arm
+    p.reset_at_exit = 0;
     p.pdl = g.pdl ? 1 : 0;
     p.trace = g.trace;
     switch (dyn_bn(g.M)) {

@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_2311_09550_b200 import device as dev  # noqa: E402
 
-m = 16
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 stream = torch.cuda.Stream()
 copies = [[dev.W4Weight.quantize(bench._weights_f32(n, k, 1000 * c + i)) for i, (_, n, k) in
            enumerate(bench.LAYERS)] for c in range(4)]
