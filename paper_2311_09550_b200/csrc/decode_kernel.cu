@@ -1901,27 +1901,17 @@ static int dyn_split(int kblocks) {
     static const int target = env ? std::max(1, std::atoi(env)) : 56;
     return std::max(1, (kblocks + target - 1) / target);
 }
-// Dependency chain: every linear runs alone between two grid-wide completions, so its
-// split is chosen for that linear's own critical path: items per CTA (waves w) x
-// max(mainloop, epilogue) + the last epilogue, with a measured ~0.15 us per k-block of
-// mainloop and ~1 us (whole-K item: the completion release) / ~2.5 us (split item: plus
-// the partial-sum round trips) of epilogue latency per item (tools/chain_trace.py).
+// A linear that runs alone (a lone launch, or a chain link between two grid-wide
+// completions) is split along K only as far as ONE wave of items allows: s = floor(CTAs /
+// tiles), at least 1, and items of >= 4 k-blocks.  Measured per forced split
+// (tools/single_linear_ab.py, M = 16, us): 4096^2 12.7 / 11.3 / 11.1 / 10.8 (s = 4 = 148/32)
+// / 15.1; o 14.4 / 13.0 / 12.0 (s = 3) / 16.1; qkv and gate_up best unsplit (15.6, 23.0;
+// 17.7, 26.5 at s = 2); down 27.8 / 21.9 / 19.1 (s = 3) / 22.8 -- a second item per CTA
+// costs more (its pipeline ramp and epilogue round trips) than the balance it buys.
 static int chain_split(int n_tiles, int kblocks, int sms) {
     static const char* env = ODY_DIAG_ENV("ODY_CHAIN_SPLIT");  // diagnostics: fixed split
     if (env) return std::max(1, std::min(std::atoi(env), kblocks));
-    int best = 1;
-    double best_t = 1e30;
-    for (int sp = 1; sp <= 8 && sp <= kblocks; ++sp) {
-        const int waves = (n_tiles * sp + sms - 1) / sms;
-        const double ml = 0.15 * ((kblocks + sp - 1) / sp);
-        const double ep = sp > 1 ? 2.5 : 1.0;
-        const double t = waves * std::max(ml, ep) + ep;
-        if (t < best_t - 1e-9) {
-            best_t = t;
-            best = sp;
-        }
-    }
-    return best;
+    return std::max(1, std::min({sms / std::max(n_tiles, 1), kblocks / 4, 8}));
 }
 static size_t dyn_items(const LinearArgs* a, int L) {
     // upper bound over the tail refinement (any linear may be the tail one, <= 12-block
