@@ -1257,6 +1257,17 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     ns = ns < 1024 ? 2 * ns : 1024;
                 }
             }
+            if (p.next_bytes > 0 && lane == 0) {
+                // every own load is issued: stream this CTA's share of the NEXT launch's
+                // weights (the caller's hint, e.g. the next linear of the layer) into L2,
+                // so its ramp reads L2 and the HBM keeps streaming through this kernel's
+                // drain, epilogues and the act quant in between
+                const size_t share = (p.next_bytes / gridDim.x + 16383) & ~static_cast<size_t>(16383);
+                const size_t lo = share * blockIdx.x;
+                const size_t hi = min(p.next_bytes, lo + share);
+                for (size_t off = lo; off < hi; off += 16384)
+                    bulk_prefetch_l2(p.next_wp + off, static_cast<uint32_t>(min(static_cast<size_t>(16384), hi - off)));
+            }
             if (trc && lane == 0) trc[6] = globaltimer();
         }
     } else if (warp == kWarpMma) {
