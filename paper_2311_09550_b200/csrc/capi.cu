@@ -294,7 +294,7 @@ void run_gemm(const ody_qtensor* a_q, const ody_qtensor* w_q, float* out_dev, in
     Runtime& r = rt();
     const int M = static_cast<int>(a_q->rows), N = static_cast<int>(w_q->rows), K = static_cast<int>(w_q->cols);
     if (gemm_prequant_eligible(M, N, K)) {  // decode widths: the dynamic decode kernel
-        const size_t need = gemm_prequant_scratch_bytes(M, N, K);
+        const size_t need = gemm_prequant_scratch_bytes(M, N, K, r.sms);
         if (r.pscratch_bytes < need) {
             if (r.pscratch) cuda_check(cudaFreeAsync(r.pscratch, st), "cudaFreeAsync");
             r.pscratch = nullptr;

@@ -110,7 +110,9 @@ struct LinDesc {
     int signal;           // a later linear depends on this one: publish its completion
     int rot;              // tile rotation (independent linears spread over the clusters)
     // dynamic schedule (w4a8_decode_dyn_kernel): work items = (tile, k-split) pairs
-    int split;            // k-splits per tile
+    int split;            // k-splits per tile (tiles [0, t1))
+    int t1, split2;       // tiles [t1, n_tiles): the last partial wave, split2 k-splits each
+    int items;            // work items of this linear: t1 * split + (n_tiles - t1) * split2
     int off;              // static chain schedule: CTA of this linear's item 0
     int ibase;            // first work item of this linear
     int tbase;            // first tile of this linear in the program's tile numbering
@@ -124,6 +126,18 @@ struct LinDesc {
     const uint32_t* amax_src;  // dependent linear: per-token max |x| (its producer's amax_dst)
     uint32_t* qdone;      // dependent linear: k-blocks of x quantized into qa (grid-wide), or NULL
     uint32_t qtarget;     //   complete at kblocks
+};
+
+constexpr int kRowThreads = 128;
+constexpr int kRowChunks = 7;  // K <= 128 * 7 * 16 = 14336
+struct RowBatch {
+    const unsigned short* x[kMaxLin];
+    size_t ldx[kMaxLin];
+    int M[kMaxLin], K[kMaxLin], Mp[kMaxLin], bf16[kMaxLin];
+    int8_t* q[kMaxLin];
+    float* s[kMaxLin];
+    const float* amax_in[kMaxLin];  // optional row max override (row-parallel TP: all-reduced max)
+    int n, pdl;
 };
 
 struct PParams {
@@ -160,6 +174,14 @@ __device__ __forceinline__ void stg_b16(void* p, unsigned short v) {
 }
 __device__ __forceinline__ void stg_b32(void* p, uint32_t v) {
     asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// The same stores with no compiler memory barrier (the epilogue's independent per-token
+// stores may interleave with the next token's arithmetic).
+__device__ __forceinline__ void stg_b16_free(void* p, unsigned short v) {
+    asm("st.global.b16 [%0], %1;" ::"l"(p), "h"(v));
+}
+__device__ __forceinline__ void stg_b32_free(void* p, uint32_t v) {
+    asm("st.global.b32 [%0], %1;" ::"l"(p), "r"(v));
 }
 template <typename T>
 __device__ __forceinline__ T* ld_keep_ptr(T* v) {
@@ -966,8 +988,118 @@ struct DynCfg {
 };
 
 
+// One item's outputs from thread r's accumulators (output column n, BN tokens), specialised
+// per output format so the token loop is straight-line and the tokens' conversions and
+// stores overlap: with the format switched at run time inside the loop every token cost
+// ~5 branches and a serial convert->store chain (measured ~0.1 us per token, 1.6 us per
+// 16-token item on the critical path of every linear).  ODT -1: int32 pre-shift
+// accumulators (acc_out).  AMX: also reduce max |stored value| per token into the CTA's
+// smem maxima (the dependent linear's x scale).
+template <bool BF16>
+__device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float* red) {
+    const unsigned short* row = b.x[i] + static_cast<size_t>(t) * b.ldx[i];
+    const int K = b.K[i];
+    const int nch = static_cast<int>(pad_k(K) / 16);
+    uint4 raw[kRowChunks][2];
+    uint32_t mb = 0u;
+#pragma unroll
+    for (int j = 0; j < kRowChunks; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c < nch) {
+            load16_raw(row, c * 16, K, false, raw[j][0], raw[j][1]);
+            mb = max(mb, absmax16_bits<BF16>(raw[j][0], raw[j][1]));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if ((threadIdx.x & 31) == 0) reinterpret_cast<uint32_t*>(red)[threadIdx.x >> 5] = mb;
+    __syncthreads();
+    uint32_t m = 0u;
+#pragma unroll
+    for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
+    if (b.amax_in[i]) m = __float_as_uint(b.amax_in[i][t]);  // the global max of a K-sharded row
+    float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
+    if (!(sc > 0.0f)) sc = kMinScale;
+    const float rcp = 1.0f / sc;
+    if (threadIdx.x == 0) b.s[i][t] = sc;
+#pragma unroll
+    for (int j = 0; j < kRowChunks; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c < nch) {
+            const uint4 qv = quant16<BF16>(raw[j][0], raw[j][1], sc, rcp, 0);
+            *reinterpret_cast<uint4*>(b.q[i] + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, b.Mp[i])) = qv;
+        }
+    }
+}
+
+__device__ __forceinline__ void act_quant_rows_body(const RowBatch& b) {
+    if (b.pdl) {
+        pdl_launch_dependents();
+        pdl_wait();
+    }
+    __shared__ float red[kRowThreads / 32];
+    int i = 0, t = blockIdx.x;
+    while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
+    if (b.bf16[i])
+        quant_row<true>(b, i, t, red);
+    else
+        quant_row<false>(b, i, t, red);
+}
+
+
+__global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __grid_constant__ RowBatch b) {
+    act_quant_rows_body(b);
+}
+
+template <int BN, int ODT, bool AMX>
+__device__ __forceinline__ void epi_store(const uint32_t (&v)[BN], const float* tsc, float sw_n, int m_rows,
+                                          int n_cols, int n, bool own, bool amx, void* outv, uint32_t emax_a,
+                                          int lane) {
+#pragma unroll
+    for (int t0 = 0; t0 < BN; t0 += 16) {
+        float sat[16];  // the token scales of 16 tokens at a time, loaded ahead of the stores
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 s4 = lds128(smem_u32(tsc + t0 + 4 * q4));
+            sat[4 * q4] = __uint_as_float(s4.x);
+            sat[4 * q4 + 1] = __uint_as_float(s4.y);
+            sat[4 * q4 + 2] = __uint_as_float(s4.z);
+            sat[4 * q4 + 3] = __uint_as_float(s4.w);
+        }
+#pragma unroll
+        for (int tt = 0; tt < 16; ++tt) {
+            const int t = t0 + tt;
+            if (t >= m_rows) break;  // warp-uniform
+            const size_t idx = static_cast<size_t>(t) * n_cols + n;
+            if constexpr (ODT < 0) {
+                if (own) stg_b32_free(static_cast<uint32_t*>(outv) + idx, v[t]);  // pre-shift (TP all-reduce)
+            } else {
+                const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
+                const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sat[tt], sw_n));
+                uint32_t mag = 0u;  // |stored value| as f32 bits (the dependent linear's x)
+                if constexpr (ODT == kDtypeF32) {
+                    if (own) stg_b32_free(static_cast<float*>(outv) + idx, __float_as_uint(y));
+                } else if constexpr (ODT == kDtypeF16) {
+                    const __half h = __float2half_rn(y);
+                    if (own) stg_b16_free(static_cast<__half*>(outv) + idx, __half_as_ushort(h));
+                    mag = __float_as_uint(fabsf(__half2float(h)));
+                } else {
+                    const __nv_bfloat16 h = __float2bfloat16_rn(y);
+                    if (own) stg_b16_free(static_cast<__nv_bfloat16*>(outv) + idx, __bfloat16_as_ushort(h));
+                    mag = __float_as_uint(fabsf(__bfloat162float(h)));
+                }
+                if constexpr (AMX) {  // every lane joins the reduction
+                    mag = __reduce_max_sync(0xffffffffu, (own && amx) ? mag : 0u);
+                    if (lane == 0 && mag != 0u) atom_max_shared_u32(emax_a + 4 * t, mag);
+                }
+            }
+        }
+    }
+}
+
 struct DynItem {
     int l, nt, kb_lo, kb_hi, r;
+    int s, i0;  // the tile's k-split count, its split 0's item index within the linear
 };
 __device__ __forceinline__ DynItem dyn_item(const PParams& p, const LinDesc* lin, int it) {
     DynItem x;
@@ -976,10 +1108,21 @@ __device__ __forceinline__ DynItem dyn_item(const PParams& p, const LinDesc* lin
     const LinDesc& d = lin[l];
     const int rel = it - d.ibase;
     x.l = l;
-    x.nt = rel / d.split;
-    x.r = rel - x.nt * d.split;
-    x.kb_lo = x.r * d.kblocks / d.split;
-    x.kb_hi = (x.r + 1) * d.kblocks / d.split;
+    const int head = d.t1 * d.split;
+    if (rel < head) {
+        x.s = d.split;
+        x.nt = rel / x.s;
+        x.r = rel - x.nt * x.s;
+        x.i0 = x.nt * x.s;
+    } else {
+        x.s = d.split2;
+        const int t = (rel - head) / x.s;
+        x.r = rel - head - t * x.s;
+        x.nt = d.t1 + t;
+        x.i0 = head + t * x.s;
+    }
+    x.kb_lo = x.r * d.kblocks / x.s;
+    x.kb_hi = (x.r + 1) * d.kblocks / x.s;
     return x;
 }
 
@@ -1008,6 +1151,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint32_t* emax = tmem_slot + 1;  // [BN] the CTA's per-token max |y| of the current item
     // [2][64] token scales of the item (parity), 16-byte aligned for ld.shared.v4
     float* ssc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(emax + 64) + 15) & ~uintptr_t(15));
+    static_assert((3 * kDynStages + 2 * C::kAStages + 2 * kDBufs + 2 * kItemSlots) * 8 + kItemSlots * 4 + 8 + 64 * 4 +
+                          16 + 128 * 4 <= 2048,
+                  "barrier / item / scale region");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned long long* trc = p.trace ? p.trace + blockIdx.x * kTraceCta : nullptr;
@@ -1050,6 +1196,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
         // Lanes 0 and 1 issue alternate units of each item in SIMT lockstep (halves the
         // per-unit producer overhead); lane 0 fetches the items.
         if (lane < 2) {
+            if (trc && lane == 0) trc[2] = globaltimer();
             const uint64_t pol = l2_policy_evict_first();
             const uint64_t pol_b = l2_policy_evict_last();
             // B tiles come from the act-quant kernel: units issued before griddepcontrol.wait
@@ -1084,6 +1231,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     }
                 pdl_wait();
                 waited = true;
+                if (trc && lane == 0) trc[8] = globaltimer();
                 for (int i = 0; i < ndef; ++i) issue_b(p.lin[dq[i]], dst[i], dkb[i], dnb[i]);
             };
             // DEP: the B tiles of a dependent linear come from its a8 buffer, which the
@@ -1174,7 +1322,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     it = -1;
                     while (cl < p.L) {
                         const LinDesc& dl = p.lin[cl];
-                        const int nl = dl.n_tiles * dl.split;
+                        const int nl = dl.items;
                         const int C = static_cast<int>(gridDim.x);
                         const int i = ci < 0 ? ((static_cast<int>(blockIdx.x) - dl.off) % C + C) % C : ci + C;
                         if (i < nl) {
@@ -1197,10 +1345,12 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     mbar_arrive(&i_full[is]);  // release: the item id is visible to the consumers
                 }
                 if (it < 0) break;
+                if (trc && j == 0 && lane == 0) trc[3] = globaltimer();
                 const DynItem x = dyn_item(p, p.lin, it);
                 const LinDesc& d = p.lin[x.l];
                 const uint8_t* wtile = d.wp + static_cast<size_t>(x.nt) * d.kblocks * kWBlockBytes;
                 const int nunits = (x.kb_hi - x.kb_lo + C::kUB - 1) / C::kUB;
+                if (trc && j == 0 && lane == 0) trc[30] = globaltimer() + (ld_keep(nunits) == -7 ? 1 : 0);
                 // A dependent linear's B tiles are quantized in-kernel by the converters once
                 // its producer linear completes.  While it has not, keep HBM streaming: pull
                 // this whole item's weights into L2 (the ring then refills from L2).
@@ -1209,6 +1359,12 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
                                      static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
+#ifdef ODY_DIAG
+                    // dbg 2048 / 4096: weights streamed before griddepcontrol.wait capped at
+                    // 0 / 2 units (does the ring fill starve the act quant of memory bandwidth?)
+                    if (!waited && (p.dbg & 2048)) release_deferred();
+                    if (!waited && (p.dbg & 4096) && U + k0 >= 2) release_deferred();
+#endif
                     if (!waited && U + k0 + 1 >= kDynStages) release_deferred();
                     const int k = k0 + lane;
                     {
@@ -1225,6 +1381,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         bulk_g2s(ring + s * kStageBytes, wtile + static_cast<size_t>(kb) * kWBlockBytes,
                                  nb * kWBlockBytes, &w_full[s], pol);
                         if (utr && Uk < 64) utr[8 * Uk + 0] = globaltimer();
+                        if (trc && Uk == 0) trc[31] = globaltimer();
                         if (DEP && depi) {
                             if (released(x.l)) {
                                 issue_b(d, s, kb, nb);
@@ -1294,6 +1451,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 if (utr && lane == 0 && U < 64) utr[8 * U + 1] = globaltimer();
                 mbar_wait(&b_full[s], (U / kDynStages) & 1);
                 if (utr && lane == 0 && U < 64) utr[8 * U + 6] = globaltimer();
+                if (trc && lane == 0 && U == 0) trc[9] = globaltimer();  // first B tiles landed
                 tc_fence_after();
                 const uint32_t a_tmem = tmem + C::kAColBase + as * C::kAStageColsD;
                 const uint32_t b0 = smem_u32(ring) + s * kStageBytes + C::kUBytes;
@@ -1504,7 +1662,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             emark(j, 2);
             bool fin = true;
-            if (d.split > 1) {
+            if (x.s > 1) {
                 // Per-ROW last-arriver reduction, no barrier and no waiting: thread r stores
                 // its row's partial into this item's slot, then an acq_rel increment of the
                 // row's counter (release: the store is visible before the count; acquire:
@@ -1518,19 +1676,19 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     if (t < d.M) __stcg(part + t * kTileN + r, static_cast<int32_t>(v[t]));
                 uint32_t* rc = reinterpret_cast<uint32_t*>(p.acc) + static_cast<size_t>(d.tbase + x.nt) * kTileN + r;
                 const uint32_t old = atom_add_acq_rel_u32(rc, 1u);
-                fin = old == static_cast<uint32_t>(d.split - 1);
+                fin = old == static_cast<uint32_t>(x.s - 1);
                 emark(j, 3);
                 if (fin) {
                     // the other splits' rows, kPer splits' loads in flight per round trip
                     constexpr int kPer = BN >= 32 ? 1 : 32 / BN;
-                    const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.nt * d.split) * BN * kTileN;
+                    const int32_t* p0 = p.part + static_cast<size_t>(d.ibase + x.i0) * BN * kTileN;
 #pragma unroll 1
-                    for (int s0 = 0; s0 < d.split; s0 += kPer) {
+                    for (int s0 = 0; s0 < x.s; s0 += kPer) {
                         uint32_t add[kPer][BN];
 #pragma unroll
                         for (int j2 = 0; j2 < kPer; ++j2) {
                             const int s2 = s0 + j2;
-                            const bool use = s2 < d.split && s2 != x.r;
+                            const bool use = s2 < x.s && s2 != x.r;
 #pragma unroll
                             for (int t = 0; t < BN; ++t)
                                 add[j2][t] = (use && t < d.M)
@@ -1557,49 +1715,27 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             uint8_t* const outp = ld_keep_ptr(static_cast<uint8_t*>(d.out));
             int32_t* const accp = ld_keep_ptr(d.acc_out);
             float* const sa_outp = (depi && x.nt == 0 && r == 0) ? ld_keep_ptr(d.sa_out) : nullptr;
+            emark(j, 9);
             const bool amx_on = d.amax_dst != nullptr;
             const bool own = fin && n < n_cols;
             const bool amx = amx_on && n >= d.amax_c0 && n < d.amax_c1;
-            float sat[16];  // the token scales of 16 tokens at a time, loaded ahead of the stores
-#pragma unroll
-            for (int t = 0; t < BN; ++t) {
-                if ((t & 15) == 0) {
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const uint4 s4 = lds128(smem_u32(tsc + t + 4 * q4));
-                        sat[4 * q4] = __uint_as_float(s4.x);
-                        sat[4 * q4 + 1] = __uint_as_float(s4.y);
-                        sat[4 * q4 + 2] = __uint_as_float(s4.z);
-                        sat[4 * q4 + 3] = __uint_as_float(s4.w);
-                    }
-                }
-                if (t < m_rows) {
-                    const size_t idx = static_cast<size_t>(t) * n_cols + n;
-                    if (accp) {
-                        if (own) stg_b32(accp + idx, v[t]);  // pre-shift (TP all-reduce)
-                        continue;
-                    }
-                    const float sa_t = sat[t & 15];
-                    if (sa_outp && own) stg_b32(sa_outp + t, __float_as_uint(sa_t));
-                    const int32_t sh = static_cast<int32_t>(v[t]) >> 4;  // exact (ref gemm.cpp:269)
-                    const float y = __fmul_rn(__int2float_rn(sh), __fmul_rn(sa_t, sw_n));
-                    uint32_t mag = 0u;  // |stored value| as f32 bits (the dependent linear's x)
-                    if (odt == kDtypeF32) {
-                        if (own) stg_b32(outp + 4 * idx, __float_as_uint(y));
-                    } else if (odt == kDtypeF16) {
-                        const __half h = __float2half_rn(y);
-                        if (own) stg_b16(outp + 2 * idx, __half_as_ushort(h));
-                        mag = __float_as_uint(fabsf(__half2float(h)));
-                    } else {
-                        const __nv_bfloat16 h = __float2bfloat16_rn(y);
-                        if (own) stg_b16(outp + 2 * idx, __bfloat16_as_ushort(h));
-                        mag = __float_as_uint(fabsf(__bfloat162float(h)));
-                    }
-                    if (amx_on) {  // warp-uniform: every lane joins the reduction
-                        mag = __reduce_max_sync(0xffffffffu, (own && amx) ? mag : 0u);
-                        if (lane == 0 && mag != 0u) atom_max_shared_u32(smem_u32(emax + t), mag);
-                    }
-                }
+            if (sa_outp && own)
+                for (int t = 0; t < m_rows; ++t) stg_b32(sa_outp + t, __float_as_uint(tsc[t]));
+            const uint32_t emax_a = smem_u32(emax);
+            if (accp) {
+                epi_store<BN, -1, false>(v, tsc, sw_n, m_rows, n_cols, n, own, false, accp, emax_a, lane);
+            } else if (odt == kDtypeF32) {
+                epi_store<BN, kDtypeF32, false>(v, tsc, sw_n, m_rows, n_cols, n, own, false, outp, emax_a, lane);
+            } else if (odt == kDtypeF16) {
+                if (amx_on)
+                    epi_store<BN, kDtypeF16, true>(v, tsc, sw_n, m_rows, n_cols, n, own, amx, outp, emax_a, lane);
+                else
+                    epi_store<BN, kDtypeF16, false>(v, tsc, sw_n, m_rows, n_cols, n, own, false, outp, emax_a, lane);
+            } else {
+                if (amx_on)
+                    epi_store<BN, kDtypeBF16, true>(v, tsc, sw_n, m_rows, n_cols, n, own, amx, outp, emax_a, lane);
+                else
+                    epi_store<BN, kDtypeBF16, false>(v, tsc, sw_n, m_rows, n_cols, n, own, false, outp, emax_a, lane);
             }
             emark(j, 5);
             if (trc && r == 0 && x.l < 4) trc[11 + 4 * x.l] = globaltimer();
@@ -1609,12 +1745,12 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 // atomicMax per token per item, each token on its own 128-byte line (the
                 // whole grid's items hit these few addresses: same-line atomics serialise).
                 named_bar_sync(3, 128);
-                if (d.amax_dst != nullptr && r < d.M) {
+                if (amx_on && r < d.M) {
                     const uint32_t m = emax[r];
                     emax[r] = 0u;
                     if (m != 0u) atomicMax(d.amax_dst + r * kAmaxStride, m);
                 }
-                if (d.amax_dst != nullptr) named_bar_sync(3, 128);
+                if (amx_on) named_bar_sync(3, 128);
                 emark(j, 6);
                 if (r == 0) red_release_add_u32(d.done, 1u);  // cumulative over the CTA barrier
                 emark(j, 7);
@@ -1652,69 +1788,6 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
 // enough (<= 80 registers x 128 threads, no shared arrays beyond 16 B) to stay
 // co-resident with a running decode program CTA, so in the PDL chain program -> K1 ->
 // program the next program's CTAs take every SM the previous one frees.
-constexpr int kRowThreads = 128;
-constexpr int kRowChunks = 7;  // K <= 128 * 7 * 16 = 14336
-struct RowBatch {
-    const unsigned short* x[kMaxLin];
-    size_t ldx[kMaxLin];
-    int M[kMaxLin], K[kMaxLin], Mp[kMaxLin], bf16[kMaxLin];
-    int8_t* q[kMaxLin];
-    float* s[kMaxLin];
-    const float* amax_in[kMaxLin];  // optional row max override (row-parallel TP: all-reduced max)
-    int n, pdl;
-};
-
-template <bool BF16>
-__device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float* red) {
-    const unsigned short* row = b.x[i] + static_cast<size_t>(t) * b.ldx[i];
-    const int K = b.K[i];
-    const int nch = static_cast<int>(pad_k(K) / 16);
-    uint4 raw[kRowChunks][2];
-    uint32_t mb = 0u;
-#pragma unroll
-    for (int j = 0; j < kRowChunks; ++j) {
-        const int c = threadIdx.x + j * kRowThreads;
-        if (c < nch) {
-            load16_raw(row, c * 16, K, false, raw[j][0], raw[j][1]);
-            mb = max(mb, absmax16_bits<BF16>(raw[j][0], raw[j][1]));
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
-    if ((threadIdx.x & 31) == 0) reinterpret_cast<uint32_t*>(red)[threadIdx.x >> 5] = mb;
-    __syncthreads();
-    uint32_t m = 0u;
-#pragma unroll
-    for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
-    if (b.amax_in[i]) m = __float_as_uint(b.amax_in[i][t]);  // the global max of a K-sharded row
-    float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
-    if (!(sc > 0.0f)) sc = kMinScale;
-    const float rcp = 1.0f / sc;
-    if (threadIdx.x == 0) b.s[i][t] = sc;
-#pragma unroll
-    for (int j = 0; j < kRowChunks; ++j) {
-        const int c = threadIdx.x + j * kRowThreads;
-        if (c < nch) {
-            const uint4 qv = quant16<BF16>(raw[j][0], raw[j][1], sc, rcp, 0);
-            *reinterpret_cast<uint4*>(b.q[i] + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, b.Mp[i])) = qv;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __grid_constant__ RowBatch b) {
-    if (b.pdl) {
-        pdl_launch_dependents();
-        pdl_wait();
-    }
-    __shared__ float red[kRowThreads / 32];
-    int i = 0, t = blockIdx.x;
-    while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
-    if (b.bf16[i])
-        quant_row<true>(b, i, t, red);
-    else
-        quant_row<false>(b, i, t, red);
-}
-
 template <int BN, bool DEP, int UB>
 cudaError_t ensure_dyn_attr() {
     static std::once_flag once;
@@ -1726,10 +1799,26 @@ cudaError_t ensure_dyn_attr() {
     return err;
 }
 
+// rb != NULL: first the batched activation quant (rb_rows token rows, act_quant_rows_kernel),
+// then the GEMM, PDL-chained.  (Measured: the same act quant as a mode of this kernel
+// function -- warm instruction caches for the GEMM launch -- made no difference.)
 template <int BN, bool DEP, int UB>
-cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st) {
+cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st, const RowBatch* rb = nullptr, int rb_rows = 0) {
     const cudaError_t ed = ensure_dyn_attr<BN, DEP, UB>();
     if (ed != cudaSuccess) return ed;
+    if (rb) {
+        cudaLaunchConfig_t acfg = {};
+        acfg.gridDim = dim3(rb_rows);
+        acfg.blockDim = dim3(kRowThreads);
+        acfg.stream = st;
+        cudaLaunchAttribute aattr;
+        aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        aattr.val.programmaticStreamSerializationAllowed = 1;
+        acfg.attrs = &aattr;
+        acfg.numAttrs = rb->pdl ? 1 : 0;
+        const cudaError_t ea = cudaLaunchKernelEx(&acfg, act_quant_rows_kernel, *rb);
+        if (ea != cudaSuccess) return ea;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.C);
     cfg.blockDim = dim3(kDynThreads);
@@ -1924,6 +2013,41 @@ static int chain_split(int n_tiles, int kblocks, int sms) {
     if (env) return std::max(1, std::min(std::atoi(env), kblocks));
     return std::max(1, std::min({sms / std::max(n_tiles, 1), kblocks / 4, 8}));
 }
+// Uniform k-split s for every tile of d.
+static int split_uniform(LinDesc& d, int s) {
+    d.split = s;
+    d.t1 = d.n_tiles;
+    d.split2 = 1;
+    d.items = d.n_tiles * s;
+    return d.items;
+}
+// A linear that runs alone, dealt round-robin over `sms` CTAs: chain_split's k-split, and
+// when it leaves a partial last wave of whole tiles (n_tiles > sms, e.g. gate_up's 216
+// tiles on 148 SMs: 68 CTAs stream two whole tiles while 80 stream one) the tiles of that
+// wave are cut into split2 pieces spread over all CTAs -- the busiest CTA streams
+// kb + ceil(R * s2 / sms) * kb / s2 blocks instead of 2 * kb.
+static int split_alone(LinDesc& d, int sms) {
+    const int s = chain_split(d.n_tiles, d.kblocks, sms);
+    split_uniform(d, s);
+    static const char* env = ODY_DIAG_ENV("ODY_TAIL_SPLIT");  // diagnostics: 0 = off, n = forced split2
+    const int forced = env ? std::atoi(env) : -1;
+    if (s != 1 || d.n_tiles <= sms || d.n_tiles % sms == 0 || forced == 0) return d.items;
+    const int R = d.n_tiles % sms;
+    int best = 1;
+    long long best_cost = static_cast<long long>((R + sms - 1) / sms) * d.kblocks;
+    for (int s2 = 2; s2 <= 8 && d.kblocks / s2 >= 4; ++s2) {
+        const long long cost = static_cast<long long>((R * s2 + sms - 1) / sms) * ((d.kblocks + s2 - 1) / s2);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = s2;
+        }
+    }
+    if (forced > 0) best = std::min(forced, std::min(8, d.kblocks));
+    d.t1 = d.n_tiles - R;
+    d.split2 = best;
+    d.items = d.t1 + R * best;
+    return d.items;
+}
 static size_t dyn_items(const LinearArgs* a, int L) {
     // upper bound over the tail refinement (any linear may be the tail one, <= 12-block
     // items) and the chain split (<= 8)
@@ -2062,6 +2186,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     for (int l = 0; l < L; ++l)
         if (p.lin[l].dep >= 0) p.lin[p.lin[l].dep].signal = 1;
     bool prog_pdl = pdl;
+    RowBatch rb_pending = {};
+    int rb_rows = 0;
+    bool has_rb = false;
     if (nb > 0) {
         cudaError_t ea = cudaSuccess;
         if (batch_ok) {
@@ -2081,16 +2208,10 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             }
             rb.n = nb;
             rb.pdl = pdl ? 1 : 0;
-            cudaLaunchConfig_t acfg = {};
-            acfg.gridDim = dim3(rows);
-            acfg.blockDim = dim3(kRowThreads);
-            acfg.stream = st;
-            cudaLaunchAttribute aattr;
-            aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            aattr.val.programmaticStreamSerializationAllowed = 1;
-            acfg.attrs = &aattr;
-            acfg.numAttrs = pdl ? 1 : 0;
-            ea = cudaLaunchKernelEx(&acfg, act_quant_rows_kernel, rb);
+            // launched right before the GEMM below (launch_dyn)
+            rb_pending = rb;
+            rb_rows = rows;
+            has_rb = true;
         } else {
             for (int i = 0; i < nb && ea == cudaSuccess; ++i)
                 ea = launch_act_quant(bx[i], bdt[i], bld[i], bm[i], bk[i], bq[i], bs[i], bam[i], nullptr,
@@ -2119,6 +2240,20 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     int n_ext = 0;
     for (int l = 0; l < L; ++l) n_ext += p.lin[l].dep < 0 ? 1 : 0;
     const bool dyn = nb == n_ext && (!chain || dyn_chain_ok(a, deps, L)) && !(dyn_env && dyn_env[0] == '0');
+    const RowBatch* rbp = has_rb ? &rb_pending : nullptr;
+    if (has_rb && !dyn) {  // the cluster kernel: the stand-alone act-quant kernel
+        cudaLaunchConfig_t acfg = {};
+        acfg.gridDim = dim3(rb_rows);
+        acfg.blockDim = dim3(kRowThreads);
+        acfg.stream = st;
+        cudaLaunchAttribute aattr;
+        aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        aattr.val.programmaticStreamSerializationAllowed = 1;
+        acfg.attrs = &aattr;
+        acfg.numAttrs = rb_pending.pdl ? 1 : 0;
+        const cudaError_t ea = cudaLaunchKernelEx(&acfg, act_quant_rows_kernel, rb_pending);
+        if (ea != cudaSuccess) return ea;
+    }
     if (dyn && chain) {
         // Dependency chain on the dynamic kernel: items in PROGRAM order (a producer's items
         // are all handed out before its dependent's), per-linear completion counters and
@@ -2132,11 +2267,11 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         int ib = 0, tb = 0;
         for (int l = 0; l < L; ++l) {
             LinDesc& d = p.lin[l];
-            d.split = chain_split(d.n_tiles, d.kblocks, std::min(sms, device_sm_count()));
+            split_alone(d, std::min(sms, device_sm_count()));
             d.off = ib;  // round-robin continues across linears (reduced mod C in the kernel)
             d.ibase = ib;
             d.tbase = tb;
-            ib += d.n_tiles * d.split;
+            ib += d.items;
             tb += d.n_tiles;
         }
         for (int l = 0; l < L; ++l) {
@@ -2150,7 +2285,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             y.amax_c0 = c0;
             y.amax_c1 = c0 + d.K;
             d.dep_done = y.done;
-            d.dep_target = static_cast<uint32_t>(y.n_tiles * y.split);
+            d.dep_target = static_cast<uint32_t>(y.items);
             d.amax_src = y.amax_dst;
             // the grid-wide quantized x (compact a8: BN rows per k-block), after the
             // external linears' buffers in the scratch
@@ -2171,9 +2306,9 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         for (int l = 0; l < L; ++l) p.lin[l].off %= p.C;
         if (plan_log) std::fprintf(stderr, "[ody] dynamic chain: %d items over %d CTAs\n", ib, p.C);
         switch (bn) {
-            case 16: return launch_dyn<16, true, 2>(p, prog_pdl, st);
-            case 32: return launch_dyn<32, true, 2>(p, prog_pdl, st);
-            default: return launch_dyn<64, true, 2>(p, prog_pdl, st);
+            case 16: return launch_dyn<16, true, 2>(p, prog_pdl, st, rbp, rb_rows);
+            case 32: return launch_dyn<32, true, 2>(p, prog_pdl, st, rbp, rb_rows);
+            default: return launch_dyn<64, true, 2>(p, prog_pdl, st, rbp, rb_rows);
         }
     }
     if (dyn) {
@@ -2193,11 +2328,16 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             LinDesc& d = sorted[l];
             // a lone linear is split like a chain link (all SMs, short last wave); in a
             // program the other linears' items fill the machine
-            d.split = L == 1 ? chain_split(d.n_tiles, d.kblocks, std::min(sms, device_sm_count())) : dyn_split(d.kblocks);
-            if (l == L - 1 && L > 1 && tail_kb > 0) d.split = std::max(d.split, (d.kblocks + tail_kb - 1) / tail_kb);
+            if (L == 1) {
+                split_alone(d, std::min(sms, device_sm_count()));
+            } else {
+                int s = dyn_split(d.kblocks);
+                if (l == L - 1 && tail_kb > 0) s = std::max(s, (d.kblocks + tail_kb - 1) / tail_kb);
+                split_uniform(d, s);
+            }
             d.ibase = ib;
             d.tbase = tb;
-            ib += d.n_tiles * d.split;
+            ib += d.items;
             tb += d.n_tiles;
         }
         for (int l = 0; l < L; ++l) p.lin[l] = sorted[l];
@@ -2214,9 +2354,12 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         int mmax = 1;
         for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
         switch (dyn_bn(mmax)) {
-            case 16: return (L == 1 ? launch_dyn<16, false, 4>(p, prog_pdl, st) : launch_dyn<16, false, 2>(p, prog_pdl, st));
-            case 32: return (L == 1 ? launch_dyn<32, false, 4>(p, prog_pdl, st) : launch_dyn<32, false, 2>(p, prog_pdl, st));
-            default: return (L == 1 ? launch_dyn<64, false, 4>(p, prog_pdl, st) : launch_dyn<64, false, 2>(p, prog_pdl, st));
+            case 16: return (L == 1 ? launch_dyn<16, false, 4>(p, prog_pdl, st, rbp, rb_rows)
+                                    : launch_dyn<16, false, 2>(p, prog_pdl, st, rbp, rb_rows));
+            case 32: return (L == 1 ? launch_dyn<32, false, 4>(p, prog_pdl, st, rbp, rb_rows)
+                                    : launch_dyn<32, false, 2>(p, prog_pdl, st, rbp, rb_rows));
+            default: return (L == 1 ? launch_dyn<64, false, 4>(p, prog_pdl, st, rbp, rb_rows)
+                                    : launch_dyn<64, false, 2>(p, prog_pdl, st, rbp, rb_rows));
         }
     }
     cudaLaunchConfig_t cfg = {};
@@ -2250,10 +2393,12 @@ cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st) {
 // ody_gemm's decode widths (M <= 64) on pre-quantized activations (an ody_qtensor: the
 // 128-row padded a8 layout): the dynamic decode kernel as a program of ONE linear, its
 // k-split chosen like a chain link's so every SM streams weights.
-size_t gemm_prequant_scratch_bytes(int M, int N, int K) {
-    const int sms = device_sm_count();
-    const int kb = static_cast<int>(pad_k(K) / kBlockK), nt = static_cast<int>(pad_n(N) / kTileN);
-    return kZeroRegion + static_cast<size_t>(nt) * chain_split(nt, kb, sms) * dyn_bn(M) * kTileN * 4;
+size_t gemm_prequant_scratch_bytes(int M, int N, int K, int max_ctas) {
+    const int sms = std::min(max_ctas > 0 ? max_ctas : device_sm_count(), device_sm_count());
+    LinDesc d = {};
+    d.kblocks = static_cast<int>(pad_k(K) / kBlockK);
+    d.n_tiles = static_cast<int>(pad_n(N) / kTileN);
+    return kZeroRegion + static_cast<size_t>(split_alone(d, sms)) * dyn_bn(M) * kTileN * 4;
 }
 
 bool gemm_prequant_eligible(int M, int N, int K) {
@@ -2262,7 +2407,7 @@ bool gemm_prequant_eligible(int M, int N, int K) {
 
 cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& g, void* scratch, size_t scratch_bytes, cudaStream_t st) {
     if (!gemm_prequant_eligible(g.M, g.N, g.K)) return cudaErrorInvalidValue;
-    if (!scratch || scratch_bytes < gemm_prequant_scratch_bytes(g.M, g.N, g.K)) return cudaErrorInvalidValue;
+    if (!scratch || scratch_bytes < gemm_prequant_scratch_bytes(g.M, g.N, g.K, g.max_ctas)) return cudaErrorInvalidValue;
     const int sms = std::min(g.max_ctas > 0 ? g.max_ctas : device_sm_count(), device_sm_count());
     PParams p = {};
     p.L = 1;
@@ -2281,8 +2426,7 @@ cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& g, void* scratch, size_t s
     d.sa = g.sa;
     d.Mp = static_cast<int>(pad_m(g.M));
     d.dep = -1;
-    d.split = chain_split(d.n_tiles, d.kblocks, sms);
-    p.n_items = d.n_tiles * d.split;
+    p.n_items = split_alone(d, sms);
     uint32_t* counters = static_cast<uint32_t*>(scratch);
     p.ctr = counters;
     p.work = counters + kMaxLin + 1;

@@ -78,7 +78,7 @@ cudaError_t launch_w4a8_prefill(const GemmArgs& a, cudaStream_t st);
 // kernel as a one-linear program (decode_kernel.cu).  scratch: gemm_prequant_scratch_bytes,
 // its first program_zero_bytes() zeroed once (left zeroed).
 bool gemm_prequant_eligible(int M, int N, int K);
-size_t gemm_prequant_scratch_bytes(int M, int N, int K);
+size_t gemm_prequant_scratch_bytes(int M, int N, int K, int max_ctas);
 cudaError_t launch_w4a8_gemm_prequant(const GemmArgs& a, void* scratch, size_t scratch_bytes, cudaStream_t st);
 
 // The W4A8 linear y = x W^T end to end from unquantized activations: K1 fused into the

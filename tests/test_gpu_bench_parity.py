@@ -139,6 +139,20 @@ def test_config1_c_abi_vs_oracle(oracle):
     assert np.array_equal(bits_of(out), bits_of(oracle.exact_fast_gemm(codes, sa, wcodes, sw)))
 
 
+@pytest.mark.parametrize("m,n,k", [(16, 27648, 5120), (5, 20544, 2048)])
+def test_c_abi_over_one_wave_vs_oracle(oracle, m, n, k):
+    """ody_gemm at decode widths with more 128-row tiles than SMs (gate_up's 216; 161):
+    the partial last wave runs k-split (split2 2 / 4); bit-exact vs the oracle."""
+    from paper_2311_09550_b200 import api
+    a, w = oracle.bench_inputs(7, m, n, k)
+    aq = api.quantize_activations_per_token(a)
+    wq = api.quantize_weights(w)
+    out = api.gemm_w4a8_fast(aq, wq)
+    codes, sa = oracle.quantize_activations(a)
+    wcodes, _, sw = oracle.quantize_weights(w)
+    assert np.array_equal(bits_of(out), bits_of(oracle.exact_fast_gemm(codes, sa, wcodes, sw)))
+
+
 def test_acceptance_sweep_c_abi(oracle):
     """acceptance.cpp:65-105 replayed on the GPU through the C ABI: 100 random matrices
     (Rng(101), w 0.2 N(0,1)): acc % 16 == 0, acc >> 4 == the int code dot, and the whole

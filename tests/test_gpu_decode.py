@@ -52,6 +52,7 @@ def _assert_bits(got, want):
     (16, 5120, 14336),   # the largest K a program's batched act quant holds (128 x 7 x 16)
     (5, 15360, 5120), (16, 27648, 5120), (11, 5120, 13824), (1, 5120, 5120),
     (17, 640, 1536), (33, 5120, 5120), (64, 2048, 13824), (48, 130, 1000),  # BN 32 / 64 kernels
+    (3, 20544, 2048), (40, 27648, 5120),  # > 148 tiles: the partial last wave k-split (split2 4 / 2)
 ])
 def test_decode_linear_vs_oracle(m, n, k, oracle, torch_cuda, dev):
     torch = torch_cuda
@@ -328,3 +329,4 @@ def test_program_row_parallel_shards(oracle, torch_cuda, dev):
         assert torch.equal(accs[0] + accs[1], want_acc), m
         y = dev.dequant_epilogue(accs[0] + accs[1], aq.s, full.s, torch.float16)
         assert torch.equal(y, dev.w4a8_gemm(aq, full, torch.float16)), m
+

@@ -33,10 +33,13 @@ def main(m=16, single=None):
                             dev.LinearCall(outs[0][:, :H], ws[1], outs[1], dep=0),
                             dev.LinearCall(outs[1], ws[2], outs[2], dep=1),
                             dev.LinearCall(outs[2][:, :I], ws[3], outs[3], dep=2)])
+    buf = torch.zeros(148 * 32 + 512 + 512, dtype=torch.int64, device="cuda")
     for _ in range(3):
         prog.run()
     torch.cuda.synchronize()
-    buf = torch.zeros(148 * 32 + 512 + 512, dtype=torch.int64, device="cuda")
+    # traced launch right behind an untraced one: no other kernel in between (any other
+    # kernel leaves the SM instruction caches cold, tools/icache_probe.cu)
+    prog.run()
     lib().ody_dev_set_trace(buf.data_ptr())
     prog.run()
     lib().ody_dev_set_trace(None)
@@ -60,7 +63,7 @@ def main(m=16, single=None):
         v = (v - base) / 1e3
         return f"{v.min():6.2f}/{np.median(v):6.2f}/{v.max():6.2f} n={len(v):3d}"
     print(f"CTAs {len(t)}  (min/median/max us from the first CTA entry)")
-    for nm, col in [("entry", 0), ("setup", 1), ("producer done", 6), ("epilogues done", 4), ("exit", 5)]:
+    for nm, col in [("entry", 0), ("setup", 1), ("producer in", 2), ("item id", 3), ("first item", 30), ("first W issued", 31), ("producer done", 6), ("epilogues done", 4), ("exit", 5)]:
         print(f"  {nm:14s} {stat(col)}")
     for i, (name, _, _) in enumerate(LAYERS):
         print(f"  {name:8s} first MMA {stat(10 + 4 * i)}  dep released {stat(12 + 4 * i)}  last epilogue {stat(11 + 4 * i)}")
@@ -81,7 +84,8 @@ def main(m=16, single=None):
                   ", ".join(f"{c}({d[c]:.2f})" for c in order[:5]) +
                   f"; non-quantizing max {d[~quant].max() if (~quant).any() else 0:.2f}")
     et = buf[148 * 32 + 512:].view(32, 16).cpu().numpy()[:, :11]
-    print("last CTA, per item epilogue (us): d_full, tmem ld, scales, atom, reduced, stored, amax, done, after-bar")
+    print("last CTA, per item epilogue (us): d_full, tmem ld, scales, atom, reduced, stored, amax, done, after-bar, "
+          "fields, token 8")
     for j2 in range(32):
         row = et[j2]
         if row.max() == 0:
