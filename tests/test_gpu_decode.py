@@ -49,7 +49,7 @@ def _assert_bits(got, want):
 
 @pytest.mark.parametrize("m,n,k", [
     (1, 128, 128), (3, 130, 1000), (16, 1000, 4100), (7, 384, 64), (2, 257, 2049),
-    (16, 5120, 14336),   # the largest K a program's batched act quant holds (128 x 7 x 16)
+    (16, 5120, 14336), (3, 640, 16384),  # largest K the batched act quant holds: 256 x 4 x 16
     (5, 15360, 5120), (16, 27648, 5120), (11, 5120, 13824), (1, 5120, 5120),
     (17, 640, 1536), (33, 5120, 5120), (64, 2048, 13824), (48, 130, 1000),  # BN 32 / 64 kernels
     (3, 20544, 2048), (40, 27648, 5120),  # > 148 tiles: the partial last wave k-split (split2 4 / 2)
