@@ -250,14 +250,18 @@ class SeqLayer:
     one-launch chain program (tools/layer_launch_ab.py).  Shares one
     workspace across its programs (stream-ordered)."""
 
-    def __init__(self, dev, ws, x, workspace=None):
+    def __init__(self, dev, ws, x, workspace=None, links=False):
         import torch
         m = x.shape[0]
         self.outs = [torch.empty((m, w.n), dtype=torch.float16, device=x.device) for w in ws]
         o, d = ws[1], ws[3]
         ins = [x, self.outs[0][:, :o.k], self.outs[1], self.outs[2][:, :d.k]]
         self.progs = []
-        for i, w, y in zip(ins, ws, self.outs):
+        if links:
+            calls = [dev.LinearCall(i, w, y, dep=li - 1) for li, (i, w, y) in enumerate(zip(ins, ws, self.outs))]
+            self.progs.append(dev.Program(calls, workspace=workspace, links=True))
+            workspace = self.progs[-1].workspace
+        for i, w, y in ([] if links else zip(ins, ws, self.outs)):
             self.progs.append(dev.Program([dev.LinearCall(i, w, y)], workspace=workspace))
             workspace = self.progs[-1].workspace
         self.workspace = workspace
@@ -378,6 +382,9 @@ def roofline(args, dev, h, stream):
     chains = [ChainLayer(dev, cw, h["x"]) for cw in h["copies"]]
     ms_chain = _graph_time(lambda: [c.run(pdl=True, stream=stream) for c in chains], stream, reps=50) / len(chains)
     del chains
+    links = [SeqLayer(dev, cw, h["x"], links=True) for cw in h["copies"]]
+    ms_links = _graph_time(lambda: [c.run(pdl=True, stream=stream) for c in links], stream, reps=50) / len(links)
+    del links
     torch.cuda.empty_cache()
     per = {}
     wsl = dev.Workspace.get_linear(m, 27648, 13824, "cuda")
@@ -408,6 +415,12 @@ def roofline(args, dev, h, stream):
                               "frac": round(step_bytes(m) / (ms_chain * 1e-3) / 1e9 / hbm, 4),
                               "note": "the same dependent layer as ONE program launch (in-kernel grid-wide "
                                       "quantization of each dependent x), PDL"},
+            "chain_links": {"us": round(ms_links * 1e3, 3),
+                            "GB/s": round(step_bytes(m) / (ms_links * 1e-3) / 1e9, 1),
+                            "frac": round(step_bytes(m) / (ms_links * 1e-3) / 1e9 / hbm, 4),
+                            "note": "the same dependent layer as one launch per linear with each dependent x "
+                                    "quantized in-kernel from the producer launch's row maxima "
+                                    "(ody_dev_w4a8_linear_chain: one act-quant kernel per layer), PDL"},
             "independent_linears_program": {"us": round(ms_ind * 1e3, 3),
                                             "GB/s": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9, 1),
                                             "frac": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9 / hbm, 4),

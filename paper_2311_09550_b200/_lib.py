@@ -85,6 +85,8 @@ SIGNATURES = {
     "ody_dev_w4a8_linear_program": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p,
                                             c_size_t, c_void_p]),
     "ody_dev_program_is_fused": (c_int, [c_void_p, c_int]),
+    "ody_dev_w4a8_linear_chain": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p]),
+    "ody_dev_chain_is_links": (c_int, [c_void_p, c_int]),
     "ody_dev_linear_is_fused": (c_int, [c_size_t, c_size_t, c_size_t]),
     "ody_dev_set_linear_mode": (None, [c_int]),
     "ody_dev_set_prefill_min_m": (None, [c_int]),

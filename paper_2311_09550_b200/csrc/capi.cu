@@ -903,9 +903,8 @@ int ody_dev_program_is_fused(const ody_linear_desc* lin, int count) {
     return linear_mode() == 2 && program_eligible(a.data(), deps.data(), count, 0) ? 1 : 0;
 }
 
-ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, void* workspace,
-                                       size_t workspace_bytes, int max_ctas, int pdl,
-                                       const void* next_w, size_t next_w_bytes, void* stream) {
+namespace {
+ody_status program_check(const ody_linear_desc* lin, int count, void* workspace, size_t workspace_bytes) {
     if (!lin || !workspace) return einval("ody_dev_w4a8_linear_program: null argument");
     if (count < 1 || count > kProgramMaxLinears)
         return einval("ody_dev_w4a8_linear_program: 1..8 linears per program");
@@ -925,6 +924,40 @@ ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, vo
     }
     if (workspace_bytes < ody_dev_program_workspace_bytes(lin, count))
         return einval("ody_dev_w4a8_linear_program: workspace too small");
+    return ODY_OK;
+}
+}  // namespace
+
+int ody_dev_chain_is_links(const ody_linear_desc* lin, int count) {
+    if (!lin || count < 1 || count > kProgramMaxLinears) return 0;
+    std::vector<LinearArgs> a;
+    std::vector<int> deps;
+    program_args(lin, count, 0, &a, &deps);
+    return chain_links_eligible(a.data(), deps.data(), count) ? 1 : 0;
+}
+
+ody_status ody_dev_w4a8_linear_chain(const ody_linear_desc* lin, int count, void* workspace,
+                                     size_t workspace_bytes, int max_ctas, int pdl, void* stream) {
+    const ody_status c = program_check(lin, count, workspace, workspace_bytes);
+    if (c != ODY_OK) return c;
+    std::vector<LinearArgs> a;
+    std::vector<int> deps;
+    program_args(lin, count, max_ctas, &a, &deps);
+    if (!chain_links_eligible(a.data(), deps.data(), count))  // same results, as a program
+        return ody_dev_w4a8_linear_program(lin, count, workspace, workspace_bytes, max_ctas, pdl, nullptr, 0,
+                                           stream);
+    return guarded([&] {
+        cuda_check(launch_w4a8_chain_links(a.data(), deps.data(), count, workspace, workspace_bytes, pdl != 0,
+                                           static_cast<cudaStream_t>(stream)),
+                   "w4a8 chain links launch");
+    });
+}
+
+ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, void* workspace,
+                                       size_t workspace_bytes, int max_ctas, int pdl,
+                                       const void* next_w, size_t next_w_bytes, void* stream) {
+    const ody_status c = program_check(lin, count, workspace, workspace_bytes);
+    if (c != ODY_OK) return c;
     return guarded([&] {
         std::vector<LinearArgs> a;
         std::vector<int> deps;

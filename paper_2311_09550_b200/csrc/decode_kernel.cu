@@ -126,6 +126,8 @@ struct LinDesc {
     const uint32_t* amax_src;  // dependent linear: per-token max |x| (its producer's amax_dst)
     uint32_t* qdone;      // dependent linear: k-blocks of x quantized into qa (grid-wide), or NULL
     uint32_t qtarget;     //   complete at kblocks
+    uint32_t* amax_reset; // row maxima this launch's last CTA re-zeroes (the chain program: its
+                          // amax_dst; a chain link launch: the amax_src its x was quantized with)
 };
 
 constexpr int kRowThreads = 256;
@@ -156,6 +158,7 @@ struct PParams {
     uint32_t* tile_cnt;   // [program tiles] split arrivals (zeroed)
     int pdl;
     int pf_units;         // L2 prefetch window past the smem ring (units)
+    int no_item_pf;       // a dependent item does not L2-prefetch its weights while x is quantized
     const uint8_t* next_wp;  // cross-kernel hint: L2-prefetch this slice of the next weights
     size_t next_bytes;
     int dbg;              // diagnostics (ODY_DBG_DECODE): 1 store raw x (no quant math), 2 no IEEE redo
@@ -1368,7 +1371,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 // its producer linear completes.  While it has not, keep HBM streaming: pull
                 // this whole item's weights into L2 (the ring then refills from L2).
                 const bool depi = d.qdone != nullptr;
-                if (depi && lane == 0 && ld_acquire_u32(d.qdone) < d.qtarget)
+                if (depi && !p.no_item_pf && lane == 0 && ld_acquire_u32(d.qdone) < d.qtarget)
                     bulk_prefetch_l2(wtile + static_cast<size_t>(x.kb_lo) * kWBlockBytes,
                                      static_cast<uint32_t>(x.kb_hi - x.kb_lo) * kWBlockBytes);
                 for (int k0 = 0; k0 < nunits; k0 += 2) {
@@ -1505,13 +1508,20 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 if (trc && l < 4) trc[12 + 4 * l] = globaltimer();
             }
             named_bar_sync(4, 64);
-            int nq = 0;
-            for (int kb = static_cast<int>(blockIdx.x); kb < d.kblocks; kb += static_cast<int>(gridDim.x), ++nq) {
-                // BN rows x 8 sixteen-element chunks of k-block kb (unrolled: every load of
-                // a thread is in flight at once, one L2 round trip)
+            // CTA c owns an even share [lo, hi) of the x's kblocks x BN x 8 sixteen-element
+            // chunks (a k-block per CTA left most CTAs idle and made the grid wait on the
+            // few that quantized: ~1-2 chunks per thread is one L2 round trip)
+            const int nchunks = d.kblocks * BN * 8;
+            const int lo = static_cast<int>((static_cast<long long>(nchunks) * blockIdx.x) / gridDim.x);
+            const int hi = static_cast<int>((static_cast<long long>(nchunks) * (blockIdx.x + 1)) / gridDim.x);
+            {
+                for (int task0 = lo; task0 < hi; task0 += 4 * 64) {
 #pragma unroll
-                for (int task = qt; task < BN * 8; task += 64) {
-                    const int t = task >> 3, c = task & 7;
+                for (int u = 0; u < 4; ++u) {
+                    const int task = task0 + u * 64 + qt;
+                    if (task >= hi) break;
+                    const int kb = task / (BN * 8);
+                    const int t = (task >> 3) % BN, c = task & 7;
                     const int k0 = kb * kBlockK + c * 16;
                     uint4 v = make_uint4(0u, 0u, 0u, 0u);
                     if (t < d.M && k0 < d.K) {
@@ -1538,12 +1548,14 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     *reinterpret_cast<uint4*>(const_cast<int8_t*>(d.qa) + static_cast<size_t>(kb) * BN * 128 + t * 128 +
                                               ((c ^ (t & 7)) << 4)) = v;
                 }
+                }
             }
             // no writer-side proxy fence: each consumer orders its bulk copies (async proxy)
             // after its acquire of qdone with fence.proxy.async (the `released` check); the
-            // release below publishes these generic stores at gpu scope
+            // release below publishes these generic stores at gpu scope.  Every CTA counts
+            // once (qtarget = the grid).
             named_bar_sync(4, 64);
-            if (qt == 0 && nq > 0) red_release_add_u32(d.qdone, static_cast<uint32_t>(nq));
+            if (qt == 0) red_release_add_u32(d.qdone, 1u);
             if (trc && qt == 0 && l < 4) trc[13 + 4 * l] = globaltimer();
         }
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4 * kDynConvGroups) {
@@ -1752,11 +1764,13 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             emark(j, 5);
             if (trc && r == 0 && x.l < 4) trc[11 + 4 * x.l] = globaltimer();
-            if (d.done != nullptr) {
+            if (d.done != nullptr || amx_on) {
                 // publish: every store (and row-max contribution) of this item happens
                 // before the release increment the dependent linear acquires.  One global
                 // atomicMax per token per item, each token on its own 128-byte line (the
                 // whole grid's items hit these few addresses: same-line atomics serialise).
+                // A chain link launch (no `done`: its consumer is the NEXT launch, ordered
+                // by kernel completion) only contributes the row maxima.
                 named_bar_sync(3, 128);
                 if (amx_on && r < d.M) {
                     const uint32_t m = emax[r];
@@ -1765,7 +1779,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 }
                 if (amx_on) named_bar_sync(3, 128);
                 emark(j, 6);
-                if (r == 0) red_release_add_u32(d.done, 1u);  // cumulative over the CTA barrier
+                if (r == 0 && d.done) red_release_add_u32(d.done, 1u);  // cumulative over the CTA barrier
                 emark(j, 7);
             }
         }
@@ -1786,8 +1800,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             for (int l = 0; l < p.L; ++l) {  // chain state of this launch (zero region)
                 if (p.lin[l].done) *p.lin[l].done = 0u;
                 if (p.lin[l].qdone) *p.lin[l].qdone = 0u;
-                if (p.lin[l].amax_dst)
-                    for (int t = 0; t < p.lin[l].M; ++t) p.lin[l].amax_dst[t * kAmaxStride] = 0u;
+                if (p.lin[l].amax_reset)
+                    for (int t = 0; t < p.lin[l].M; ++t) p.lin[l].amax_reset[t * kAmaxStride] = 0u;
             }
             __threadfence();
         }
@@ -2297,6 +2311,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             y.amax_dst = amax + d.dep * kChainMaxM * kAmaxStride;
             y.amax_c0 = c0;
             y.amax_c1 = c0 + d.K;
+            y.amax_reset = y.amax_dst;
             d.dep_done = y.done;
             d.dep_target = static_cast<uint32_t>(y.items);
             d.amax_src = y.amax_dst;
@@ -2306,13 +2321,14 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             cursor += round_up(static_cast<size_t>(bn) * pad_k(d.K), 256);
             d.Mp = bn;
             d.qdone = qdone + l;
-            d.qtarget = static_cast<uint32_t>(d.kblocks);
         }
         p.n_items = ib;
         p.work = counters + kMaxLin + 1;
         p.pf_units = 0;
         p.S = 1;
         p.C = std::min(sms, ib);
+        for (int l = 0; l < L; ++l)  // every CTA quantizes a share of each dependent x
+            if (p.lin[l].qdone) p.lin[l].qtarget = static_cast<uint32_t>(p.C);
         static const char* st_env = ODY_DIAG_ENV("ODY_CHAIN_DYNAMIC");  // diagnostics: 1 = counter
         p.chain_static = (st_env && st_env[0] == '1') ? 0 : 1;
         p.reset_at_exit = 1;  // done / qdone / row maxima (and the counter when dynamic)
@@ -2395,6 +2411,138 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
     cfg.attrs = attr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, w4a8_decode_kernel, p);
+}
+
+// A dependency chain as ONE LAUNCH PER LINEAR ("chain links"): each linear is a lone
+// linear on the dynamic kernel (its own balanced split, static deal), and the kernel
+// boundary replaces the chain program's grid-wide `done` counter.  A producer's epilogues
+// accumulate its consumer's per-token row maxima (as in the chain program); the consumer
+// launch, once griddepcontrol.wait returned (the producer grid completed, its maxima
+// final), quantizes its x grid-wide in-kernel (B-quantizer warps, `qdone`) while its
+// weights already stream -- no act-quant kernel and no second kernel boundary between
+// two linears.  The consumer's last CTA re-zeroes its qdone and the row maxima it read.
+// External linears keep the act-quant kernel.  Same scratch as launch_w4a8_program.
+bool chain_links_eligible(const LinearArgs* a, const int* deps, int L) {
+    if (!deps || L < 1 || L > kMaxLin || !dyn_chain_ok(a, deps, L)) return false;
+    for (int l = 0; l < L; ++l) {
+        if (!lin_ok(a[l], deps[l] < 0) || a[l].M > kChainMaxM) return false;
+        if (pad_n(a[l].N) / kTileN > kProgramMaxTiles) return false;
+    }
+    return true;
+}
+
+cudaError_t launch_w4a8_chain_links(const LinearArgs* a, const int* deps, int L, void* scratch,
+                                    size_t scratch_bytes, bool pdl, cudaStream_t st) {
+    if (!chain_links_eligible(a, deps, L)) return cudaErrorInvalidValue;
+    if (!scratch || scratch_bytes < program_scratch_bytes(a, deps, L)) return cudaErrorInvalidValue;
+    const int sms = std::min(a[0].max_ctas > 0 ? a[0].max_ctas : device_sm_count(), device_sm_count());
+    int mmax = 1;
+    for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
+    const int bn = dyn_bn(mmax);
+    uint32_t* counters = static_cast<uint32_t*>(scratch);
+    uint32_t* qdone = counters + kChainDoneU32 + kMaxLin;
+    uint32_t* amax = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kChainAmaxOffset);
+    uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion + dyn_items(a, L) * bn * kTileN * 4;
+    int consumer[kMaxLin];
+    for (int l = 0; l < L; ++l) consumer[l] = -1;
+    for (int l = 0; l < L; ++l)
+        if (deps[l] >= 0) consumer[deps[l]] = l;
+    for (int l = 0; l < L; ++l) {
+        PParams p = {};
+        p.L = 1;
+        LinDesc& d = p.lin[0];
+        d.x = a[l].x;
+        d.ldx = a[l].ldx;
+        d.x_bf16 = a[l].x_dtype == kDtypeBF16 ? 1 : 0;
+        d.wp = a[l].wp;
+        d.sw = a[l].sw;
+        d.out = a[l].out;
+        d.out_dtype = a[l].out_dtype;
+        d.sa_out = a[l].sa_out;
+        d.M = a[l].M;
+        d.N = a[l].N;
+        d.K = a[l].K;
+        d.kblocks = static_cast<int>(pad_k(a[l].K) / kBlockK);
+        d.n_tiles = static_cast<int>(pad_n(a[l].N) / kTileN);
+        d.dep = -1;  // the producer is an earlier LAUNCH, not a linear of this one
+        d.acc_out = a[l].acc_out;
+        const bool dep = deps[l] >= 0;
+        RowBatch rb = {};
+        if (!dep) {
+            int8_t* q = reinterpret_cast<int8_t*>(cursor);
+            cursor += round_up(a8_bytes(d.M, d.K), 256);
+            float* sa = a[l].sa_out ? a[l].sa_out : reinterpret_cast<float*>(cursor);
+            cursor += round_up(pad_m(d.M) * 4, 256);
+            d.qa = q;
+            d.sa = sa;
+            d.Mp = bn;  // compact a8 layout: BN rows per k-block
+            rb.x[0] = static_cast<const unsigned short*>(a[l].x);
+            rb.ldx[0] = a[l].ldx;
+            rb.M[0] = d.M;
+            rb.K[0] = d.K;
+            rb.Mp[0] = bn;
+            rb.bf16[0] = d.x_bf16;
+            rb.q[0] = q;
+            rb.s[0] = sa;
+            rb.amax_in[0] = a[l].absmax_in;
+            rb.n = 1;
+            rb.pdl = (pdl || l > 0) ? 1 : 0;
+        } else {
+            d.qa = reinterpret_cast<const int8_t*>(cursor);
+            cursor += round_up(static_cast<size_t>(bn) * pad_k(d.K), 256);
+            d.Mp = bn;
+            d.qdone = qdone + l;
+            d.dep_done = d.qdone;  // satisfied at once (dep_target 0): griddepcontrol.wait orders
+            d.dep_target = 0;      //   this launch after its producer's
+            d.amax_src = amax + deps[l] * kChainMaxM * kAmaxStride;
+            d.amax_reset = const_cast<uint32_t*>(d.amax_src);
+        }
+        if (consumer[l] >= 0) {
+            int c0 = 0;
+            dyn_chain_slice(a, deps, L, consumer[l], &c0);
+            d.amax_dst = amax + l * kChainMaxM * kAmaxStride;
+            d.amax_c0 = c0;
+            d.amax_c1 = c0 + a[consumer[l]].K;
+        }
+        p.n_items = split_alone(d, sms);
+        p.ctr = counters;
+        p.work = counters + kMaxLin + 1;
+        p.tile_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kProgramCounterRegion);
+        p.acc = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kAccOffset);
+        p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
+        p.S = 1;
+        p.C = std::min(sms, p.n_items);
+        if (dep) d.qtarget = static_cast<uint32_t>(p.C);  // every CTA quantizes a share of x
+        // the whole-item L2 prefetch while x is quantized floods the memory queues the
+        // quantizers' loads wait in (their round trip is this launch's critical path)
+        static const char* lpf_env = ODY_DIAG_ENV("ODY_LINKS_ITEM_PF");  // diagnostics: 1 = on
+        p.no_item_pf = (lpf_env && lpf_env[0] == '1') ? 0 : 1;
+        p.chain_static = 1;
+        p.reset_at_exit = dep ? 1 : 0;  // qdone + the consumed row maxima
+        // a link after the first always waits on the previous launch in-kernel (PDL)
+        const bool lpdl = pdl || l > 0;
+        p.pdl = (lpdl || !dep) ? 1 : 0;  // an external link overlaps its act quant
+        // diagnostics: one trace block per link (the per-CTA slots + the last CTA's units)
+        p.trace = a[l].trace ? a[l].trace + static_cast<size_t>(l) * (148 * kTraceCta + 1536) : nullptr;
+        cudaError_t e = cudaSuccess;
+        const RowBatch* rbp = dep ? nullptr : &rb;  // lin_ok: an external K fits the row kernel
+        const bool kpdl = p.pdl != 0;
+        if (dep) {
+            switch (bn) {
+                case 16: e = launch_dyn<16, true, 4>(p, kpdl, st); break;
+                case 32: e = launch_dyn<32, true, 4>(p, kpdl, st); break;
+                default: e = launch_dyn<64, true, 4>(p, kpdl, st); break;
+            }
+        } else {
+            switch (bn) {
+                case 16: e = launch_dyn<16, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
+                case 32: e = launch_dyn<32, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
+                default: e = launch_dyn<64, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
+            }
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_w4a8_decode(const LinearArgs& a, cudaStream_t st) {

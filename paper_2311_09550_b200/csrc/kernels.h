@@ -135,6 +135,12 @@ size_t program_zero_bytes();
 DecodePlan plan_program(const LinearArgs* a, const int* deps, int L, int sms);
 bool program_eligible(const LinearArgs* a, const int* deps, int L, int num_sms);
 size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L);
+// A dependency chain as one launch per linear (decode_kernel.cu "chain links"): dependent
+// linears quantize their x in-kernel from the row maxima their producer launch's
+// epilogues accumulated.  Same scratch as launch_w4a8_program.
+bool chain_links_eligible(const LinearArgs* a, const int* deps, int L);
+cudaError_t launch_w4a8_chain_links(const LinearArgs* a, const int* deps, int L, void* scratch,
+                                    size_t scratch_bytes, bool pdl, cudaStream_t st);
 cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, void* scratch, size_t scratch_bytes,
                                 bool pdl, const uint8_t* next_wp, size_t next_bytes, cudaStream_t st);
 

@@ -271,7 +271,7 @@ class Program:
     is built once; ``run`` launches it (also inside CUDA-graph capture)."""
 
     def __init__(self, calls: list, workspace: torch.Tensor | None = None,
-                 prefetch_next: "W4Weight | None" = None, max_ctas: int = 0):
+                 prefetch_next: "W4Weight | None" = None, max_ctas: int = 0, links: bool = False):
         if not 1 <= len(calls) <= 8:
             raise OdyError(1, "a linear program holds 1..8 linears")
         self.calls = list(calls)
@@ -302,12 +302,22 @@ class Program:
         self.workspace = workspace
         self.prefetch_next = prefetch_next
         self.max_ctas = max_ctas
+        # links: a dependency chain as one launch per linear (ody_dev_w4a8_linear_chain),
+        # each dependent launch quantizing its x in-kernel
+        self.links = links
 
     @property
     def fused(self) -> bool:
+        if self.links:
+            return bool(lib().ody_dev_chain_is_links(self.descs, len(self.calls)))
         return bool(lib().ody_dev_program_is_fused(self.descs, len(self.calls)))
 
     def run(self, pdl: bool = False, stream=None):
+        if self.links:
+            check(lib().ody_dev_w4a8_linear_chain(self.descs, len(self.calls), self.workspace.data_ptr(),
+                                                  self.workspace.numel(), self.max_ctas, int(pdl),
+                                                  _stream(stream)))
+            return [c.acc_out if c.acc_out is not None else c.out for c in self.calls]
         nxt = self.prefetch_next.packed if self.prefetch_next is not None else None
         check(lib().ody_dev_w4a8_linear_program(
             self.descs, len(self.calls), self.workspace.data_ptr(), self.workspace.numel(), self.max_ctas,

@@ -79,11 +79,13 @@ def test_bench_program_vs_oracle(layer, oracle, torch_cuda, dev):
             assert np.array_equal(got.view(np.uint16), want.view(np.uint16)), (name, pdl)
 
 
-def test_dependent_chain_vs_oracle(layer, oracle, torch_cuda, dev):
+@pytest.mark.parametrize("links", [False, True])
+def test_dependent_chain_vs_oracle(links, layer, oracle, torch_cuda, dev):
     """qkv -> o -> gate_up -> down as a dependency chain in one program: each linear's
     input is the previous linear's fp16 output (column slices as the attention / SiLU
     stand-ins), quantized per token inside the launch.  Bit-exact vs the oracle run
-    step by step on the same fp16 intermediates."""
+    step by step on the same fp16 intermediates.  links: bench.py's headline step, the
+    chain as one launch per linear (each dependent x quantized in-kernel)."""
     torch = torch_cuda
     for m in (1, 16):
         rs = np.random.default_rng(70 + m)
@@ -94,8 +96,10 @@ def test_dependent_chain_vs_oracle(layer, oracle, torch_cuda, dev):
         prog = dev.Program([dev.LinearCall(xd, w[0], outs[0]),
                             dev.LinearCall(outs[0][:, :H], w[1], outs[1], dep=0),
                             dev.LinearCall(outs[1], w[2], outs[2], dep=1),
-                            dev.LinearCall(outs[2][:, :I], w[3], outs[3], dep=2)])
-        prog.run(pdl=True)
+                            dev.LinearCall(outs[2][:, :I], w[3], outs[3], dep=2)], links=links)
+        assert prog.fused
+        for _ in range(2):  # the second run starts from the state the first left behind
+            prog.run(pdl=True)
         torch.cuda.synchronize()
         cur = x
         for li, (name, n, k, wq, wcodes, sw) in enumerate(layer):

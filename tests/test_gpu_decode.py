@@ -204,12 +204,14 @@ def test_program_independent_layer(m, torch_cuda, dev):
             assert torch.equal(c.out, ref), name
 
 
+@pytest.mark.parametrize("links", [False, True])
 @pytest.mark.parametrize("m", [1, 16, 17, 32, 48, 64])
-def test_program_dependency_chain(torch_cuda, dev, m):
+def test_program_dependency_chain(torch_cuda, dev, m, links):
     """x of each linear is (a column slice of) an earlier linear's output inside the same
     launch: grid-wide completion counters order them; bit-identical to sequential runs,
     eagerly, back to back and from a CUDA graph.  Every decode width (BN = 16/32/64), in
-    a workspace of exactly the queried size."""
+    a workspace of exactly the queried size.  links: the same chain as one launch per
+    linear (ody_dev_w4a8_linear_chain, dependent x quantized in-kernel)."""
     torch = torch_cuda
     dims = [(3072, 1024), (1024, 2048), (2048, 1024), (1024, 2048)]  # (n, k); x1 = out0[:, :2048]
     ws = [_weights(torch, dev, n, k, seed=200 + i, scale=0.03)[0] for i, (n, k) in enumerate(dims)]
@@ -225,7 +227,7 @@ def test_program_dependency_chain(torch_cuda, dev, m):
         y = _two_kernel(dev, torch, h, w, torch.float16)
         refs.append(y)
         h = y[:, :2048] if i == 0 else y
-    prog = dev.Program(calls)
+    prog = dev.Program(calls, links=links)
     assert prog.fused
     st = torch.cuda.Stream()
     for pdl in (False, True):
@@ -267,8 +269,9 @@ def test_program_fallback_and_errors(torch_cuda, dev):
         dev.Program([dev.LinearCall(x2, w, o2, dep=0)]).run()
 
 
+@pytest.mark.parametrize("links", [False, True])
 @pytest.mark.parametrize("m,xdt", [(1, "f16"), (16, "bf16"), (32, "f16"), (64, "bf16")])
-def test_program_chain_vs_oracle(m, xdt, oracle, torch_cuda, dev):
+def test_program_chain_vs_oracle(m, xdt, links, oracle, torch_cuda, dev):
     """Dependency chain on the dynamic kernel (producer epilogues accumulate the consumer's
     per-token row max; the consumer quantizes its B tiles in-kernel): every linear's
     output bit-exact vs the oracle applied step by step to the same 16-bit intermediates.
@@ -283,7 +286,7 @@ def test_program_chain_vs_oracle(m, xdt, oracle, torch_cuda, dev):
              dev.LinearCall(outs[0][:, 8:1008], ws[1][0], outs[1], dep=0),
              dev.LinearCall(outs[1], ws[2][0], outs[2], dep=1),
              dev.LinearCall(outs[2], ws[3][0], outs[3], dep=2)]
-    prog = dev.Program(calls)
+    prog = dev.Program(calls, links=links)
     assert prog.fused
     for rep in range(3):
         for o in outs:
