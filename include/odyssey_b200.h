@@ -71,10 +71,15 @@ typedef struct ody_gemm_counters {
 
 const char* ody_last_error(void);                 /* ref odyssey.h:55 */
 void ody_string_free(char* s);                    /* ref odyssey.h:57 */
-void ody_set_threads(int n);                      /* ref odyssey.h:61 (host threads: no-op) */
+void ody_set_threads(int n);                      /* ref odyssey.h:61 -- here: the host threads
+                                                   * of the ABI's host copies (<= 0: auto) */
 
 ody_status ody_tensor_create(size_t rows, size_t cols, const float* data,
                              ody_tensor** out);   /* ref odyssey.h:65 */
+/* Extension: the same from a row-strided host matrix (row r at data + r * ld), so a column
+ * slice of a larger matrix needs no intermediate contiguous copy. */
+ody_status ody_tensor_create_strided(size_t rows, size_t cols, size_t ld, const float* data,
+                                     ody_tensor** out);
 void ody_tensor_free(ody_tensor* t);              /* ref odyssey.h:66 */
 ody_status ody_tensor_dims(const ody_tensor* t, size_t* rows, size_t* cols); /* :67 */
 ody_status ody_tensor_data(const ody_tensor* t, const float** data);        /* :69 */

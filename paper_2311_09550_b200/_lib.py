@@ -45,6 +45,7 @@ SIGNATURES = {
     "ody_string_free": (None, [c_void_p]),
     "ody_set_threads": (None, [c_int]),
     "ody_tensor_create": (c_int, [c_size_t, c_size_t, POINTER(c_float), POINTER(c_void_p)]),
+    "ody_tensor_create_strided": (c_int, [c_size_t, c_size_t, c_size_t, POINTER(c_float), POINTER(c_void_p)]),
     "ody_tensor_free": (None, [c_void_p]),
     "ody_tensor_dims": (c_int, [c_void_p, POINTER(c_size_t), POINTER(c_size_t)]),
     "ody_tensor_data": (c_int, [c_void_p, POINTER(POINTER(c_float))]),

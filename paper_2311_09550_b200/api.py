@@ -40,11 +40,18 @@ class Tensor:
         if _handle is not None:
             self._h = _handle
             return
-        arr = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+        arr = np.asarray(data, dtype=np.float32)
         if arr.ndim != 2:
             raise ValueError("Tensor expects a 2-D array")
         h = c_void_p()
-        check(lib().ody_tensor_create(arr.shape[0], arr.shape[1], _fptr(arr), byref(h)))
+        if arr.shape[0] > 1 and arr.strides[1] == 4 and arr.strides[0] % 4 == 0 and arr.strides[0] >= 4 * arr.shape[1]:
+            # row-strided (e.g. a column slice): ody_tensor_create_strided copies it straight
+            # into the tensor, no intermediate contiguous copy
+            check(lib().ody_tensor_create_strided(arr.shape[0], arr.shape[1], arr.strides[0] // 4, _fptr(arr),
+                                                  byref(h)))
+        else:
+            arr = np.ascontiguousarray(arr)
+            check(lib().ody_tensor_create(arr.shape[0], arr.shape[1], _fptr(arr), byref(h)))
         self._h = h
 
     @property

@@ -10,7 +10,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -261,6 +265,120 @@ struct ody_qtensor {
 
 namespace {
 
+// Host worker threads for the ABI's host-side copies (ody_tensor_create: the copy of the
+// caller's f32 matrix into pinned memory fused with the reference's finite check).  One
+// thread copies ~12 GB/s; the e2e step's inputs are 0.3-0.9 MB per call.  Workers spin
+// ~200 us after a job before sleeping, so the back-to-back calls of a decode step find them
+// awake.  ody_set_threads(n) sizes the pool (n <= 0: min(8, hardware threads)), as the
+// reference's ody_set_threads sizes its CPU engine's pool (capi.cpp / parallel.cpp).
+class HostPool {
+   public:
+    static HostPool& get() {
+        static HostPool* p = new HostPool();  // never destroyed: workers are detached
+        return *p;
+    }
+    void set_threads(int n) {
+        std::lock_guard<std::mutex> l(dispatch_);
+        want_ = n > 0 ? std::min(n, 64) : 0;
+    }
+    int threads() {
+        const int hw = static_cast<int>(std::thread::hardware_concurrency());
+        return want_ > 0 ? want_ : std::max(1, std::min(8, hw));
+    }
+    // f(i) for i in [0, parts); the caller runs part 0.  Serial when another caller holds
+    // the pool or parts == 1.
+    void parallel(int parts, const std::function<void(int)>& f) {
+        if (parts <= 1) {
+            for (int i = 0; i < parts; ++i) f(i);
+            return;
+        }
+        std::unique_lock<std::mutex> dl(dispatch_, std::try_to_lock);
+        if (!dl.owns_lock()) {
+            for (int i = 0; i < parts; ++i) f(i);
+            return;
+        }
+        grow(parts - 1);
+        const int nw = static_cast<int>(workers_);
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            job_ = &f;
+            parts_ = parts;
+            remaining_.store(nw, std::memory_order_relaxed);
+            gen_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_all();
+        f(0);
+        while (remaining_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+        job_ = nullptr;
+    }
+
+   private:
+    void grow(int n) {
+        while (static_cast<int>(workers_) < n) {
+            const int idx = static_cast<int>(workers_) + 1;
+            const uint64_t seen = gen_.load(std::memory_order_acquire);  // before this dispatch's bump
+            std::thread([this, idx, seen] { loop(idx, seen); }).detach();
+            ++workers_;
+        }
+    }
+    void loop(int idx, uint64_t seen) {
+        for (;;) {
+            const auto t0 = std::chrono::steady_clock::now();
+            uint64_t g;
+            while ((g = gen_.load(std::memory_order_acquire)) == seen) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                    std::unique_lock<std::mutex> l(mu_);
+                    cv_.wait(l, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                }
+            }
+            seen = g;
+            if (idx < parts_) (*job_)(idx);
+            remaining_.fetch_sub(1, std::memory_order_acq_rel);
+        }
+    }
+    std::mutex dispatch_, mu_;
+    std::condition_variable cv_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> remaining_{0};
+    const std::function<void(int)>* job_ = nullptr;
+    int parts_ = 0;
+    size_t workers_ = 0;
+    int want_ = 0;
+};
+
+// rows x cols f32 from `src` (row stride ld elements) into the contiguous `dst`, fused with
+// the finite check (ref tensor.cpp:21-27): one pass over the exponent bits, split over the
+// host pool in >= 128 KiB pieces.  Returns true when every value is finite.
+bool copy_finite(float* dst, const float* src, size_t rows, size_t cols, size_t ld) {
+    const size_t nel = rows * cols;
+    HostPool& pool = HostPool::get();
+    const int parts = static_cast<int>(std::max<size_t>(1, std::min<size_t>(pool.threads(), nel / 32768)));
+    std::vector<uint32_t> bad(parts, 0u);
+    auto piece = [&](int i) {
+        // contiguous: element ranges; strided: row ranges (copied row by row)
+        const size_t units = ld == cols ? nel : rows;
+        const size_t lo = units * i / parts, hi = units * (i + 1) / parts;
+        uint32_t b = 0;
+        auto run = [&](const uint32_t* s, uint32_t* d, size_t n) {
+            for (size_t e = 0; e < n; ++e) {
+                const uint32_t v = s[e];
+                d[e] = v;
+                b |= static_cast<uint32_t>((v & 0x7f800000u) == 0x7f800000u);
+            }
+        };
+        if (ld == cols)
+            run(reinterpret_cast<const uint32_t*>(src) + lo, reinterpret_cast<uint32_t*>(dst) + lo, hi - lo);
+        else
+            for (size_t r = lo; r < hi; ++r)
+                run(reinterpret_cast<const uint32_t*>(src + r * ld), reinterpret_cast<uint32_t*>(dst + r * cols), cols);
+        bad[i] = b;
+    };
+    pool.parallel(parts, piece);
+    uint32_t any = 0;
+    for (uint32_t b : bad) any |= b;
+    return any == 0;
+}
+
 ody_tensor* new_tensor(size_t rows, size_t cols) {
     auto* t = new ody_tensor();
     t->rows = rows;
@@ -485,24 +603,20 @@ const char* ody_last_error(void) { return g_last_error.c_str(); }
 
 void ody_string_free(char* s) { delete[] s; }
 
-void ody_set_threads(int n) { (void)n; }  // no host worker threads on the GPU path
+// ref: ody_set_threads sizes the CPU engine's pool; here the host pool of the ABI's copies
+void ody_set_threads(int n) { HostPool::get().set_threads(n); }
 
 ody_status ody_tensor_create(size_t rows, size_t cols, const float* data, ody_tensor** out) {
+    return ody_tensor_create_strided(rows, cols, cols, data, out);
+}
+
+ody_status ody_tensor_create_strided(size_t rows, size_t cols, size_t ld, const float* data, ody_tensor** out) {
     if (!data || !out) return einval("ody_tensor_create: null argument");
+    if (ld < cols && rows > 1) return einval("ody_tensor_create_strided: ld < cols");
     return guarded([&] {
-        // ref tensor.cpp:21-27 (reject NaN/Inf), fused with the copy into pinned memory:
-        // one vectorizable pass over the exponent bits
+        // ref tensor.cpp:21-27 (reject NaN/Inf), fused with the copy into pinned memory
         ody_tensor* t = new_tensor(rows, cols);
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(data);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(t->data);
-        uint32_t bad = 0;
-        const size_t nel = rows * cols;
-        for (size_t i = 0; i < nel; ++i) {
-            const uint32_t b = src[i];
-            dst[i] = b;
-            bad |= static_cast<uint32_t>((b & 0x7f800000u) == 0x7f800000u);
-        }
-        if (bad) {
+        if (rows * cols > 0 && !copy_finite(t->data, data, rows, cols, rows > 1 ? ld : cols)) {
             delete t;
             fail(ODY_EINVAL, "DenseTensor: non-finite value");
         }
@@ -685,6 +799,38 @@ ody_status ody_gemm(ody_engine engine, const ody_tensor* a_dense, const ody_qten
         std::lock_guard<std::mutex> lock(r.mu);
         cudaStream_t st = r.stream;
         const size_t m = a_q->rows, n = w_q->rows, k = w_q->cols;
+        if (gemm_prequant_eligible(static_cast<int>(m), static_cast<int>(n), static_cast<int>(k))) {
+            // decode widths: the epilogue stores the f32 outputs straight into the result
+            // tensor's pinned (host-mapped) buffer over PCIe while the weights stream -- no
+            // device output buffer and no D2H copy after the kernel
+            ody_tensor* t = new_tensor(m, n);
+            void* mapped = nullptr;
+            if (cudaHostGetDevicePointer(&mapped, t->data, 0) == cudaSuccess && mapped) {
+                cudaError_t e = cudaSuccess;
+                try {
+                    run_gemm(a_q, w_q, static_cast<float*>(mapped), nullptr, st);
+                } catch (...) {
+                    delete t;
+                    throw;
+                }
+                e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) {
+                    delete t;
+                    cuda_check(e, "ody_gemm");
+                }
+                if (counters) {  // ref gemm.cpp:270-272
+                    counters->int8_mac_ops = static_cast<uint64_t>(m) * n * k;
+                    counters->dequant_events = static_cast<uint64_t>(m) * n;
+                    counters->zero_point_sub_ops = 0;
+                    counters->final_scale_ops = static_cast<uint64_t>(m) * n;
+                }
+                *out = t;
+                return;
+            }
+            cudaGetLastError();  // not pinned (pool fell back to pageable memory)
+            delete t;
+        }
         DevBuf<float> od(m * n, st);
         run_gemm(a_q, w_q, od.p, nullptr, st);
         ody_tensor* t = new_tensor(m, n);

@@ -122,3 +122,41 @@ def test_tensor_create_large_copy_and_finite_check():
         with pytest.raises(OdyError) as e:
             api.Tensor(y.reshape(1024, 1000))
         assert e.value.status == 1
+
+
+@pytest.mark.parametrize("threads", [1, 3, 0])
+def test_tensor_create_strided_and_threads(threads):
+    """ody_tensor_create_strided (a column slice, no intermediate copy) == ody_tensor_create
+    of the contiguous copy, for every host-pool size (ody_set_threads); a non-finite value
+    inside the slice is rejected at any position and piece boundary, one in the columns
+    the slice skips is not."""
+    import numpy as np
+
+    from paper_2311_09550_b200 import api
+    from paper_2311_09550_b200._lib import OdyError, lib
+    lib().ody_set_threads(threads)
+    try:
+        big = np.random.default_rng(1).standard_normal((64, 15360), dtype=np.float32)
+        for cols in (5120, 13824, 1, 15360):
+            sl = big[:, :cols]
+            assert np.array_equal(api.Tensor(sl).numpy(), np.ascontiguousarray(sl)), cols
+        sl = big[3:40, 100:6100]
+        assert np.array_equal(api.Tensor(sl).numpy(), np.ascontiguousarray(sl))
+        outside = big.copy()
+        outside[:, 6000] = np.nan  # skipped by the slice
+        assert np.array_equal(api.Tensor(outside[:, :5120]).numpy(), big[:, :5120])
+        for r, c in ((0, 0), (31, 2559), (32, 0), (63, 5119), (17, 4000)):
+            y = big.copy()
+            y[r, c] = np.inf
+            with pytest.raises(OdyError) as e:
+                api.Tensor(y[:, :5120])
+            assert e.value.status == 1, (r, c)
+        flat = np.random.default_rng(2).standard_normal((16, 65536), dtype=np.float32)
+        for pos in (0, 131071, 131072, 16 * 65536 - 1):
+            y = flat.copy().reshape(-1)
+            y[pos] = np.nan
+            with pytest.raises(OdyError):
+                api.Tensor(y.reshape(16, 65536))
+        assert np.array_equal(api.Tensor(flat).numpy(), flat)
+    finally:
+        lib().ody_set_threads(0)

@@ -22,7 +22,7 @@ def measure(threads, iters=30):
         t_step = time.perf_counter()
         for (name, n, k), w in zip(LAYERS, wq):
             t0 = time.perf_counter()
-            hs = np.ascontiguousarray(h[:, :k])
+            hs = h[:, :k]  # row-strided view: ody_tensor_create_strided
             t1 = time.perf_counter()
             t = api.Tensor(hs)
             t2 = time.perf_counter()
@@ -39,6 +39,6 @@ def measure(threads, iters=30):
     return acc, tot
 
 
-for threads in (0, 0):
+for threads in (1, 0, 0):
     acc, tot = measure(threads)
     print(f"threads={threads}: step {tot:7.1f} us  " + "  ".join(f"{k} {v:6.1f}" for k, v in acc.items()))
