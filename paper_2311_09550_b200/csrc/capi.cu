@@ -910,10 +910,25 @@ ody_status ody_dev_w4_quantize(const float* w, size_t n, size_t k, const float* 
     if (!w || !w_packed || !s_w) return einval("ody_dev_w4_quantize: null argument");
     if (n == 0 || k == 0) return einval("quantize_weights: empty tensor");
     return guarded([&] {
-        cuda_check(launch_w4_quant_prepack(w, static_cast<int>(n), static_cast<int>(k), 4, gamma,
-                                           beta, static_cast<uint8_t*>(w_packed), s_w, nullptr,
-                                           static_cast<cudaStream_t>(stream)),
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!gamma && !beta) {
+            cuda_check(launch_w4_quant_prepack(w, static_cast<int>(n), static_cast<int>(k), 4, nullptr, nullptr,
+                                               static_cast<uint8_t*>(w_packed), s_w, nullptr, st),
+                       "w4 quantize launch");
+            return;
+        }
+        // clip factors (device arrays) are validated on the device as the scales are
+        // computed (ref quantize.cpp:22-35 / tensor.cpp:86-110: gamma, beta in (0, 1]);
+        // the offline weight path then synchronizes once to report EINVAL like the reference
+        DevBuf<int> err(1, st);
+        cuda_check(cudaMemsetAsync(err.p, 0, sizeof(int), st), "memset");
+        cuda_check(launch_w4_quant_prepack(w, static_cast<int>(n), static_cast<int>(k), 4, gamma, beta,
+                                           static_cast<uint8_t*>(w_packed), s_w, err.p, st),
                    "w4 quantize launch");
+        int herr = 0;
+        cuda_check(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "ody_dev_w4_quantize");
+        if (herr) fail(ODY_EINVAL, "compute_scale_symmetric: gamma/beta outside (0,1]");
     });
 }
 

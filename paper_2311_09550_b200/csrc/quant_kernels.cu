@@ -175,7 +175,7 @@ __global__ void w_scale_kernel(const float* __restrict__ w, int N, int K, int bi
     if (lane == 0) {
         const float g = gamma ? gamma[row] : 1.0f;
         const float b = beta ? beta[row] : 1.0f;
-        if (!(g > 0.0f && g <= 1.0f && b > 0.0f && b <= 1.0f)) atomicExch(err, 1);
+        if (err && !(g > 0.0f && g <= 1.0f && b > 0.0f && b <= 1.0f)) atomicExch(err, 1);
         const float qmax = static_cast<float>((1 << (bits - 1)) - 1);
         float sc = fmaxf(fabsf(__fmul_rn(g, mx)), fabsf(__fmul_rn(b, mn))) / qmax;
         s[row] = sc > 0.0f ? sc : kMinScale;

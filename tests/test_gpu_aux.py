@@ -139,3 +139,30 @@ def test_matmul_f32_bit_exact_and_capi_agreement(oracle):
     out = api.gemm_w4a8_fast(aq, wq)
     ref = api.matmul_f32(api.dequantize(aq), api.dequantize(wq))
     assert np.all(np.abs(out - ref) <= 1e-4 * np.maximum(1.0, np.abs(ref)))
+
+
+def test_device_w4_quantize_rejects_bad_clip_factors():
+    """ody_dev_w4_quantize with device gamma/beta outside (0, 1] returns EINVAL (as the
+    reference's QuantScheme::validate / compute_scale_symmetric reject them) instead of
+    faulting, and the context stays usable; valid factors give the same scales as the
+    host ABI path."""
+    import torch
+
+    from paper_2311_09550_b200 import api
+    from paper_2311_09550_b200 import device as dev
+    from paper_2311_09550_b200._lib import OdyError
+    rs = np.random.default_rng(11)
+    w = rs.standard_normal((64, 256), dtype=np.float32)
+    wd = torch.from_numpy(w).cuda()
+    for g, b in ((0.0, 1.0), (1.0, 1.5), (-0.5, 0.5), (float("nan"), 1.0)):
+        gd = torch.full((64,), g, device="cuda")
+        bd = torch.full((64,), b, device="cuda")
+        with pytest.raises(OdyError) as e:
+            dev.W4Weight.quantize(wd, gamma=gd, beta=bd)
+        assert e.value.status == 1, (g, b)
+    ok_g = np.linspace(0.5, 1.0, 64, dtype=np.float32)
+    ok_b = np.linspace(1.0, 0.6, 64, dtype=np.float32)
+    q = dev.W4Weight.quantize(wd, gamma=torch.from_numpy(ok_g).cuda(), beta=torch.from_numpy(ok_b).cuda())
+    torch.cuda.synchronize()
+    _, sw = api.quantize_weights(w, clip_gamma=ok_g, clip_beta=ok_b).export()
+    assert np.array_equal(bits_of(q.s.cpu().numpy()), bits_of(sw))

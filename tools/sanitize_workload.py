@@ -5,8 +5,8 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck) runs (GPU box o
 
 Kernels: act_quant_kernel / act_quant_rows_kernel (K1), w_scale + w4_quant_prepack (K2),
 w4a8_gemm_kernel (tile GEMM, decode + stream-K widths), w4a8_prefill_kernel (2-SM),
-w4a8_decode_dyn_kernel (independent program, dependency chain at BN 16/32/64, one-linear
-ody_gemm path), the engine kernels (W8A8 / ASYM / FINE incl. regroup / W4A16), LWC."""
+w4a8_decode_dyn_kernel (independent program, dependency chain at BN 16/32/64 as one program
+and as chain links, one-linear ody_gemm path storing into host-mapped memory), the engine kernels (W8A8 / ASYM / FINE incl. regroup / W4A16), LWC."""
 import sys
 
 import numpy as np
@@ -51,6 +51,10 @@ def main():
                              dev.LinearCall(outs[1], ws[2], outs[2], dep=1),
                              dev.LinearCall(outs[2][:, :640], ws[3], outs[3], dep=2)])
         chain.run(pdl=True)
+        links = dev.Program(chain.calls, links=True)  # the chain as one launch per linear
+        assert links.fused
+        links.run(pdl=True)
+        links.run(pdl=True)
         xs = {kk: (torch.randn((mm, kk), device="cuda") * 2).half() for _, kk in dims}
         ind = dev.Program([dev.LinearCall(xs[kk], wq, torch.empty((mm, nn), dtype=torch.float16, device="cuda"))
                            for (nn, kk), wq in zip(dims, ws)])
