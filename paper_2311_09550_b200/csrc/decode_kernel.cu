@@ -159,6 +159,8 @@ struct PParams {
     int pdl;
     int pf_units;         // L2 prefetch window past the smem ring (units)
     int no_item_pf;       // a dependent item does not L2-prefetch its weights while x is quantized
+    int rest_pf;          // a CTA whose ring filled before griddepcontrol.wait L2-prefetches the
+                          // rest of its first item
     const uint8_t* next_wp;  // cross-kernel hint: L2-prefetch this slice of the next weights
     size_t next_bytes;
     int dbg;              // diagnostics (ODY_DBG_DECODE): 1 store raw x (no quant math), 2 no IEEE redo
@@ -1381,7 +1383,16 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     if (!waited && (p.dbg & 2048)) release_deferred();
                     if (!waited && (p.dbg & 4096) && U + k0 >= 2) release_deferred();
 #endif
-                    if (!waited && U + k0 + 1 >= kDynStages) release_deferred();
+                    if (!waited && U + k0 + 1 >= kDynStages) {
+                        // the ring is full and the B tiles wait on the act quant (i.e. on the
+                        // previous launch): pull the rest of this item into L2 meanwhile
+                        if (p.rest_pf && lane == 0 && k0 + 2 < nunits) {
+                            const int kb_r = x.kb_lo + C::kUB * (k0 + 2);
+                            bulk_prefetch_l2(wtile + static_cast<size_t>(kb_r) * kWBlockBytes,
+                                             static_cast<uint32_t>(x.kb_hi - kb_r) * kWBlockBytes);
+                        }
+                        release_deferred();
+                    }
                     const int k = k0 + lane;
                     {
                         const int Uk = U + k;
@@ -2377,6 +2388,8 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
         p.reset_at_exit = L == 1 ? 0 : 1;
         static const char* pfi_env = ODY_DIAG_ENV("ODY_DYN_PF_ITEMS");  // second-round items to L2
         p.pf_units = pfi_env ? std::atoi(pfi_env) : 0;  // measured: guessing next items costs more
+        static const char* rpf_env = ODY_DIAG_ENV("ODY_REST_PF");  // diagnostics: 1 = on
+        p.rest_pf = (rpf_env && rpf_env[0] == '1') ? 1 : 0;
         p.S = 1;
         p.C = std::min(sms, ib);
         if (plan_log) std::fprintf(stderr, "[ody] dynamic schedule: %d items over %d CTAs\n", ib, p.C);
