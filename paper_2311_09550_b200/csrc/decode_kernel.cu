@@ -1169,8 +1169,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
     uint32_t* emax = tmem_slot + 1;  // [BN] the CTA's per-token max |y| of the current item
     // [2][64] token scales of the item (parity), 16-byte aligned for ld.shared.v4
     float* ssc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(emax + 64) + 15) & ~uintptr_t(15));
+    // [64] the B-quantizers' token row maxima (one global load per token per CTA: the
+    // whole grid reading them per chunk hot-spotted their few L2 lines)
+    uint32_t* qam = reinterpret_cast<uint32_t*>(ssc + 128);
     static_assert((3 * kDynStages + 2 * C::kAStages + 2 * kDBufs + 2 * kItemSlots) * 8 + kItemSlots * 4 + 8 + 64 * 4 +
-                          16 + 128 * 4 <= 2048,
+                          16 + 128 * 4 + 64 * 4 <= 2048,
                   "barrier / item / scale region");
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1518,6 +1521,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                 }
                 if (trc && l < 4) trc[12 + 4 * l] = globaltimer();
             }
+            named_bar_sync(4, 64);  // the producer completed (qt 0 acquired dep_done)
+            if (qt < BN) qam[qt] = qt < d.M ? __ldcg(d.amax_src + qt * kAmaxStride) : 0u;
             named_bar_sync(4, 64);
             // CTA c owns an even share [lo, hi) of the x's kblocks x BN x 8 sixteen-element
             // chunks (a k-block per CTA left most CTAs idle and made the grid wait on the
@@ -1536,7 +1541,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                     const int k0 = kb * kBlockK + c * 16;
                     uint4 v = make_uint4(0u, 0u, 0u, 0u);
                     if (t < d.M && k0 < d.K) {
-                        float sc = __uint_as_float(__ldcg(d.amax_src + t * kAmaxStride)) / 127.0f;
+                        float sc = __uint_as_float(qam[t]) / 127.0f;
                         if (!(sc > 0.0f)) sc = kMinScale;
                         const unsigned short* row = static_cast<const unsigned short*>(d.x) + static_cast<size_t>(t) * d.ldx;
                         uint4 r0, r1;
@@ -1556,6 +1561,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
                         }
                         v = d.x_bf16 ? quant16<true>(r0, r1, sc, 1.0f / sc, 0) : quant16<false>(r0, r1, sc, 1.0f / sc, 0);
                     }
+                    if (trc && p.L == 1 && qt == 0 && u == 0 && task0 == lo) trc[14] = globaltimer() + (v.x == 0x7fffffffu);
                     *reinterpret_cast<uint4*>(const_cast<int8_t*>(d.qa) + static_cast<size_t>(kb) * BN * 128 + t * 128 +
                                               ((c ^ (t & 7)) << 4)) = v;
                 }
@@ -1565,7 +1571,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             // after its acquire of qdone with fence.proxy.async (the `released` check); the
             // release below publishes these generic stores at gpu scope.  Every CTA counts
             // once (qtarget = the grid).
+            if (trc && p.L == 1 && qt == 0) trc[15] = globaltimer();
             named_bar_sync(4, 64);
+            if (trc && p.L == 1 && qt == 0) trc[16] = globaltimer();
             if (qt == 0) red_release_add_u32(d.qdone, 1u);
             if (trc && qt == 0 && l < 4) trc[13 + 4 * l] = globaltimer();
         }

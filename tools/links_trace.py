@@ -51,8 +51,8 @@ def st(a):
     return f"{f(np.median(a)):6.2f}/{f(a.max()):6.2f}" if len(a) else "     -/     -"
 
 
-print("med/max us:   entry         pdl_wait      quant start   qdone rel     qdone acq     first B       "
-      "first MMA     last epi      exit")
+print("med/max us:   entry         pdl_wait      quant start   chunk0 quant  quant done    bar done      "
+      "qdone rel     qdone acq     first B       first MMA     last epi      exit")
 for (name, _, _), tt in zip(bench.LAYERS, t):
     v = tt[tt[:, 0] > 0]
-    print(f"{name:8s} {len(v):3d} " + "  ".join(st(v[:, c]) for c in (0, 8, 12, 13, 26, 9, 10, 11, 5)))
+    print(f"{name:8s} {len(v):3d} " + "  ".join(st(v[:, c]) for c in (0, 8, 12, 14, 15, 16, 13, 26, 9, 10, 11, 5)))
