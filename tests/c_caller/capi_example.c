@@ -49,7 +49,16 @@ int main(int argc, char** argv) {
     CHECK(ody_tensor_dims(t, &r, &c) == ODY_OK && r == 2 && c == 3);
     CHECK(ody_tensor_data(t, &d) == ODY_OK && d[5] == 6.0f);
     ody_tensor_free(t);
-    ody_set_threads(8); /* accepted, no host workers */
+    ody_set_threads(8); /* the host pool of the ABI's host copies */
+    /* extension: a column slice [:, 1:3] of the 2 x 3 matrix, no intermediate copy */
+    CHECK(ody_tensor_create_strided(2, 2, 3, good + 1, &t) == ODY_OK);
+    CHECK(ody_tensor_data(t, &d) == ODY_OK && d[0] == 2.0f && d[1] == 3.0f && d[2] == 5.0f && d[3] == 6.0f);
+    ody_tensor_free(t);
+    const float bad_outside[6] = {NAN, 2, 3, NAN, 5, 6}; /* NaN only in the skipped column */
+    CHECK(ody_tensor_create_strided(2, 2, 3, bad_outside + 1, &t) == ODY_OK);
+    ody_tensor_free(t);
+    CHECK(ody_tensor_create_strided(2, 2, 3, bad_outside, &t) == ODY_EINVAL);
+    ody_set_threads(0);
     if (link_only) {
         printf(failures ? "FAILED\n" : "capi_example (link-only): ok\n");
         return failures ? 1 : 0;
