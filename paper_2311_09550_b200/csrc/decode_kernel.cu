@@ -130,8 +130,8 @@ struct LinDesc {
                           // amax_dst; a chain link launch: the amax_src its x was quantized with)
 };
 
-constexpr int kRowThreads = 256;
-constexpr int kRowChunks = 4;  // K <= 256 * 4 * 16 = 16384
+constexpr int kRowThreads = 1024;  // one 16-element chunk per thread: the row quantizes in one pass
+constexpr int kRowChunks = 1;  // K <= 1024 * 16 = 16384
 struct RowBatch {
     const unsigned short* x[kMaxLin];
     size_t ldx[kMaxLin];
@@ -140,6 +140,7 @@ struct RowBatch {
     float* s[kMaxLin];
     const float* amax_in[kMaxLin];  // optional row max override (row-parallel TP: all-reduced max)
     int n, pdl;
+    unsigned long long* trace;  // diagnostics: [cta][entry, griddepcontrol.wait returned, done, -]
 };
 
 struct PParams {
@@ -1009,10 +1010,29 @@ struct DynCfg {
 // 16-token item on the critical path of every linear).  ODT -1: int32 pre-shift
 // accumulators (acc_out).  AMX: also reduce max |stored value| per token into the CTA's
 // smem maxima (the dependent linear's x scale).
+// One row-batch entry's fields, read from the kernel parameters ONCE (and kept in
+// registers: a parameter indexed by a run-time entry number compiles to an indexed
+// constant load, whose cold miss costs ~0.3 us on a fresh SM -- measured, several of them
+// serialised were most of the act quant's run time after its loads landed).
+struct RowArgs {
+    const unsigned short* x;
+    size_t ldx;
+    int K, Mp;
+    int8_t* q;
+    float* s;
+    const float* amax_in;
+};
+__device__ __forceinline__ size_t ld_keep_u64(size_t v) {
+    unsigned long long r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(static_cast<unsigned long long>(v)));
+    return static_cast<size_t>(r);
+}
+
 template <bool BF16>
-__device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float* red) {
-    const unsigned short* row = b.x[i] + static_cast<size_t>(t) * b.ldx[i];
-    const int K = b.K[i];
+__device__ __forceinline__ void quant_row(const RowArgs& ra, int t, float* red, bool dry,
+                                          unsigned long long* trc = nullptr) {
+    const unsigned short* row = ra.x + static_cast<size_t>(t) * ra.ldx;
+    const int K = ra.K;
     const int nch = static_cast<int>(pad_k(K) / 16);
     uint4 raw[kRowChunks][2];
     uint32_t mb = 0u;
@@ -1028,14 +1048,15 @@ __device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float
     for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
     if ((threadIdx.x & 31) == 0) reinterpret_cast<uint32_t*>(red)[threadIdx.x >> 5] = mb;
     __syncthreads();
+    if (trc && !dry && threadIdx.x == 0) trc[3] = globaltimer();  // every load of the row landed
     uint32_t m = 0u;
 #pragma unroll
     for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
-    if (b.amax_in[i]) m = __float_as_uint(b.amax_in[i][t]);  // the global max of a K-sharded row
+    if (ra.amax_in) m = __float_as_uint(ra.amax_in[t]);  // the global max of a K-sharded row
     float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
     if (!(sc > 0.0f)) sc = kMinScale;
     const float rcp = 1.0f / sc;
-    if (threadIdx.x == 0) b.s[i][t] = sc;
+    if (threadIdx.x == 0 && !dry) ra.s[t] = sc;
     uint4 qv[kRowChunks];
     bool ok[kRowChunks];
 #pragma unroll
@@ -1045,27 +1066,55 @@ __device__ __forceinline__ void quant_row(const RowBatch& b, int i, int t, float
         const int c = threadIdx.x + j * kRowThreads;
         if (c < nch) {
             if (!ok[j]) qv[j] = fix16(qv[j], raw[j][0], raw[j][1], sc, rcp, BF16);
-            *reinterpret_cast<uint4*>(b.q[i] + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, b.Mp[i])) = qv[j];
+            if (!dry)
+                *reinterpret_cast<uint4*>(ra.q + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16,
+                                                           ra.Mp)) = qv[j];
         }
     }
 }
 
 __device__ __forceinline__ void act_quant_rows_body(const RowBatch& b) {
-    if (b.pdl) {
-        pdl_launch_dependents();
-        pdl_wait();
-    }
+    unsigned long long* trc = (b.trace && blockIdx.x < 128) ? b.trace + 4 * blockIdx.x : nullptr;
+    if (trc && threadIdx.x == 0) trc[0] = globaltimer();
+    if (b.pdl) pdl_launch_dependents();
     __shared__ float red[kRowThreads / 32];
     int i = 0, t = blockIdx.x;
     while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
-    if (b.bf16[i])
-        quant_row<true>(b, i, t, red);
-    else
-        quant_row<false>(b, i, t, red);
+    // Under PDL the CTA is resident long before its input exists: pass 0 runs the whole
+    // row quantization dry (x as it is now, no stores) so its instructions are fetched
+    // into the SM's instruction cache while waiting; the real pass then runs warm.  Cold
+    // fetch of this straight-line code measured 1.5-3 us per launch (trace marks), most
+    // of the act quant's time between two dependent linears.  One copy of the code
+    // (`unroll 1`): the dry pass must warm the very instructions the real pass runs.
+    RowArgs ra;
+    ra.x = ld_keep_ptr(b.x[i]);
+    ra.ldx = ld_keep_u64(b.ldx[i]);
+    ra.K = ld_keep(b.K[i]);
+    ra.Mp = ld_keep(b.Mp[i]);
+    ra.q = ld_keep_ptr(b.q[i]);
+    ra.s = ld_keep_ptr(b.s[i]);
+    ra.amax_in = ld_keep_ptr(b.amax_in[i]);
+    const int bf16 = ld_keep(b.bf16[i]);
+    const int pdl = ld_keep(b.pdl);
+#pragma unroll 1
+    for (int pass = pdl ? 0 : 1; pass < 2; ++pass) {
+        if (pass == 1) {
+            if (pdl) pdl_wait();
+            if (trc && threadIdx.x == 0) trc[1] = globaltimer();
+        }
+        if (bf16)
+            quant_row<true>(ra, t, red, pass == 0, trc);
+        else
+            quant_row<false>(ra, t, red, pass == 0, trc);
+    }
+    if (trc) {
+        __syncthreads();
+        if (threadIdx.x == 0) trc[2] = globaltimer();
+    }
 }
 
 
-__global__ void __launch_bounds__(kRowThreads, 4) act_quant_rows_kernel(const __grid_constant__ RowBatch b) {
+__global__ void __launch_bounds__(kRowThreads, 1) act_quant_rows_kernel(const __grid_constant__ RowBatch b) {
     act_quant_rows_body(b);
 }
 
@@ -1848,6 +1897,14 @@ cudaError_t ensure_dyn_attr() {
 // rb != NULL: first the batched activation quant (rb_rows token rows, act_quant_rows_kernel),
 // then the GEMM, PDL-chained.  (Measured: the same act quant as a mode of this kernel
 // function -- warm instruction caches for the GEMM launch -- made no difference.)
+// Dynamic shared memory the act-quant kernel reserves so it never shares an SM with a
+// decode CTA (launch_dyn); diagnostics: ODY_ACT_SMEM overrides (0 = co-reside).
+size_t act_excl_smem() {
+    static const char* env = ODY_DIAG_ENV("ODY_ACT_SMEM");
+    static const size_t v = env ? static_cast<size_t>(std::atoi(env)) : 0;
+    return v;
+}
+
 template <int BN, bool DEP, int UB>
 cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st, const RowBatch* rb = nullptr, int rb_rows = 0) {
     const cudaError_t ed = ensure_dyn_attr<BN, DEP, UB>();
@@ -1857,6 +1914,10 @@ cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st, const RowBat
         acfg.gridDim = dim3(rb_rows);
         acfg.blockDim = dim3(kRowThreads);
         acfg.stream = st;
+        // Keep the act quant off SMs that hold a decode CTA: its x loads would queue behind
+        // that CTA's ring fill (~160 KiB per SM at the SM's HBM share: ~3.6 us).  Reserving
+        // more shared memory than a decode CTA leaves free places it on idle SMs only.
+        acfg.dynamicSmemBytes = act_excl_smem();
         cudaLaunchAttribute aattr;
         aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
         aattr.val.programmaticStreamSerializationAllowed = 1;
@@ -2254,6 +2315,7 @@ cudaError_t launch_w4a8_program(const LinearArgs* a, const int* deps, int L, voi
             }
             rb.n = nb;
             rb.pdl = pdl ? 1 : 0;
+            rb.trace = a[0].trace ? a[0].trace + 148 * kTraceCta + 512 : nullptr;
             // launched right before the GEMM below (launch_dyn)
             rb_pending = rb;
             rb_rows = rows;

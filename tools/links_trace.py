@@ -56,3 +56,15 @@ print("med/max us:   entry         pdl_wait      quant start   chunk0 quant  qua
 for (name, _, _), tt in zip(bench.LAYERS, t):
     v = tt[tt[:, 0] > 0]
     print(f"{name:8s} {len(v):3d} " + "  ".join(st(v[:, c]) for c in (0, 8, 12, 14, 15, 16, 13, 26, 9, 10, 11, 5)))
+
+if not links:
+    print("act quant before each launch (16 CTAs): entry / griddepcontrol.wait returned / loads landed / done, med/max us")
+    for i, (name, _, _) in enumerate(bench.LAYERS):
+        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 4 * 128].view(128, 4).cpu().numpy()
+        a = a[3:16]  # CTAs 0-2's slots overlap another trace region
+        a = a[a[:, 0] > 0]
+        print(f"{name:8s} {len(a):3d} " + "  ".join(st(a[:, c]) for c in (0, 1, 3, 2)))
+if not links and len(sys.argv) > 3:
+    for i, (name, _, _) in enumerate(bench.LAYERS):
+        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 4 * 128].view(128, 4).cpu().numpy()
+        print(name, [(round(f(r[0]), 2), round(f(r[1]), 2), round(f(r[2]), 2)) for r in a[a[:, 0] > 0]])
