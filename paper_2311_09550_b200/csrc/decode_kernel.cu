@@ -1049,18 +1049,24 @@ __device__ __forceinline__ void quant_row(const RowArgs& ra, int t, float* red, 
     if ((threadIdx.x & 31) == 0) reinterpret_cast<uint32_t*>(red)[threadIdx.x >> 5] = mb;
     __syncthreads();
     if (trc && !dry && threadIdx.x == 0) trc[3] = globaltimer();  // every load of the row landed
-    uint32_t m = 0u;
+    // the CTA max: one shared load per lane + a shuffle tree (32 dependent shared loads
+    // per thread measured ~0.5 us)
+    const int lane = threadIdx.x & 31;
+    uint32_t m = lane < kRowThreads / 32 ? reinterpret_cast<uint32_t*>(red)[lane] : 0u;
 #pragma unroll
-    for (int w = 0; w < kRowThreads / 32; ++w) m = max(m, reinterpret_cast<uint32_t*>(red)[w]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (ra.amax_in) m = __float_as_uint(ra.amax_in[t]);  // the global max of a K-sharded row
+    if (trc && !dry && threadIdx.x == 0) trc[4] = globaltimer() + (m == 0x7fffffffu);  // row max
     float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
     if (!(sc > 0.0f)) sc = kMinScale;
     const float rcp = 1.0f / sc;
+    if (trc && !dry && threadIdx.x == 0) trc[5] = globaltimer() + (rcp == 3.0f);  // scale
     if (threadIdx.x == 0 && !dry) ra.s[t] = sc;
     uint4 qv[kRowChunks];
     bool ok[kRowChunks];
 #pragma unroll
     for (int j = 0; j < kRowChunks; ++j) qv[j] = quant16_fast<BF16>(raw[j][0], raw[j][1], rcp, ok[j]);
+    if (trc && !dry && threadIdx.x == 0) trc[6] = globaltimer() + (qv[0].x == 0x7fffffffu);  // codes
 #pragma unroll
     for (int j = 0; j < kRowChunks; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
@@ -1074,7 +1080,7 @@ __device__ __forceinline__ void quant_row(const RowArgs& ra, int t, float* red, 
 }
 
 __device__ __forceinline__ void act_quant_rows_body(const RowBatch& b) {
-    unsigned long long* trc = (b.trace && blockIdx.x < 128) ? b.trace + 4 * blockIdx.x : nullptr;
+    unsigned long long* trc = (b.trace && blockIdx.x < 64) ? b.trace + 8 * blockIdx.x : nullptr;
     if (trc && threadIdx.x == 0) trc[0] = globaltimer();
     if (b.pdl) pdl_launch_dependents();
     __shared__ float red[kRowThreads / 32];

@@ -58,13 +58,13 @@ for (name, _, _), tt in zip(bench.LAYERS, t):
     print(f"{name:8s} {len(v):3d} " + "  ".join(st(v[:, c]) for c in (0, 8, 12, 14, 15, 16, 13, 26, 9, 10, 11, 5)))
 
 if not links:
-    print("act quant before each launch (16 CTAs): entry / griddepcontrol.wait returned / loads landed / done, med/max us")
+    print("act quant (16 CTAs): entry / wait returned / loads landed / row max / scale / codes / done, med/max us")
     for i, (name, _, _) in enumerate(bench.LAYERS):
-        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 4 * 128].view(128, 4).cpu().numpy()
-        a = a[3:16]  # CTAs 0-2's slots overlap another trace region
+        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 8 * 64].view(64, 8).cpu().numpy()
+        a = a[3:16]  # CTAs 0-2's slots overlap another trace region (8 slots per CTA)
         a = a[a[:, 0] > 0]
-        print(f"{name:8s} {len(a):3d} " + "  ".join(st(a[:, c]) for c in (0, 1, 3, 2)))
+        print(f"{name:8s} {len(a):3d} " + "  ".join(st(a[:, c]) for c in (0, 1, 3, 4, 5, 6, 2)))
 if not links and len(sys.argv) > 3:
     for i, (name, _, _) in enumerate(bench.LAYERS):
-        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 4 * 128].view(128, 4).cpu().numpy()
+        a = buf[i * blk + 148 * 32 + 512:i * blk + 148 * 32 + 512 + 8 * 64].view(64, 8).cpu().numpy()
         print(name, [(round(f(r[0]), 2), round(f(r[1]), 2), round(f(r[2]), 2)) for r in a[a[:, 0] > 0]])
