@@ -418,9 +418,9 @@ def roofline(args, dev, h, stream):
             "chain_links": {"us": round(ms_links * 1e3, 3),
                             "GB/s": round(step_bytes(m) / (ms_links * 1e-3) / 1e9, 1),
                             "frac": round(step_bytes(m) / (ms_links * 1e-3) / 1e9 / hbm, 4),
-                            "note": "the same dependent layer as one launch per linear with each dependent x "
-                                    "quantized in-kernel from the producer launch's row maxima "
-                                    "(ody_dev_w4a8_linear_chain: one act-quant kernel per layer), PDL"},
+                            "note": "the same dependent layer as one launch per linear, each dependent x "
+                                    "quantized from the row maxima its producer launch's epilogues "
+                                    "accumulated (ody_dev_w4a8_linear_chain, act_quant_premax_kernel), PDL"},
             "independent_linears_program": {"us": round(ms_ind * 1e3, 3),
                                             "GB/s": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9, 1),
                                             "frac": round(step_bytes(m) / (ms_ind * 1e-3) / 1e9 / hbm, 4),

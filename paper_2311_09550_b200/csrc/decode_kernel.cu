@@ -128,6 +128,8 @@ struct LinDesc {
     uint32_t qtarget;     //   complete at kblocks
     uint32_t* amax_reset; // row maxima this launch's last CTA re-zeroes (the chain program: its
                           // amax_dst; a chain link launch: the amax_src its x was quantized with)
+    uint32_t* amax_zero;  // chain link: the row maxima its act quant consumed, re-zeroed by CTA 0
+                          // once griddepcontrol.wait returned (the act quant completed)
 };
 
 constexpr int kRowThreads = 1024;  // one 16-element chunk per thread: the row quantizes in one pass
@@ -141,6 +143,7 @@ struct RowBatch {
     const float* amax_in[kMaxLin];  // optional row max override (row-parallel TP: all-reduced max)
     int n, pdl;
     unsigned long long* trace;  // diagnostics: [cta][entry, griddepcontrol.wait returned, done, -]
+    const uint32_t* amax_src[kMaxLin];  // act_quant_premax_kernel: the producer's per-token maxima
 };
 
 struct PParams {
@@ -1124,6 +1127,49 @@ __global__ void __launch_bounds__(kRowThreads, 1) act_quant_rows_kernel(const __
     act_quant_rows_body(b);
 }
 
+// K1 of a dependent chain link: the token row maxima come from the producer launch's
+// epilogues (per-token atomicMax of the stored |y|, f32 bits -- the same value the row
+// reduction would find), so a row needs no reduction and is spread over kPreCtas CTAs of
+// 256 threads, one 16-element chunk per thread.  Bit-exact with act_quant_rows_kernel.
+constexpr int kPreCtas = 4;
+constexpr int kPreThreads = 256;
+static_assert(kPreCtas * kPreThreads * 16 >= kRowThreads * kRowChunks * 16, "premax covers every external K");
+__global__ void __launch_bounds__(kPreThreads, 4) act_quant_premax_kernel(const __grid_constant__ RowBatch b) {
+    if (b.pdl) pdl_launch_dependents();
+    int i = 0, t = blockIdx.x / kPreCtas;
+    const int part = blockIdx.x % kPreCtas;
+    while (i + 1 < b.n && t >= b.M[i]) t -= b.M[i++];
+    const unsigned short* row = ld_keep_ptr(b.x[i]) + static_cast<size_t>(t) * ld_keep_u64(b.ldx[i]);
+    const int K = ld_keep(b.K[i]);
+    const int Mp = ld_keep(b.Mp[i]);
+    int8_t* const q = ld_keep_ptr(b.q[i]);
+    float* const s = ld_keep_ptr(b.s[i]);
+    const uint32_t* const am = ld_keep_ptr(b.amax_src[i]);
+    const int bf16 = ld_keep(b.bf16[i]);
+    const int pdl = ld_keep(b.pdl);
+    const int nch = static_cast<int>(pad_k(K) / 16);
+    const int c = part * kPreThreads + threadIdx.x;
+    // pass 0 runs dry before griddepcontrol.wait (warm instruction / constant caches)
+#pragma unroll 1
+    for (int pass = pdl ? 0 : 1; pass < 2; ++pass) {
+        if (pass == 1 && pdl) pdl_wait();
+        const bool dry = pass == 0;
+        const uint32_t m = __ldcg(am + t * kAmaxStride);
+        float sc = __uint_as_float(m) / 127.0f;  // ref quantize.cpp:22-35 (IEEE division)
+        if (!(sc > 0.0f)) sc = kMinScale;
+        const float rcp = 1.0f / sc;
+        if (threadIdx.x == 0 && part == 0 && !dry) s[t] = sc;
+        if (c < nch) {
+            uint4 r0, r1;
+            load16_raw(row, c * 16, K, true, r0, r1);
+            bool ok;
+            uint4 v = bf16 ? quant16_fast<true>(r0, r1, rcp, ok) : quant16_fast<false>(r0, r1, rcp, ok);
+            if (!ok || dry) v = fix16(v, r0, r1, sc, rcp, bf16 != 0);
+            if (!dry) *reinterpret_cast<uint4*>(q + a8_offset(static_cast<size_t>(t), static_cast<size_t>(c) * 16, Mp)) = v;
+        }
+    }
+}
+
 template <int BN, int ODT, bool AMX>
 __device__ __forceinline__ void epi_store(const uint32_t (&v)[BN], const float* tsc, float sw_n, int m_rows,
                                           int n_cols, int n, bool own, bool amx, void* outv, uint32_t emax_a,
@@ -1554,6 +1600,13 @@ __global__ void __launch_bounds__(kDynThreads, 1) w4a8_decode_dyn_kernel(const _
             }
             ++JD;
         }
+    } else if (!DEP && warp == kWarpAlloc + 1) {
+        // chain link: re-zero the row maxima this launch's act quant consumed (it completed:
+        // griddepcontrol.wait) before the producer of the next step accumulates into them
+        if (blockIdx.x == 0 && p.lin[0].amax_zero) {
+            if (p.pdl) pdl_wait();
+            for (int t = lane; t < p.lin[0].M; t += 32) p.lin[0].amax_zero[t * kAmaxStride] = 0u;
+        }
     } else if (DEP && (warp == kWarpAlloc || warp == kWarpAlloc + 1)) {
         // B-quantizer (warps 2-3, idle once TMEM is allocated).  A DEPENDENT linear's x
         // is an earlier linear's 16-bit output.  Once that linear completed, x is
@@ -1911,6 +1964,19 @@ size_t act_excl_smem() {
     return v;
 }
 
+cudaError_t launch_premax(const RowBatch& rb, int rows, cudaStream_t st) {
+    cudaLaunchConfig_t acfg = {};
+    acfg.gridDim = dim3(rows * kPreCtas);
+    acfg.blockDim = dim3(kPreThreads);
+    acfg.stream = st;
+    cudaLaunchAttribute aattr;
+    aattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    aattr.val.programmaticStreamSerializationAllowed = 1;
+    acfg.attrs = &aattr;
+    acfg.numAttrs = rb.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&acfg, act_quant_premax_kernel, rb);
+}
+
 template <int BN, bool DEP, int UB>
 cudaError_t launch_dyn(const PParams& p, bool pdl, cudaStream_t st, const RowBatch* rb = nullptr, int rb_rows = 0) {
     const cudaError_t ed = ensure_dyn_attr<BN, DEP, UB>();
@@ -2209,8 +2275,8 @@ size_t program_scratch_bytes(const LinearArgs* a, const int* deps, int L) {
     for (int l = 0; l < L; ++l) {
         if (!deps || deps[l] < 0)
             b += round_up(a8_bytes(a[l].M, a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
-        else  // dependency chain: the grid-wide quantized x (compact a8, BN rows)
-            b += round_up(static_cast<size_t>(dyn_bn(mmax)) * pad_k(a[l].K), 256);
+        else  // dependency chain: the quantized x (compact a8, BN rows) + its token scales
+            b += round_up(static_cast<size_t>(dyn_bn(mmax)) * pad_k(a[l].K), 256) + round_up(pad_m(a[l].M) * 4, 256);
     }
     return b;
 }
@@ -2529,7 +2595,6 @@ cudaError_t launch_w4a8_chain_links(const LinearArgs* a, const int* deps, int L,
     for (int l = 0; l < L; ++l) mmax = std::max(mmax, a[l].M);
     const int bn = dyn_bn(mmax);
     uint32_t* counters = static_cast<uint32_t*>(scratch);
-    uint32_t* qdone = counters + kChainDoneU32 + kMaxLin;
     uint32_t* amax = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + kChainAmaxOffset);
     uint8_t* cursor = static_cast<uint8_t*>(scratch) + kZeroRegion + dyn_items(a, L) * bn * kTileN * 4;
     int consumer[kMaxLin];
@@ -2577,14 +2642,29 @@ cudaError_t launch_w4a8_chain_links(const LinearArgs* a, const int* deps, int L,
             rb.n = 1;
             rb.pdl = (pdl || l > 0) ? 1 : 0;
         } else {
-            d.qa = reinterpret_cast<const int8_t*>(cursor);
+            // the act quant reads the row maxima the producer launch's epilogues accumulated
+            // (act_quant_premax_kernel: no row reduction, 4 CTAs per token row); this
+            // launch's CTA 0 re-zeroes them after its griddepcontrol.wait
+            int8_t* q = reinterpret_cast<int8_t*>(cursor);
             cursor += round_up(static_cast<size_t>(bn) * pad_k(d.K), 256);
+            float* sa = a[l].sa_out ? a[l].sa_out : reinterpret_cast<float*>(cursor);
+            cursor += round_up(pad_m(d.M) * 4, 256);
+            d.qa = q;
+            d.sa = sa;
             d.Mp = bn;
-            d.qdone = qdone + l;
-            d.dep_done = d.qdone;  // satisfied at once (dep_target 0): griddepcontrol.wait orders
-            d.dep_target = 0;      //   this launch after its producer's
-            d.amax_src = amax + deps[l] * kChainMaxM * kAmaxStride;
-            d.amax_reset = const_cast<uint32_t*>(d.amax_src);
+            uint32_t* src = amax + deps[l] * kChainMaxM * kAmaxStride;
+            d.amax_zero = src;
+            rb.x[0] = static_cast<const unsigned short*>(a[l].x);
+            rb.ldx[0] = a[l].ldx;
+            rb.M[0] = d.M;
+            rb.K[0] = d.K;
+            rb.Mp[0] = bn;
+            rb.bf16[0] = d.x_bf16;
+            rb.q[0] = q;
+            rb.s[0] = sa;
+            rb.amax_src[0] = src;
+            rb.n = 1;
+            rb.pdl = 1;
         }
         if (consumer[l] >= 0) {
             int c0 = 0;
@@ -2601,33 +2681,21 @@ cudaError_t launch_w4a8_chain_links(const LinearArgs* a, const int* deps, int L,
         p.part = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + kZeroRegion);
         p.S = 1;
         p.C = std::min(sms, p.n_items);
-        if (dep) d.qtarget = static_cast<uint32_t>(p.C);  // every CTA quantizes a share of x
-        // the whole-item L2 prefetch while x is quantized floods the memory queues the
-        // quantizers' loads wait in (their round trip is this launch's critical path)
-        static const char* lpf_env = ODY_DIAG_ENV("ODY_LINKS_ITEM_PF");  // diagnostics: 1 = on
-        p.no_item_pf = (lpf_env && lpf_env[0] == '1') ? 0 : 1;
         p.chain_static = 1;
-        p.reset_at_exit = dep ? 1 : 0;  // qdone + the consumed row maxima
-        // a link after the first always waits on the previous launch in-kernel (PDL)
-        const bool lpdl = pdl || l > 0;
-        p.pdl = (lpdl || !dep) ? 1 : 0;  // an external link overlaps its act quant
+        p.reset_at_exit = 0;  // static deal, nothing to re-arm
+        p.pdl = 1;            // every link overlaps its act quant
         // diagnostics: one trace block per link (the per-CTA slots + the last CTA's units)
         p.trace = a[l].trace ? a[l].trace + static_cast<size_t>(l) * (148 * kTraceCta + 1536) : nullptr;
         cudaError_t e = cudaSuccess;
         const RowBatch* rbp = dep ? nullptr : &rb;  // lin_ok: an external K fits the row kernel
-        const bool kpdl = p.pdl != 0;
         if (dep) {
-            switch (bn) {
-                case 16: e = launch_dyn<16, true, 4>(p, kpdl, st); break;
-                case 32: e = launch_dyn<32, true, 4>(p, kpdl, st); break;
-                default: e = launch_dyn<64, true, 4>(p, kpdl, st); break;
-            }
-        } else {
-            switch (bn) {
-                case 16: e = launch_dyn<16, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
-                case 32: e = launch_dyn<32, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
-                default: e = launch_dyn<64, false, 4>(p, kpdl, st, rbp, rbp ? d.M : 0); break;
-            }
+            e = launch_premax(rb, d.M, st);
+            if (e != cudaSuccess) return e;
+        }
+        switch (bn) {
+            case 16: e = launch_dyn<16, false, 4>(p, true, st, rbp, rbp ? d.M : 0); break;
+            case 32: e = launch_dyn<32, false, 4>(p, true, st, rbp, rbp ? d.M : 0); break;
+            default: e = launch_dyn<64, false, 4>(p, true, st, rbp, rbp ? d.M : 0); break;
         }
         if (e != cudaSuccess) return e;
     }
