@@ -234,9 +234,9 @@ ody_status ody_dev_w4a8_linear_program(const ody_linear_desc* lin, int count, vo
                                        size_t workspace_bytes, int max_ctas, int pdl,
                                        const void* next_w, size_t next_w_bytes, void* stream);
 /* A dependency chain (deps set as for a program) run as ONE LAUNCH PER LINEAR: a dependent
- * linear's launch quantizes its x in-kernel from the per-token row maxima its producer
- * launch's epilogues accumulated (no act-quant kernel between two linears); external
- * linears keep the act-quant kernel.  Eligible (ody_dev_chain_is_links) when every dependent
+ * linear's x is quantized from the per-token row maxima its producer launch's epilogues
+ * accumulated (a reduction-free act quant spread over 4 CTAs per token row); external
+ * linears keep the row-reducing act-quant kernel.  Eligible (ody_dev_chain_is_links) when every dependent
  * x is a column slice of its producer's 16-bit output and m <= 64; otherwise it runs as
  * ody_dev_w4a8_linear_program.  Results are identical to the program's.  Same workspace
  * (ody_dev_program_workspace_bytes, zeroed once, left zeroed). */
